@@ -1,0 +1,177 @@
+/*
+ * fracinv_b200.h — C-ABI of the B200-native preconditioned-GMRES path for the
+ * all-at-once space-time system of arXiv 2507.02809 (reference library "fracinv").
+ *
+ * Plain C: opaque handles, plain pointers and sizes, integer status codes.  No C++
+ * exceptions and no torch types cross this boundary.  Every entry point names the
+ * reference interface it replaces (paths relative to /root/reference/proj).
+ *
+ * Vector layout at the boundary is the reference's (system.cpp:154-157): a stacked
+ * block vector of length (S+1)*N, block s (1-based) at offset (s-1)*N, the source
+ * block f last.  Device pointers ("*_dev") are CUDA global-memory pointers on the
+ * context's device; host pointers ("*_host") are ordinary host memory.  Internally
+ * the library keeps a padded level-major layout.
+ *
+ * Threading: one CUDA stream per fi_ctx; a context and the objects created from it
+ * must not be used from two host threads at once without external locking (the
+ * reference's "independent workspaces" rule, toeplitz.hpp:20-22).  Objects are
+ * immutable after creation.
+ */
+#ifndef FRACINV_B200_H
+#define FRACINV_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. Mapping to the reference's exception taxonomy (errors.hpp:9-43):
+ *   FI_E_DIM       DimensionError
+ *   FI_E_RESOURCE  ResourceLimitError (block cap, device memory)
+ *   FI_E_SINGULAR  SingularBlockError (time index via fi_last_error_time_index)
+ *   FI_E_DOMAIN    std::domain_error (invalid parameters)
+ *   FI_E_CUDA      CUDA runtime failure / no device
+ *   FI_E_NOCONV    reserved (non-convergence is reported in fi_gmres_report, not as an error)
+ *   FI_E_CONFIG    ConfigError
+ */
+enum {
+    FI_OK = 0,
+    FI_E_DIM = 1,
+    FI_E_RESOURCE = 2,
+    FI_E_SINGULAR = 3,
+    FI_E_DOMAIN = 4,
+    FI_E_CUDA = 5,
+    FI_E_NOCONV = 6,
+    FI_E_CONFIG = 7
+};
+
+typedef struct fi_ctx fi_ctx;
+typedef struct fi_system fi_system;
+typedef struct fi_precond fi_precond;
+
+/* ------------------------------------------------------------------ context / errors */
+int fi_ctx_create(int device, fi_ctx** out);
+void fi_ctx_destroy(fi_ctx* ctx);
+/* cudaStream_t of the context (all work is enqueued on it). */
+void* fi_ctx_stream(fi_ctx* ctx);
+int fi_ctx_synchronize(fi_ctx* ctx);
+/* Message of the last failing call on this host thread. */
+const char* fi_last_error(void);
+/* SingularBlockError::time_index (errors.hpp:22-30): 1-based level, S+1 = f-block. */
+int fi_last_error_time_index(void);
+/* Number of this library's kernels launched on `ctx` since creation (launch accounting). */
+long long fi_ctx_kernel_launches(fi_ctx* ctx);
+
+/* ------------------------------------------------------------------ host setup numerics
+ * Host restatements used to assemble fi_system_desc (setup, not the hot path). */
+int fi_gamma(double x, double* out);                                    /* numerics.cpp:57-61 */
+int fi_l1_weights(double beta, int S, double* b, double* e);            /* numerics.cpp:63-80 */
+int fi_time_grid(double beta, int S, double T, double* dt, double* eta);/* numerics.cpp:82-96 */
+/* coeffs: 2n-1 entries, index l+n-1 (symbol.cpp:88-110). */
+int fi_symbol_coeffs_1d(double omega, int n, double* coeffs);
+/* coeffs: prod(2n_i-1) entries, lexicographic (symbol.cpp:112-191). d in {1,2}. */
+int fi_symbol_coeffs_md(double omega, int d, const int* n, long long sample_cap, double* coeffs);
+/* Gaussian relative-L2 noise (EXTENSION for BASELINE.json; SplitMix64-at-index + Box-Muller)
+ * and the reference's additive uniform noise (system.cpp:240-251). out may alias mu. */
+int fi_add_gaussian_noise(const double* mu, long long n, double rel_eps, unsigned long long seed, double* out);
+int fi_add_noise(const double* mu, long long n, double eps, unsigned long long seed, double* out);
+
+/* ------------------------------------------------------------------ system operator
+ * Replaces SystemOperator (system.hpp:72-104, system.cpp:121-174).  All arrays are host
+ * pointers, copied at creation:
+ *   gen : generating tensor of B, prod(2 n_i - 1) entries (SymbolCoefficients::coeffs)
+ *   e, b: L1 weights (S entries each), q: q(t_s) (S entries, must be > 0)
+ *   D1, D2: S x N, row-major by level (row s-1 = gamma_k(x, t_s), CoefficientDiagonals)
+ *   eta = dt^beta Gamma(2-beta); scale_space = eta/h^omega; scale_reg = lambda/h^omega. */
+typedef struct {
+    int d;          /* 1 or 2 */
+    int n[2];       /* interior points per direction (n[1] ignored when d == 1) */
+    int S;          /* time steps */
+    double h, eta, scale_space, scale_reg;
+    const double* gen;
+    const double* e;
+    const double* b;
+    const double* q;
+    const double* D1;
+    const double* D2;
+} fi_system_desc;
+
+int fi_system_create(fi_ctx* ctx, const fi_system_desc* desc, fi_system** out);
+void fi_system_destroy(fi_system* sys);
+long long fi_system_dim(const fi_system* sys);        /* (S+1)*N   (SystemOperator::dim) */
+long long fi_system_space_dim(const fi_system* sys);  /* N         (space_dim) */
+/* z = A y on device vectors (SystemOperator::apply, system.cpp:144-174). Async on the stream. */
+int fi_system_apply(fi_system* sys, const double* y_dev, double* z_dev);
+/* Host-buffer convenience: H2D, apply, D2H, synchronize. */
+int fi_system_apply_host(fi_system* sys, const double* y_host, double* z_host);
+
+/* ------------------------------------------------------------------ preconditioner
+ * Replaces BlockTriangularPreconditioner (krylov.hpp:33-50, krylov.cpp:24-70).
+ * block_cap <= 0 selects the reference default 4096 (kDefaultBlockCap); N > block_cap
+ * returns FI_E_RESOURCE like the reference.  Singular blocks return FI_E_SINGULAR with
+ * the 1-based time index (S+1 = regularisation block). */
+int fi_precond_create(fi_system* sys, long long block_cap, fi_precond** out);
+void fi_precond_destroy(fi_precond* P);
+/* y = P^{-1} z (forward block substitution), device vectors, async. */
+int fi_precond_apply(fi_precond* P, const double* z_dev, double* y_dev);
+int fi_precond_apply_host(fi_precond* P, const double* z_host, double* y_host);
+/* Device memory held by the preconditioner's per-level inverses (bytes). */
+long long fi_precond_bytes(const fi_precond* P);
+
+/* ------------------------------------------------------------------ problem assembly helpers
+ * build_rhs (system.cpp:176-190): z^(s) = b_{s-1} D1^(s) o rho, z^(S+1) = mu_eps. Host pointers. */
+int fi_build_rhs(const fi_system* sys, const double* rho_host, const double* mu_eps_host, double* z_host);
+/* forward_solve (system.cpp:192-224) on the device through P's cached time-level inverses
+ * (P == NULL builds a temporary one).  states_host: S*N (may be NULL); mu_host: N. */
+int fi_forward_solve(fi_system* sys, fi_precond* P, const double* rho_host, const double* f_host,
+                     double* states_host, double* mu_host);
+
+/* ------------------------------------------------------------------ GMRES
+ * Replaces gmres() (krylov.hpp:52-69, krylov.cpp:72-209).  Left-preconditioned, MGS with one
+ * conditional re-orthogonalisation, Givens least squares, all on the device: the host
+ * synchronises once per restart cycle, never per iteration.
+ *   restart = 0 : full GMRES (the reference); restart = m > 0 : GMRES(m) (EXTENSION, see
+ *                 DESIGN.md §5 for the exact restart semantics, shared with the oracle).
+ *   maxit = 0   : the system dimension (reference default).
+ * history_host receives residual_history (history_len = iterations + 1 entries, truncated to
+ * history_cap). */
+typedef struct {
+    double tol;
+    int maxit;
+    int restart;
+} fi_gmres_opts;
+
+typedef struct {
+    int iterations;
+    int converged;
+    int breakdown;
+    double wall_time_seconds;
+    double final_true_residual;
+    int history_len;
+} fi_gmres_report;
+
+/* P may be NULL (no preconditioning); x0_dev may be NULL (zero start). */
+int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x0_dev, double* x_dev,
+             const fi_gmres_opts* opts, fi_gmres_report* report, double* history_host, int history_cap);
+/* Host-buffer variant: H2D of b (and x0), solve, D2H of x — the reference-facing call. */
+int fi_gmres_host(fi_system* sys, fi_precond* P, const double* b_host, const double* x0_host, double* x_host,
+                  const fi_gmres_opts* opts, fi_gmres_report* report, double* history_host, int history_cap);
+
+/* Generic LinearOp form (krylov.hpp:52 `LinearOp`): callbacks that enqueue y = op(x) on
+ * the context stream for device vectors of length n and return 0 on success.  apply_M may be
+ * NULL.  Used for the reference's operator-agnostic GMRES known-answer tests. */
+typedef int (*fi_linop_fn)(void* user, const double* x_dev, double* y_dev);
+int fi_gmres_op(fi_ctx* ctx, long long n, fi_linop_fn apply_A, void* user_A, fi_linop_fn apply_M, void* user_M,
+                const double* b_dev, const double* x0_dev, double* x_dev, const fi_gmres_opts* opts,
+                fi_gmres_report* report, double* history_host, int history_cap);
+
+/* ------------------------------------------------------------------ instrumentation
+ * Average device time (ms, CUDA events on the context stream) of the last `fi_*_timed`
+ * kernel launch sequence; used by bench.py for the roofline.  kind: 0 = operator apply
+ * (K1 toeplitz GEMM), 1 = preconditioner apply (K2), 2 = one Arnoldi/MGS step. */
+int fi_system_apply_timed(fi_system* sys, const double* y_dev, double* z_dev, int reps, double* ms_avg);
+int fi_precond_apply_timed(fi_precond* P, const double* z_dev, double* y_dev, int reps, double* ms_avg);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRACINV_B200_H */

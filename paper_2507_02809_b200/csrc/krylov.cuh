@@ -1,0 +1,60 @@
+// Device GMRES engine (K3/K4) shared by fi_gmres and fi_gmres_op.
+#pragma once
+
+#include <cstddef>
+#include <functional>
+#include <vector>
+
+#include "common.cuh"
+
+namespace fib {
+
+// Device-resident Arnoldi/Givens state (one per solve).
+struct GmresState {
+    double* h;      // current Hessenberg column (cycle + 2)
+    double* c;      // second-pass corrections (cycle + 2)
+    double* cs;     // Givens cosines
+    double* sn;     // Givens sines
+    double* g;      // rotated right-hand side
+    double* ycoef;  // back-substitution result
+    double* R;      // rotated columns, column k at R + k * ldR
+    int ldR;
+    double bnorm, tol, breakdown_tol;
+    double pre_norm2, hnorm2;
+    int done, reorth, vnext_ok, iters, kc, converged, breakdown;
+    double scal[4];  // scratch norms read back by the host
+};
+
+inline double* scal_dev(GmresState* st_dev) {
+    return reinterpret_cast<double*>(reinterpret_cast<char*>(st_dev) + offsetof(GmresState, scal));
+}
+
+template <class T>
+inline T* field_dev(GmresState* st_dev, size_t off) {
+    return reinterpret_cast<T*>(reinterpret_cast<char*>(st_dev) + off);
+}
+
+// y = op(x) enqueued on the context stream; skip (device flag) lets enqueued work no-op.
+using Op = std::function<void(const double* x, double* y, const int* skip)>;
+
+class GmresEngine {
+public:
+    GmresEngine(fi_ctx* ctx, long long n);
+    // Reference semantics of gmres() (krylov.cpp:72-209) + restart extension.
+    void solve(const Op& A, const Op* M, const double* b, const double* x0, double* x, double tol, int maxit,
+               int restart, fi_gmres_report* rep, std::vector<double>& history);
+
+private:
+    void reduce(double* w, const double* x, const double* coef, const double* y, int mode, int k, int slot,
+                double* out, const int* gate_on, const int* done);
+    double norm2(const double* v, int slot);
+
+    fi_ctx* ctx_;
+    long long n_;
+    int grid_;
+    GmresState* st_ = nullptr;
+    DevBuf<double> partials_;
+    DevBuf<unsigned> ticket_;
+};
+
+}  // namespace fib

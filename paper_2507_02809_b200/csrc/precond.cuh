@@ -1,0 +1,31 @@
+// Block lower-triangular preconditioner P (replaces BlockTriangularPreconditioner,
+// krylov.hpp:33-50, krylov.cpp:24-70).
+#pragma once
+
+#include "system.cuh"
+
+struct fi_precond {
+    fi_system* sys = nullptr;
+    int nb = 0;        // 64-row blocks per level (Np / 64)
+    long long T = 0;   // lower-triangular 64x64 tiles per level: nb (nb + 1) / 2
+    int G = 0;         // persistent CTAs of the apply kernel
+    int levels = 0;    // S + 1
+    int refine = 1;    // one iterative-refinement sweep with the FP32 inverses (parity with LU solves)
+    fib::DevBuf<double> H;      // [level][tile][64*64]: packed symmetric inverses
+    fib::DevBuf<float> Hf;      // FP32 copy for the refinement sweep
+    fib::DevBuf<double> rbuf, dbuf;  // refinement residual and correction
+    fib::DevBuf<double> d2inv;  // S x Np: 1 / D2 (pads 0)
+    fib::DevBuf<double> xbuf;   // Np
+    fib::DevBuf<double> pbuf;   // nb * nb * 64 partial products
+    fib::DevBuf<unsigned> bar;  // grid barrier counter
+    fib::DevBuf<double> zbuf, ybuf;  // padded scratch for reference-layout applies
+};
+
+namespace fib {
+// y = P^{-1} z on padded vectors (K2).  levels = S+1 (full P) or S (time levels only:
+// the forward solve, system.cpp:192-224).  skip: optional device flag.
+void precond_apply(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip);
+void precond_build(fi_precond* P);
+// z_s = b_{s-1} D1_s o rho + eta q_s f (padded, levels 0..S-1): forward-solve right-hand side.
+void forward_rhs(fi_ctx* ctx, const fi_system* sys, const double* rho_pad, const double* f_pad, double* z_pad);
+}  // namespace fib

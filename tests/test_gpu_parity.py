@@ -1,0 +1,311 @@
+"""GPU parity: the B200 path (C-ABI via paper_2507_02809_b200.fracinv) against the CPU oracle
+on identical seeded inputs.  Tolerances are the north star's: operator/preconditioner applies
+<= 1e-12 relative L2, GMRES iteration count +-1, recovered f <= 1e-8 relative L2."""
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+from helpers import RandomVectors, paper_problem, test_problem_2d
+from oracle import fracinv_oracle as O
+
+pytestmark = pytest.mark.gpu
+warnings.filterwarnings("ignore", module="scipy")
+
+F = pytest.importorskip("paper_2507_02809_b200.fracinv")
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def _paper(M, beta, omega, n, S, lam=5e-3, eps=0.01):
+    return M.make_problem("paper1d", beta, omega, [n], S, lam, eps)
+
+
+def _problem2d(M, beta, omega, n, S, lam=5e-3, eps=0.01):
+    h = math.pi / (n[0] + 1)
+    grid = M.SpaceGrid(n, [0.0, 0.0], [math.pi, h * (n[1] + 1)])
+    X = grid.nodes()
+    f = X[:, 0] * np.sin(X[:, 0]) * np.sin(X[:, 1])
+    return M.make_custom_problem(
+        M.FractionalOrders(beta, omega), grid, S, 1.0,
+        lambda X, t: t * np.exp(X[:, 0]) * (1.0 + 0.5 * X[:, 1]),
+        lambda X, t: t * t * (X[:, 0] + 0.25 * X[:, 1] + 0.1),
+        lambda t: t * t, np.zeros(X.shape[0]), f, lam, eps)
+
+
+# ---------------------------------------------------------------- BASELINE configs (1D)
+def config_problem(M, cfg):
+    """BASELINE.json configs 0-4 as ProblemSpecs (mu is built separately)."""
+    pi = math.pi
+    if cfg == 0:
+        n, S, beta, omega, lam = 255, 64, 0.5, 1.5, 1e-3
+        g1 = lambda X, t: 1 + 0.5 * np.sin(pi * X[:, 0]) * np.exp(-t)
+        g2 = lambda X, t: 1 + X[:, 0] * (1 - X[:, 0]) * (1 + t)
+        q = lambda t: 1 + t
+        rho = lambda X: X[:, 0] ** 2 * (1 - X[:, 0]) ** 2
+        f = lambda X: np.sin(pi * X[:, 0])
+        grid = M.SpaceGrid([n], [0.0], [1.0])
+    elif cfg == 1:
+        n, S, beta, omega, lam = 4095, 512, 0.9, 1.8, 1e-4
+        g1 = lambda X, t: 2 + np.cos(2 * pi * X[:, 0])
+        g2 = lambda X, t: 1 + 0.5 * X[:, 0] * t
+        q = lambda t: math.exp(-t)
+        rho = lambda X: X[:, 0] ** 2 * (1 - X[:, 0]) ** 2
+        f = lambda X: X[:, 0] * (1 - X[:, 0]) * np.exp(X[:, 0])
+        grid = M.SpaceGrid([n], [0.0], [1.0])
+    elif cfg == 2:
+        n, S, beta, omega, lam = 127, 128, 0.3, 1.2, 1e-3
+        g1 = lambda X, t: 1 + 0.5 * np.sin(pi * X[:, 0]) * np.sin(pi * X[:, 1])
+        g2 = lambda X, t: 1 + X[:, 0] * X[:, 1] * (1 + t)
+        q = lambda t: 1 + t * t
+        rho = lambda X: np.zeros(X.shape[0])
+        f = lambda X: np.sin(pi * X[:, 0]) * np.sin(2 * pi * X[:, 1])
+        grid = M.SpaceGrid([n, n], [0.0, 0.0], [1.0, 1.0])
+    elif cfg in (3, 4):
+        n = 255
+        if cfg == 3:
+            S, beta, omega, lam = 256, 0.7, 1.5, 1e-4
+            g1 = lambda X, t: 1 + X[:, 0] ** 2 + X[:, 1] ** 2
+            g2 = lambda X, t: 2 + np.sin(pi * X[:, 0] * X[:, 1]) * np.exp(-t)
+            q = lambda t: math.exp(-t)
+            f = lambda X: 16 * X[:, 0] * (1 - X[:, 0]) * X[:, 1] * (1 - X[:, 1])
+        else:
+            S, beta, omega, lam = 512, 0.95, 1.9, 1e-2
+            g1 = lambda X, t: 1 + 0.9 * np.sin(3 * pi * X[:, 0]) * np.sin(3 * pi * X[:, 1])
+            g2 = lambda X, t: 1 + 10 * X[:, 0] * X[:, 1] * (1 + t)
+            q = lambda t: 1.0 + 0.0 * t  # BASELINE gives no q for config 4: q = 1
+            f = lambda X: ((X[:, 0] >= 0.25) & (X[:, 0] <= 0.75) & (X[:, 1] >= 0.25) & (X[:, 1] <= 0.75)) * 1.0
+        rho = lambda X: np.zeros(X.shape[0])
+        grid = M.SpaceGrid([n, n], [0.0, 0.0], [1.0, 1.0])
+    X = grid.nodes()
+    return M.make_custom_problem(M.FractionalOrders(beta, omega), grid, S, 1.0, g1, g2, q, rho(X), f(X), lam, 0.0)
+
+
+# ---------------------------------------------------------------- operator apply (K1)
+@pytest.mark.parametrize("beta,omega", [(0.1, 1.9), (0.5, 1.5), (0.9, 1.1)])
+def test_operator_apply_small(beta, omega):
+    rng = RandomVectors(17)
+    for mk in (lambda M: _paper(M, beta, omega, 32, 16), lambda M: _problem2d(M, beta, omega, [4, 3], 8),
+               lambda M: _problem2d(M, beta, omega, [6, 5], 16)):
+        A, Ao = F.SystemOperator(mk(F)), O.SystemOperator(mk(O))
+        for _ in range(10):
+            y = rng.vector(A.dim())
+            assert _rel(A.apply(y), Ao.apply(y)) <= 1e-12
+        # against the dense realisation as well (test_system.cpp:80-99)
+        M = O.assemble_dense_system(Ao, O.SYSTEM_A)
+        y = rng.vector(A.dim())
+        assert _rel(A.apply(y), M @ y) <= 1e-12
+
+
+def test_operator_zero_linear_and_scalar_reduction():
+    A = F.SystemOperator(_paper(F, 0.5, 1.5, 8, 4))
+    assert np.linalg.norm(A.apply(np.zeros(A.dim()))) == 0.0
+    rng = RandomVectors(5)
+    y1, y2 = rng.vector(A.dim()), rng.vector(A.dim())
+    assert _rel(A.apply(0.37 * y1 + y2), 0.37 * A.apply(y1) + A.apply(y2)) <= 1e-12
+    with pytest.raises(F.DimensionError):
+        A.apply(np.zeros(A.dim() + 1))
+    one = lambda X, t: np.ones(X.shape[0])
+    spec = F.make_custom_problem(F.FractionalOrders(0.5, 1.5), F.SpaceGrid([1], [0.0], [2.0]), 1, 1.0, one, one,
+                                 lambda t: 1.0, np.zeros(1), np.zeros(1), 7e-3, 0.0)
+    A = F.SystemOperator(spec)
+    a0, eta = A.symbol.at(0), A.spec.tgrid.eta
+    y = np.array([1.25, -0.5])
+    z = A.apply(y)
+    assert z[0] == pytest.approx((1 + eta * a0) * y[0] - eta * y[1], rel=1e-14)
+    assert z[1] == pytest.approx(y[0] + 7e-3 * a0 * y[1], rel=1e-14)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+def test_operator_apply_baseline_configs(cfg):
+    A, Ao = F.SystemOperator(config_problem(F, cfg)), O.SystemOperator(config_problem(O, cfg))
+    rng = RandomVectors(100 + cfg)
+    for _ in range(3 if cfg < 3 else 1):
+        y = rng.vector(A.dim())
+        assert _rel(A.apply(y), Ao.apply(y)) <= 1e-12
+
+
+def test_operator_apply_device_tensors():
+    torch = pytest.importorskip("torch")
+    A, Ao = F.SystemOperator(config_problem(F, 0)), O.SystemOperator(config_problem(O, 0))
+    y = RandomVectors(3).vector(A.dim())
+    z = A.apply(torch.from_numpy(y).cuda())
+    assert z.is_cuda and _rel(z.cpu().numpy(), Ao.apply(y)) <= 1e-12
+
+
+# ---------------------------------------------------------------- preconditioner (K2)
+def test_precond_inverts_dense_small():
+    for mk in (lambda M: _paper(M, 0.5, 1.5, 8, 4), lambda M: _paper(M, 0.1, 1.9, 32, 16),
+               lambda M: _problem2d(M, 0.5, 1.5, [6, 5], 16)):
+        A, Ao = F.SystemOperator(mk(F)), O.SystemOperator(mk(O))
+        P, Po = F.BlockTriangularPreconditioner(A), O.BlockTriangularPreconditioner(Ao)
+        Pd = O.assemble_dense_system(Ao, O.PRECONDITIONER_P)
+        rng = RandomVectors(3)
+        for _ in range(5):
+            y = rng.vector(A.dim())
+            assert _rel(P.apply(Pd @ y), y) <= 1e-10
+            z = rng.vector(A.dim())
+            assert _rel(P.apply(z), Po.apply(z)) <= 1e-12
+
+
+def test_precond_scalar_reduction_zero_and_errors():
+    spec = lambda M: M.make_custom_problem(M.FractionalOrders(0.5, 1.5), M.SpaceGrid([1], [0.0], [2.0]), 1, 1.0,
+                                           lambda X, t: np.full(X.shape[0], 2.0),
+                                           lambda X, t: np.full(X.shape[0], 3.0), lambda t: 1.0, np.zeros(1),
+                                           np.zeros(1), 7e-3, 0.0)
+    A = F.SystemOperator(spec(F))
+    P = F.BlockTriangularPreconditioner(A)
+    a0, eta = A.symbol.at(0), A.spec.tgrid.eta
+    z = np.array([0.8, -1.1])
+    y = P.apply(z)
+    y1 = z[0] / (2.0 + eta * 3.0 * a0)
+    assert y[0] == pytest.approx(y1, rel=1e-14)
+    assert y[1] == pytest.approx((z[1] - y1) / (7e-3 * 3.0 * a0), rel=1e-14)
+    A = F.SystemOperator(_paper(F, 0.5, 1.5, 6, 3))
+    P = F.BlockTriangularPreconditioner(A)
+    assert np.linalg.norm(P.apply(np.zeros(A.dim()))) == 0.0
+    with pytest.raises(F.DimensionError):
+        P.apply(np.zeros(A.dim() - 1))
+    with pytest.raises(F.ResourceLimitError):
+        F.BlockTriangularPreconditioner(F.SystemOperator(_paper(F, 0.5, 1.5, 16, 4)), 8)
+    one = lambda X, t: np.ones(X.shape[0])
+    spec = F.make_custom_problem(F.FractionalOrders(0.5, 1.5), F.SpaceGrid([4], [0.0], [math.pi]), 2, 1.0, one,
+                                 lambda X, t: np.full(X.shape[0], 1.0 - t), lambda t: 1.0, np.zeros(4), np.zeros(4),
+                                 1e-2, 0.0)
+    with pytest.raises(F.SingularBlockError) as ex:
+        F.BlockTriangularPreconditioner(F.SystemOperator(spec))
+    assert ex.value.time_index == 3
+
+
+def test_precond_config0_parity():
+    A, Ao = F.SystemOperator(config_problem(F, 0)), O.SystemOperator(config_problem(O, 0))
+    P, Po = F.BlockTriangularPreconditioner(A), O.BlockTriangularPreconditioner(Ao)
+    rng = RandomVectors(7)
+    for _ in range(5):
+        z = rng.vector(A.dim())
+        y = P.apply(z)
+        assert _rel(y, Po.apply(z)) <= 1e-12
+        assert _rel(Ao.apply_precond_matrix(y), z) <= 1e-13  # backward error
+
+
+def test_precond_config1_backward_error_and_levels():
+    """Config 1 (N=4095, S=512): P^{-1} via 513 packed symmetric inverses (35 GB) on the GPU.
+    The oracle's 68.8 GB of LU factors are not cached here, so parity is checked through
+    (i) the size-independent backward error ||P y - z|| / ||z|| with the oracle's matrix-free P,
+    (ii) forward parity of the first levels and of the f-block against oracle LU solves."""
+    A, Ao = F.SystemOperator(config_problem(F, 1)), O.SystemOperator(config_problem(O, 1))
+    P = F.BlockTriangularPreconditioner(A)
+    Po = O.BlockTriangularPreconditioner.__new__(O.BlockTriangularPreconditioner)
+    Po.A, Po.N, Po.S, Po.cache = Ao, Ao.N, Ao.steps, False
+    Po.Bd = Ao.laplacian.dense(Ao.N)
+    z = RandomVectors(11).vector(A.dim())
+    y = P.apply(z)
+    bwd = _rel(Ao.apply_precond_matrix(y), z)
+    N, S = Ao.N, Ao.steps
+    e = Ao.weights.e
+    Y = y[: S * N].reshape(S, N)
+    lev = []
+    for s in (1, 2, 3):
+        rhs = z[(s - 1) * N: s * N] - Ao.diags.D1[s - 1] * (e[s - 1:0:-1] @ Y[: s - 1] if s > 1 else 0.0)
+        lev.append(_rel(Y[s - 1], Po.solve_block(s, rhs)))
+    yf = Po.solve_block(S + 1, z[S * N:] - Y[S - 1])
+    fpar = _rel(y[S * N:], yf)
+    print(f"config1 P: backward error {bwd:.3e}, levels 1-3 forward parity {lev}, f-block parity {fpar:.3e}")
+    assert bwd <= 1e-12
+    assert max(lev) <= 1e-12
+    assert fpar <= 1e-10  # kappa(f-block) ~ 1.9e6: two stable solvers differ by O(kappa u)
+
+
+# ---------------------------------------------------------------- forward solve
+def test_forward_solve_parity():
+    for mk in (lambda M: _paper(M, 0.1, 1.9, 8, 4), lambda M: config_problem(M, 0)):
+        A, Ao = F.SystemOperator(mk(F)), O.SystemOperator(mk(O))
+        sol, solo = F.forward_solve(A), O.forward_solve(Ao)
+        assert _rel(np.concatenate(sol.states), np.concatenate(solo.states)) <= 1e-12
+        assert _rel(sol.mu, solo.mu) <= 1e-12
+    one = lambda X, t: np.zeros(X.shape[0])
+    spec = F.make_custom_problem(F.FractionalOrders(0.5, 1.5), F.SpaceGrid([4], [0.0], [math.pi]), 2, 1.0, one,
+                                 lambda X, t: np.full(X.shape[0], t - 0.5), lambda t: 1.0, np.zeros(4), np.ones(4),
+                                 1e-2, 0.0)
+    with pytest.raises(F.SingularBlockError) as ex:
+        F.forward_solve(F.SystemOperator(spec))
+    assert ex.value.time_index == 1
+
+
+# ---------------------------------------------------------------- GMRES known answers (K3/K4, LinearOp path)
+def test_gmres_known_answers_linear_ops():
+    torch = pytest.importorskip("torch")
+    mat = lambda M: (lambda x, M=torch.as_tensor(M, device="cuda"): M @ x)
+    b = RandomVectors(2).vector(12)
+    x, rep = F.gmres(mat(np.eye(12)), None, b)
+    assert rep.converged and rep.iterations == 1 and _rel(x, b) <= 1e-12
+    x, rep = F.gmres(mat(np.diag([2.0, 3.0])), None, np.array([2.0, 3.0]))
+    assert rep.converged and rep.iterations <= 2 and np.linalg.norm(x - 1) <= 1e-10
+    diag = np.array([1.0, 2.5, 4.0, 7.5, 10.0])[np.arange(60) % 5]
+    b = RandomVectors(8).vector(60)
+    x, rep = F.gmres(mat(np.diag(diag)), None, b, F.GmresOptions(1e-12, 0))
+    assert rep.converged and rep.iterations <= 5 and _rel(diag * x, b) <= 1e-10
+    x, rep = F.gmres(mat(np.eye(5)), None, np.zeros(5))
+    assert rep.converged and rep.iterations == 0 and np.linalg.norm(x) == 0 and rep.residual_history == [0.0]
+    x, rep = F.gmres(mat(np.diag([1.0, 1.0, 0.0])), None, np.ones(3), F.GmresOptions(1e-8, 0))
+    assert rep.breakdown and not rep.converged and rep.residual_history[-1] > 1e-8
+    assert rep.final_true_residual == pytest.approx(1 / math.sqrt(3), rel=1e-10)
+
+
+def test_gmres_random_dense_matches_oracle():
+    torch = pytest.importorskip("torch")
+    rng = RandomVectors(13)
+    for trial in range(6):
+        n = 20 + 12 * trial
+        M = np.array([rng.next_double() for _ in range(n * n)]).reshape(n, n) + 2.0 * math.sqrt(n) * np.eye(n)
+        b = rng.vector(n)
+        Mt = torch.as_tensor(M, device="cuda")
+        for restart in (0, 7):
+            x, rep = F.gmres(lambda v: Mt @ v, None, b, F.GmresOptions(1e-10, 0, restart))
+            xo, repo = O.gmres(lambda v: M @ v, None, b, tol=1e-10, restart=restart)
+            assert rep.converged and abs(rep.iterations - repo.iterations) <= 1
+            h = rep.residual_history
+            assert len(h) == rep.iterations + 1
+            if restart == 0:
+                assert all(h[i] <= h[i - 1] * (1 + 1e-15) for i in range(1, len(h)))
+            assert rep.final_true_residual <= 1e-8
+            assert _rel(x, xo) <= 1e-8
+
+
+# ---------------------------------------------------------------- GMRES on the all-at-once system
+TABLE2 = [(16, 16, (174, 117, 112), (8, 10, 13)), (16, 32, (257, 146, 154), (8, 11, 13)),
+          (32, 16, (320, 181, 151), (9, 11, 15)), (32, 32, (475, 217, 199), (8, 11, 15))]
+ORDERS = [(0.1, 1.9), (0.5, 1.5), (0.9, 1.1)]
+
+
+@pytest.mark.parametrize("n,S,unprec,prec", TABLE2)
+def test_table2_iterations_on_gpu(n, S, unprec, prec):
+    for k, (beta, omega) in enumerate(ORDERS):
+        A, Ao = F.SystemOperator(_paper(F, beta, omega, n, S)), O.SystemOperator(_paper(O, beta, omega, n, S))
+        P, Po = F.BlockTriangularPreconditioner(A), O.BlockTriangularPreconditioner(Ao)
+        z = O.build_rhs(Ao, O.add_noise(O.forward_solve(Ao).mu, 0.01, 1)).z
+        xp, rp = F.gmres(A, P, z, F.GmresOptions(1e-8))
+        xu, ru = F.gmres(A, None, z, F.GmresOptions(1e-8))
+        xpo, rpo = O.gmres(Ao.apply, Po.apply, z, tol=1e-8)
+        xuo, ruo = O.gmres(Ao.apply, None, z, tol=1e-8)
+        assert rp.converged and ru.converged
+        assert abs(rp.iterations - rpo.iterations) <= 1 and abs(ru.iterations - ruo.iterations) <= 1
+        assert abs(rp.iterations - prec[k]) <= 2 and abs(ru.iterations - unprec[k]) <= 0.1 * unprec[k]
+        assert _rel(xp[-n:], xpo[-n:]) <= 1e-8
+
+
+def test_config0_end_to_end():
+    """BASELINE config 0: GMRES(50), tol 1e-10, 1% Gaussian noise (seed 1000), P on."""
+    A, Ao = F.SystemOperator(config_problem(F, 0)), O.SystemOperator(config_problem(O, 0))
+    P, Po = F.BlockTriangularPreconditioner(A), O.BlockTriangularPreconditioner(Ao)
+    mu = O.add_gaussian_noise(O.forward_solve(Ao).mu, 0.01, 1000)
+    z = O.build_rhs(Ao, mu).z
+    assert _rel(F.build_rhs(A, mu).z, z) == 0.0
+    x, rep = F.gmres(A, P, z, F.GmresOptions(1e-10, 0, 50))
+    xo, repo = O.gmres(Ao.apply, Po.apply, z, tol=1e-10, restart=50)
+    assert rep.converged and abs(rep.iterations - repo.iterations) <= 1
+    assert _rel(x[-255:], xo[-255:]) <= 1e-8
+    assert rep.final_true_residual <= 10 * repo.final_true_residual
