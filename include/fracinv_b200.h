@@ -116,6 +116,10 @@ int fi_precond_apply(fi_precond* P, const double* z_dev, double* y_dev);
 int fi_precond_apply_host(fi_precond* P, const double* z_host, double* y_host);
 /* Device memory held by the preconditioner's per-level inverses (bytes). */
 long long fi_precond_bytes(const fi_precond* P);
+/* refine != 0 (default): each apply adds one iterative-refinement sweep (FP32 inverses, FP64
+ * residual through the operator kernel) so P^{-1} z matches LU-based solves to ~1e-13;
+ * refine == 0: single FP64 sweep (forward error ~ kappa(block) * eps). */
+int fi_precond_set_refine(fi_precond* P, int refine);
 
 /* ------------------------------------------------------------------ problem assembly helpers
  * build_rhs (system.cpp:176-190): z^(s) = b_{s-1} D1^(s) o rho, z^(S+1) = mu_eps. Host pointers. */

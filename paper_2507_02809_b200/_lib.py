@@ -82,6 +82,7 @@ _SIGS = {
     "fi_precond_apply_host": (ctypes.c_int, [c_void_p, c_double_p, c_double_p]),
     "fi_precond_apply_timed": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, ctypes.c_int, c_double_p]),
     "fi_precond_bytes": (ctypes.c_longlong, [c_void_p]),
+    "fi_precond_set_refine": (ctypes.c_int, [c_void_p, ctypes.c_int]),
     "fi_build_rhs": (ctypes.c_int, [c_void_p, c_double_p, c_double_p, c_double_p]),
     "fi_forward_solve": (ctypes.c_int, [c_void_p, c_void_p, c_double_p, c_double_p, c_double_p, c_double_p]),
     "fi_gmres": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, ctypes.POINTER(GmresOpts),

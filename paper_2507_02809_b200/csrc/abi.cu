@@ -245,6 +245,7 @@ void fi_system_destroy(fi_system* sys) {
     if (!sys || --sys->refs > 0) return;
     fi_ctx* ctx = sys->ctx;
     cudaStreamSynchronize(ctx->stream);
+    delete sys->engine;
     delete sys;
     fi_ctx_destroy(ctx);
 }
@@ -312,7 +313,14 @@ void fi_precond_destroy(fi_precond* P) {
     fi_system_destroy(sys);
 }
 
-long long fi_precond_bytes(const fi_precond* P) { return P ? (long long)P->H.bytes() : 0; }
+long long fi_precond_bytes(const fi_precond* P) { return P ? (long long)(P->H.bytes() + P->Hf.bytes()) : 0; }
+
+int fi_precond_set_refine(fi_precond* P, int refine) {
+    return guard([&] {
+        require(P != nullptr, FI_E_DOMAIN, "fi_precond_set_refine: NULL preconditioner");
+        P->refine = refine ? 1 : 0;
+    });
+}
 
 int fi_precond_apply(fi_precond* P, const double* z_dev, double* y_dev) {
     return guard([&] {
@@ -423,10 +431,16 @@ int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x
         fi_ctx* ctx = sys->ctx;
         const fib::Layout& L = sys->L;
         const long long n = L.nI();
-        fib::DevBuf<double> b((size_t)n), x((size_t)n), x0;
+        if (sys->gb.n < (size_t)n) {
+            sys->gb.alloc((size_t)n);
+            sys->gx.alloc((size_t)n);
+        }
+        fib::DevBuf<double>& b = sys->gb;
+        fib::DevBuf<double>& x = sys->gx;
+        fib::DevBuf<double>& x0 = sys->gx0;
         fib::pack_vector(ctx, L, b_dev, b.p);
         if (x0_dev) {
-            x0.alloc((size_t)n);
+            if (x0.n < (size_t)n) x0.alloc((size_t)n);
             fib::pack_vector(ctx, L, x0_dev, x0.p);
         }
         const fib::OperatorView view = sys->view();
@@ -438,10 +452,10 @@ int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x
         };
         // maxit = 0 selects the matrix dimension (krylov.hpp:56), i.e. the reference's n
         const int maxit = opts->maxit > 0 ? opts->maxit : (int)std::min<long long>(L.nRef(), 0x7fffffff);
-        fib::GmresEngine eng(ctx, n);
+        if (!sys->engine) sys->engine = new fib::GmresEngine(ctx, n);
         std::vector<double> hist;
-        eng.solve(A, P ? &M : nullptr, b.p, x0_dev ? x0.p : nullptr, x.p, opts->tol, maxit, opts->restart, report,
-                  hist);
+        sys->engine->solve(A, P ? &M : nullptr, b.p, x0_dev ? x0.p : nullptr, x.p, opts->tol, maxit, opts->restart,
+                           report, hist);
         fib::unpack_vector(ctx, L, x.p, x_dev);
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
         copy_history(hist, history_host, history_cap);
@@ -455,15 +469,17 @@ int fi_gmres_host(fi_system* sys, fi_precond* P, const double* b_host, const dou
         require(sys && b_host && x_host, FI_E_DOMAIN, "fi_gmres_host: NULL argument");
         fi_ctx* ctx = sys->ctx;
         const size_t n = (size_t)sys->L.nRef();
-        fib::DevBuf<double> b(n), x(n), x0;
-        FI_CUDA(cudaMemcpyAsync(b.p, b_host, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        if (x0_host) {
-            x0.alloc(n);
-            FI_CUDA(cudaMemcpyAsync(x0.p, x0_host, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        }
-        rc = fi_gmres(sys, P, b.p, x0_host ? x0.p : nullptr, x.p, opts, report, history_host, history_cap);
+        // staging for the reference-layout host vectors: [b | x | x0], kept across calls
+        if (sys->gio.n < 3 * n) sys->gio.alloc(3 * n);
+        double* b = sys->gio.p;
+        double* x = b + n;
+        double* x0 = x + n;
+        FI_CUDA(cudaMemcpyAsync(b, b_host, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        if (x0_host)
+            FI_CUDA(cudaMemcpyAsync(x0, x0_host, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        rc = fi_gmres(sys, P, b, x0_host ? x0 : nullptr, x, opts, report, history_host, history_cap);
         if (rc != FI_OK) throw fib::Error(rc, g_err, g_time_index);
-        FI_CUDA(cudaMemcpyAsync(x_host, x.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        FI_CUDA(cudaMemcpyAsync(x_host, x, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
     });
     return rc2;

@@ -303,11 +303,17 @@ void GmresEngine::solve(const Op& A, const Op* M, const double* b, const double*
         throw Error(FI_E_RESOURCE, "gmres: Krylov basis of " + std::to_string(cycle + 1) + " vectors (" +
                                        std::to_string(need) + " bytes) exceeds free device memory; use restart");
     const long long ldv = (n + 1) & ~1LL;
-    DevBuf<double> V((size_t)(cycle + 1) * ldv), w((size_t)n), t1((size_t)n), t2((size_t)n);
-    DevBuf<double> hist_d((size_t)maxit + 1);
+    // workspaces persist across solves (no cudaMalloc/cudaFree inside a timed solve)
+    DevBuf<double>&V = V_, &w = w_, &t1 = t1_, &t2 = t2_, &hist_d = hist_, &arr = arr_, &ycoef = ycoef_;
+    DevBuf<GmresState>& st_d = st_buf_;
+    ensure(V, (size_t)(cycle + 1) * ldv);
+    ensure(w, (size_t)n);
+    ensure(t1, (size_t)n);
+    ensure(t2, (size_t)n);
+    ensure(hist_d, (size_t)maxit + 1);
     // device state
-    DevBuf<GmresState> st_d(1);
-    DevBuf<double> arr((size_t)(cycle + 2) * 5 + (size_t)(cycle + 1) * (cycle + 1));
+    ensure(st_d, 1);
+    ensure(arr, (size_t)(cycle + 2) * 5 + (size_t)(cycle + 1) * (cycle + 1));
     GmresState hs{};
     hs.h = arr.p;
     hs.c = hs.h + (cycle + 2);
@@ -317,7 +323,7 @@ void GmresEngine::solve(const Op& A, const Op* M, const double* b, const double*
     hs.R = hs.g + (cycle + 2);
     hs.ldR = cycle + 1;
     st_ = st_d.p;
-    DevBuf<double> ycoef((size_t)cycle + 1);
+    ensure(ycoef, (size_t)cycle + 1);
     hs.ycoef = ycoef.p;
 
     auto upload_state = [&]() {

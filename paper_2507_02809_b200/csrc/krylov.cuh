@@ -40,6 +40,7 @@ using Op = std::function<void(const double* x, double* y, const int* skip)>;
 class GmresEngine {
 public:
     GmresEngine(fi_ctx* ctx, long long n);
+    long long n() const { return n_; }
     // Reference semantics of gmres() (krylov.cpp:72-209) + restart extension.
     void solve(const Op& A, const Op* M, const double* b, const double* x0, double* x, double tol, int maxit,
                int restart, fi_gmres_report* rep, std::vector<double>& history);
@@ -49,12 +50,19 @@ private:
                 double* out, const int* gate_on, const int* done);
     double norm2(const double* v, int slot);
 
+    template <class T>
+    static void ensure(DevBuf<T>& b, size_t count) {
+        if (b.n < count) b.alloc(count);
+    }
+
     fi_ctx* ctx_;
     long long n_;
     int grid_;
     GmresState* st_ = nullptr;
     DevBuf<double> partials_;
     DevBuf<unsigned> ticket_;
+    DevBuf<double> V_, w_, t1_, t2_, hist_, arr_, ycoef_;
+    DevBuf<GmresState> st_buf_;
 };
 
 }  // namespace fib

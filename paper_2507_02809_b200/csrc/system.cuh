@@ -21,6 +21,10 @@ constexpr int kEOFF = 128;
 
 }  // namespace fib
 
+namespace fib {
+class GmresEngine;
+}
+
 struct fi_system {
     int refs = 1;
     fi_ctx* ctx = nullptr;
@@ -29,6 +33,8 @@ struct fi_system {
     std::vector<double> gen_h, e_h, b_h, q_h, D1_h, D2_h;  // host copies (reference layout)
     fib::DevBuf<double> gen, epad, D1, D2, q, e, bw;
     fib::DevBuf<double> ubuf, zbuf;  // padded scratch for reference-layout applies
+    fib::DevBuf<double> gb, gx, gx0, gio;  // fi_gmres padded b / x / x0 and host-call staging
+    fib::GmresEngine* engine = nullptr;  // cached Krylov workspace (owned; freed in fi_system_destroy)
     fib::OperatorView view() const {
         fib::OperatorView v;
         v.n1 = L.n1; v.n2 = L.n2; v.ld2 = L.ld2; v.S = L.S; v.Np = L.Np;
@@ -40,6 +46,7 @@ struct fi_system {
 };
 
 namespace fib {
+class GmresEngine;
 // Z = A U on padded device vectors (K1: on-the-fly Toeplitz DMMA GEMM + fused epilogue).
 // skip: optional device flag; the kernel returns immediately when *skip != 0.
 // minus_from != nullptr: Z = minus_from - (A U) (residual form).  precond_matrix: apply P instead of

@@ -445,6 +445,10 @@ class BlockTriangularPreconditioner:
     def device_bytes(self) -> int:
         return int(lib.fi_precond_bytes(self.handle))
 
+    def set_refine(self, refine: bool):
+        """Iterative-refinement sweep on (default, LU-grade accuracy) or off (one FP64 sweep)."""
+        _check(lib.fi_precond_set_refine(self.handle, 1 if refine else 0))
+
     def apply(self, z):
         """y = P^{-1} z by forward block substitution (krylov.cpp:48-70)."""
         n = self.dim()

@@ -36,52 +36,7 @@ def _problem2d(M, beta, omega, n, S, lam=5e-3, eps=0.01):
         lambda t: t * t, np.zeros(X.shape[0]), f, lam, eps)
 
 
-# ---------------------------------------------------------------- BASELINE configs (1D)
-def config_problem(M, cfg):
-    """BASELINE.json configs 0-4 as ProblemSpecs (mu is built separately)."""
-    pi = math.pi
-    if cfg == 0:
-        n, S, beta, omega, lam = 255, 64, 0.5, 1.5, 1e-3
-        g1 = lambda X, t: 1 + 0.5 * np.sin(pi * X[:, 0]) * np.exp(-t)
-        g2 = lambda X, t: 1 + X[:, 0] * (1 - X[:, 0]) * (1 + t)
-        q = lambda t: 1 + t
-        rho = lambda X: X[:, 0] ** 2 * (1 - X[:, 0]) ** 2
-        f = lambda X: np.sin(pi * X[:, 0])
-        grid = M.SpaceGrid([n], [0.0], [1.0])
-    elif cfg == 1:
-        n, S, beta, omega, lam = 4095, 512, 0.9, 1.8, 1e-4
-        g1 = lambda X, t: 2 + np.cos(2 * pi * X[:, 0])
-        g2 = lambda X, t: 1 + 0.5 * X[:, 0] * t
-        q = lambda t: math.exp(-t)
-        rho = lambda X: X[:, 0] ** 2 * (1 - X[:, 0]) ** 2
-        f = lambda X: X[:, 0] * (1 - X[:, 0]) * np.exp(X[:, 0])
-        grid = M.SpaceGrid([n], [0.0], [1.0])
-    elif cfg == 2:
-        n, S, beta, omega, lam = 127, 128, 0.3, 1.2, 1e-3
-        g1 = lambda X, t: 1 + 0.5 * np.sin(pi * X[:, 0]) * np.sin(pi * X[:, 1])
-        g2 = lambda X, t: 1 + X[:, 0] * X[:, 1] * (1 + t)
-        q = lambda t: 1 + t * t
-        rho = lambda X: np.zeros(X.shape[0])
-        f = lambda X: np.sin(pi * X[:, 0]) * np.sin(2 * pi * X[:, 1])
-        grid = M.SpaceGrid([n, n], [0.0, 0.0], [1.0, 1.0])
-    elif cfg in (3, 4):
-        n = 255
-        if cfg == 3:
-            S, beta, omega, lam = 256, 0.7, 1.5, 1e-4
-            g1 = lambda X, t: 1 + X[:, 0] ** 2 + X[:, 1] ** 2
-            g2 = lambda X, t: 2 + np.sin(pi * X[:, 0] * X[:, 1]) * np.exp(-t)
-            q = lambda t: math.exp(-t)
-            f = lambda X: 16 * X[:, 0] * (1 - X[:, 0]) * X[:, 1] * (1 - X[:, 1])
-        else:
-            S, beta, omega, lam = 512, 0.95, 1.9, 1e-2
-            g1 = lambda X, t: 1 + 0.9 * np.sin(3 * pi * X[:, 0]) * np.sin(3 * pi * X[:, 1])
-            g2 = lambda X, t: 1 + 10 * X[:, 0] * X[:, 1] * (1 + t)
-            q = lambda t: 1.0 + 0.0 * t  # BASELINE gives no q for config 4: q = 1
-            f = lambda X: ((X[:, 0] >= 0.25) & (X[:, 0] <= 0.75) & (X[:, 1] >= 0.25) & (X[:, 1] <= 0.75)) * 1.0
-        rho = lambda X: np.zeros(X.shape[0])
-        grid = M.SpaceGrid([n, n], [0.0, 0.0], [1.0, 1.0])
-    X = grid.nodes()
-    return M.make_custom_problem(M.FractionalOrders(beta, omega), grid, S, 1.0, g1, g2, q, rho(X), f(X), lam, 0.0)
+from paper_2507_02809_b200.configs import baseline_problem as config_problem  # noqa: E402
 
 
 # ---------------------------------------------------------------- operator apply (K1)
