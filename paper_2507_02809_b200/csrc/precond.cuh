@@ -15,17 +15,21 @@ struct fi_precond {
     fib::DevBuf<float> Hf;      // FP32 copy for the refinement sweep
     fib::DevBuf<double> rbuf, dbuf;  // refinement residual and correction
     fib::DevBuf<double> d2inv;  // S x Np: 1 / D2 (pads 0)
-    fib::DevBuf<double> xbuf;   // Np
-    fib::DevBuf<double> pbuf;   // nb * nb * 64 partial products
-    fib::DevBuf<unsigned> bar;  // grid barrier counter
+    fib::DevBuf<double> xbuf;   // 2 x Np (pass parity)
+    fib::DevBuf<double> pbuf;   // 2 x nb x nb x 64 partial products (pass parity)
+    fib::DevBuf<unsigned> counters;  // xready[nb], pdone[nb], grid barrier
     fib::DevBuf<double> zbuf, ybuf;  // padded scratch for reference-layout applies
 };
 
 namespace fib {
+// sweep dataflow counters are kept one 128-byte L2 line apart (unsigned units)
+constexpr int kCounterStride = 32;
 // y = P^{-1} z on padded vectors (K2).  levels = S+1 (full P) or S (time levels only:
 // the forward solve, system.cpp:192-224).  skip: optional device flag.
 void precond_apply(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip);
 void precond_build(fi_precond* P);
+// cooperative grid size of the sweep kernel for T tiles per level and Np rows
+int precond_apply_grid(fi_ctx* ctx, long long T, long long Np);
 // z_s = b_{s-1} D1_s o rho + eta q_s f (padded, levels 0..S-1): forward-solve right-hand side.
 void forward_rhs(fi_ctx* ctx, const fi_system* sys, const double* rho_pad, const double* f_pad, double* z_pad);
 }  // namespace fib

@@ -112,9 +112,9 @@ class Context:
     def kernel_launches(self) -> int:
         return int(lib.fi_ctx_kernel_launches(self.handle))
 
-    def __del__(self):
-        if getattr(self, "handle", None) and not _SHUTDOWN[0]:
-            lib.fi_ctx_destroy(self.handle)
+    def __del__(self, _shutdown=_SHUTDOWN, _lib=lib):
+        if getattr(self, "handle", None) and not _shutdown[0]:
+            _lib.fi_ctx_destroy(self.handle)
             self.handle = None
 
 
@@ -422,9 +422,9 @@ class SystemOperator:
 
     __call__ = apply
 
-    def __del__(self):
-        if getattr(self, "handle", None) and not _SHUTDOWN[0]:
-            lib.fi_system_destroy(self.handle)
+    def __del__(self, _shutdown=_SHUTDOWN, _lib=lib):
+        if getattr(self, "handle", None) and not _shutdown[0]:
+            _lib.fi_system_destroy(self.handle)
             self.handle = None
 
 
@@ -468,9 +468,9 @@ class BlockTriangularPreconditioner:
 
     __call__ = apply
 
-    def __del__(self):
-        if getattr(self, "handle", None) and not _SHUTDOWN[0]:
-            lib.fi_precond_destroy(self.handle)
+    def __del__(self, _shutdown=_SHUTDOWN, _lib=lib):
+        if getattr(self, "handle", None) and not _shutdown[0]:
+            _lib.fi_precond_destroy(self.handle)
             self.handle = None
 
 
