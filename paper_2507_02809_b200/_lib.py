@@ -99,7 +99,8 @@ _SIGS = {
 def declared_symbols():
     """Every `fi_*` function declared in include/fracinv_b200.h."""
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(fi_[a-z0-9_]+)\s*\(", text)) - {"fi_linop_fn"})
+    decl = re.compile(r"^(?:int|void|long long|const char\s*\*|void\s*\*)\s*\*?\s*(fi_[a-z0-9_]+)\s*\(", re.M)
+    return sorted(set(decl.findall(text)))
 
 
 def load():

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(RT) reduce_kernel(ReduceArgs a) {
 }
 
 // K4: Hessenberg column + Givens update for Arnoldi step k of the cycle (krylov.cpp:141-185).
-__global__ void givens_kernel(GmresState* st, int k, int maxit, double* hist) {
+__global__ void givens_kernel(GmresState* st, int k, int maxit, double* hist, volatile int* done_host) {
     if (st->done) return;
     const double hnext = sqrt(st->hnorm2);
     double* h = st->h;
@@ -183,6 +183,8 @@ __global__ void givens_kernel(GmresState* st, int k, int maxit, double* hist) {
     if (denom <= 1e-14 * col_scale || denom == 0.0) {
         st->breakdown = 1;
         st->done = 1;
+        __threadfence_system();
+        *done_host = 1;
         return;
     }
     st->cs[k] = h[k] / denom;
@@ -204,6 +206,10 @@ __global__ void givens_kernel(GmresState* st, int k, int maxit, double* hist) {
         st->done = 1;
     } else if (st->iters >= maxit) {
         st->done = 1;
+    }
+    if (st->done) {
+        __threadfence_system();
+        *done_host = 1;  // host-mapped: lets the host stop enqueueing without a device sync
     }
 }
 
@@ -250,6 +256,9 @@ __global__ void scale_by_kernel(const double* src, double* dst, long long n, con
 
 GmresEngine::GmresEngine(fi_ctx* ctx, long long n) : ctx_(ctx), n_(n) {
     grid_ = ctx->sm_count * 4;
+    FI_CUDA(cudaHostAlloc((void**)&done_host_, sizeof(int), cudaHostAllocMapped));
+    FI_CUDA(cudaHostGetDevicePointer((void**)&done_hmap_, (void*)done_host_, 0));
+    for (auto& e : iter_ev_) FI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     partials_.alloc((size_t)2 * grid_);
     ticket_.alloc(1);
     FI_CUDA(cudaMemsetAsync(ticket_.p, 0, sizeof(unsigned), ctx->stream));
@@ -411,7 +420,15 @@ void GmresEngine::solve(const Op& A, const Op* M, const double* b, const double*
         const int steps = std::min(cycle, maxit - iters);
         const int* done = field_dev<int>(st_d.p, offsetof(GmresState, done));
         const int* reorth = field_dev<int>(st_d.p, offsetof(GmresState, reorth));
+        *done_host_ = 0;
         for (int k = 0; k < steps; ++k) {
+            // Look-ahead: before enqueueing step k, wait (host side) only for step k - kLook to have
+            // finished and read its convergence flag from host-mapped memory.  The GPU always has
+            // kLook steps queued, and at most kLook no-op steps are enqueued past convergence.
+            if (k >= kLook) {
+                FI_CUDA(cudaEventSynchronize(iter_ev_[k % kLook]));
+                if (*(volatile int*)done_host_) break;
+            }
             const double* vk = V.p + (long long)k * ldv;
             if (M) {
                 A(vk, t1.p, done);
@@ -431,10 +448,11 @@ void GmresEngine::solve(const Op& A, const Op* M, const double* b, const double*
                 reduce(w.p, V.p + (long long)(i - 1) * ldv, hs.c + (i - 1), V.p + (long long)i * ldv, RM_ROUND, k, i,
                        hs.c, reorth, done);
             reduce(w.p, V.p + (long long)k * ldv, hs.c + k, nullptr, RM_FINAL2, k, 0, nullptr, reorth, done);
-            givens_kernel<<<1, 1, 0, s>>>(st_d.p, k, maxit, hist_d.p);
+            givens_kernel<<<1, 1, 0, s>>>(st_d.p, k, maxit, hist_d.p, done_hmap_);
             FI_LAUNCHED(ctx_);
             scale_kernel<<<blocks, 256, 0, s>>>(w.p, V.p + (long long)(k + 1) * ldv, n, st_d.p);
             FI_LAUNCHED(ctx_);
+            FI_CUDA(cudaEventRecord(iter_ev_[k % kLook], s));
         }
         download_state();
         // history entries of this cycle
@@ -467,4 +485,12 @@ void GmresEngine::solve(const Op& A, const Op* M, const double* b, const double*
     finish(converged, breakdown, iters);
 }
 
+}  // namespace fib
+
+namespace fib {
+GmresEngine::~GmresEngine() {
+    for (auto& e : iter_ev_)
+        if (e) cudaEventDestroy(e);
+    if (done_host_) cudaFreeHost(done_host_);
+}
 }  // namespace fib

@@ -40,6 +40,9 @@ using Op = std::function<void(const double* x, double* y, const int* skip)>;
 class GmresEngine {
 public:
     GmresEngine(fi_ctx* ctx, long long n);
+    ~GmresEngine();
+    GmresEngine(const GmresEngine&) = delete;
+    GmresEngine& operator=(const GmresEngine&) = delete;
     long long n() const { return n_; }
     // Reference semantics of gmres() (krylov.cpp:72-209) + restart extension.
     void solve(const Op& A, const Op* M, const double* b, const double* x0, double* x, double tol, int maxit,
@@ -63,6 +66,10 @@ private:
     DevBuf<unsigned> ticket_;
     DevBuf<double> V_, w_, t1_, t2_, hist_, arr_, ycoef_;
     DevBuf<GmresState> st_buf_;
+    static constexpr int kLook = 2;  // Arnoldi steps kept queued ahead of the host's convergence check
+    int* done_host_ = nullptr;       // pinned, host-mapped copy of the device `done` flag
+    int* done_hmap_ = nullptr;       // its device alias
+    cudaEvent_t iter_ev_[kLook] = {};
 };
 
 }  // namespace fib
