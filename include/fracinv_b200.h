@@ -93,6 +93,7 @@ typedef struct {
     const double* q;
     const double* D1;
     const double* D2;
+    double omega;   /* space order (used by the tau preconditioner of 2D blocks; 0 = unknown) */
 } fi_system_desc;
 
 int fi_system_create(fi_ctx* ctx, const fi_system_desc* desc, fi_system** out);
@@ -110,6 +111,14 @@ int fi_system_apply_host(fi_system* sys, const double* y_host, double* z_host);
  * returns FI_E_RESOURCE like the reference.  Singular blocks return FI_E_SINGULAR with
  * the 1-based time index (S+1 = regularisation block). */
 int fi_precond_create(fi_system* sys, long long block_cap, fi_precond** out);
+/* Explicit choice of the per-block solve.  inner = 0: dense (the reference's direct solve, above
+ * block_cap -> FI_E_RESOURCE); inner = 1: tau-preconditioned CG per block to relative residual
+ * `tol` (at most `maxit` steps) — the substituted solve for 2D blocks beyond the cap (needs
+ * n_i + 1 a power of two); inner = -1: what fi_precond_create does (dense up to block_cap, tau-PCG
+ * above it for 2D). */
+int fi_precond_create_ex(fi_system* sys, long long block_cap, int inner, double tol, int maxit, fi_precond** out);
+/* 0 = dense inverses, 1 = tau-PCG per block. */
+int fi_precond_inner(const fi_precond* P);
 void fi_precond_destroy(fi_precond* P);
 /* y = P^{-1} z (forward block substitution), device vectors, async. */
 int fi_precond_apply(fi_precond* P, const double* z_dev, double* y_dev);

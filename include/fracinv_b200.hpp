@@ -179,6 +179,7 @@ public:
         desc.q = q_.data();
         desc.D1 = D1_.data();
         desc.D2 = D2_.data();
+        desc.omega = spec.omega;
         check(fi_system_create(ctx.handle(), &desc, &h_));
     }
     ~SystemOperator() { fi_system_destroy(h_); }

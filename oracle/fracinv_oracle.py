@@ -534,22 +534,29 @@ class ForwardSolution:
     mu: np.ndarray
 
 
-def forward_solve(A: SystemOperator, f_source: Optional[np.ndarray] = None) -> ForwardSolution:
-    """system.cpp:192-224: block forward substitution with dense LU per level."""
+def forward_solve(A: SystemOperator, f_source: Optional[np.ndarray] = None,
+                  P: Optional["BlockTriangularPreconditioner"] = None) -> ForwardSolution:
+    """system.cpp:192-224: block forward substitution with dense LU per level.
+
+    EXTENSION: with P given, each level's block G_s (identical to P's time blocks) is solved by
+    P.solve_block — the substituted solve for 2D blocks whose dense LU is infeasible."""
     N, S = A.space_dim, A.steps
     e, b = A.weights.e, A.weights.b
     eta = A.spec.tgrid.eta
     f = A.spec.f_true if f_source is None else f_source
-    Bd = A.laplacian.dense(N)
+    Bd = A.laplacian.dense(N) if P is None else None
     states: List[np.ndarray] = []
     for s in range(1, S + 1):
         d1 = A.diags.D1[s - 1]
         d2 = A.diags.D2[s - 1]
-        blk = A.scale_space * d2[:, None] * Bd
-        blk[np.diag_indices(N)] += e[0] * d1
         rhs = b[s - 1] * (d1 * A.spec.rho) + eta * A.q[s - 1] * f
         for m in range(1, s):
             rhs = rhs - e[s - m] * (d1 * states[m - 1])
+        if P is not None:
+            states.append(P.solve_block(s, rhs))
+            continue
+        blk = A.scale_space * d2[:, None] * Bd
+        blk[np.diag_indices(N)] += e[0] * d1
         lu = _lu_checked(blk, s, "forward_solve")
         states.append(sla.lu_solve(lu, rhs, check_finite=False))
     return ForwardSolution(states, states[-1])
@@ -661,10 +668,21 @@ class BlockTriangularPreconditioner:
 
     kDefaultBlockCap = 4096
 
-    def __init__(self, A: SystemOperator, block_cap: int = kDefaultBlockCap, cache: bool = True):
+    def __init__(self, A: SystemOperator, block_cap: int = kDefaultBlockCap, cache: bool = True,
+                 inner: str = "auto", tol: float = 1e-14, maxit: int = 200):
+        """inner="lu": the reference (dense PartialPivLU per block; ResourceLimitError above the cap).
+        inner="pcg": EXTENSION, the substituted per-block solve of SURVEY 7.3 #1 (tau-preconditioned
+        CG on the SPD form, identical to the device's).  inner="auto": "lu" unless the problem is 2D
+        and N exceeds the cap, where the reference cannot run at all (config 2-4)."""
         self.A = A
         self.N = A.space_dim
         self.S = A.steps
+        if inner == "auto":
+            inner = "pcg" if (A.spec.sgrid.d == 2 and self.N > block_cap) else "lu"
+        self.inner = inner
+        if inner == "pcg":
+            self.pcg = TauPCG(A, tol, maxit)
+            return
         if self.N > block_cap:
             raise ResourceLimitError(
                 f"BlockTriangularPreconditioner: block dimension {self.N} exceeds cap {block_cap}")
@@ -695,6 +713,8 @@ class BlockTriangularPreconditioner:
         return _lu_checked(self.block(s), s, "precond_build")
 
     def solve_block(self, s: int, rhs: np.ndarray) -> np.ndarray:
+        if self.inner == "pcg":
+            return self.pcg.solve(s, rhs)
         return sla.lu_solve(self._factor(s), rhs, check_finite=False)
 
     def apply(self, z: np.ndarray) -> np.ndarray:
@@ -716,6 +736,88 @@ class BlockTriangularPreconditioner:
         rhs = z[S * N:] - Y[S - 1]
         y[S * N:] = self.solve_block(S + 1, rhs)
         return y
+
+
+class TauPCG:
+    """EXTENSION: exact-to-tolerance per-block solve for blocks too large to factor.
+
+    G_s y = r with G_s = D2_s (c M0 + diag(delta_s)), c = eta/h^w, delta = e0 D1/D2 (time levels);
+    G_f = cr D2_S B (f-block, delta = 0).  Solved as M y = r / D2 with M = c B + diag(delta) SPD, by
+    CG preconditioned with the tau matrix  tau^{-1} = S diag(1/(c g(theta_j) + mean(delta))) S,
+    S the orthonormal DST-I, g the symbol (sum_i 4 sin^2(theta_i/2))^{w/2} at theta_j = j pi/(n+1).
+    x0 = 0; stop when ||r_k|| <= tol ||b|| (2-norm) or after maxit steps.  The device (precond_iter.cu)
+    runs the same recurrence in the same order of operations.
+    """
+
+    def __init__(self, A: SystemOperator, tol: float = 1e-14, maxit: int = 200):
+        import scipy.fft as sf
+        self.sf = sf
+        self.A = A
+        self.tol, self.maxit = tol, maxit
+        self.n = list(A.spec.sgrid.n)
+        th = [np.arange(1, ni + 1) * math.pi / (ni + 1) for ni in self.n]
+        acc = 0.0
+        for i, t in enumerate(th):
+            shape = [1] * len(self.n)
+            shape[i] = self.n[i]
+            acc = acc + (4.0 * np.sin(t / 2.0) ** 2).reshape(shape)
+        self.g = np.power(acc, A.spec.orders.omega / 2.0)
+        self.iterations = []
+        S, N = A.steps, A.space_dim
+        e0 = A.weights.e[0]
+        for s in range(1, S + 1):
+            d2 = A.diags.D2[s - 1]
+            if np.all(d2 == 0.0):
+                continue
+            if np.any(d2 == 0.0) or np.any(A.diags.D1[s - 1] / d2 < 0.0):
+                raise ValueError("TauPCG needs gamma2 != 0 and gamma1/gamma2 >= 0 per level")
+        if np.any(A.diags.D2[S - 1] == 0.0):
+            raise SingularBlockError(f"precond_build: singular block at time level {S + 1}", S + 1)
+
+    def _tau_inv(self, r, lam):
+        R = r.reshape(self.n)
+        X = self.sf.dstn(R, type=1, norm="ortho")
+        X /= lam
+        return self.sf.idstn(X, type=1, norm="ortho").reshape(-1)
+
+    def solve(self, s: int, rhs: np.ndarray) -> np.ndarray:
+        A = self.A
+        S = A.steps
+        e0 = A.weights.e[0]
+        if s <= S:
+            d1, d2 = A.diags.D1[s - 1], A.diags.D2[s - 1]
+            if np.all(d2 == 0.0):
+                return rhs / (e0 * d1)
+            c, delta = A.scale_space, e0 * d1 / d2
+        else:
+            d2 = A.diags.D2[S - 1]
+            c, delta = A.scale_reg, np.zeros(A.space_dim)
+        b = rhs / d2
+        lam = c * self.g + delta.mean()
+        M = lambda v: c * A.laplacian.apply(v) + delta * v
+        x = np.zeros_like(b)
+        bn = np.linalg.norm(b)
+        if bn == 0.0:
+            self.iterations.append(0)
+            return x
+        r = b.copy()
+        z = self._tau_inv(r, lam)
+        p = z.copy()
+        rz = float(r @ z)
+        it = 0
+        for it in range(1, self.maxit + 1):
+            Ap = M(p)
+            alpha = rz / float(p @ Ap)
+            x += alpha * p
+            r -= alpha * Ap
+            if np.linalg.norm(r) <= self.tol * bn:
+                break
+            z = self._tau_inv(r, lam)
+            rz_new = float(r @ z)
+            p = z + (rz_new / rz) * p
+            rz = rz_new
+        self.iterations.append(it)
+        return x
 
 
 # --------------------------------------------------------------------------- GMRES

@@ -33,6 +33,7 @@ class SystemDesc(ctypes.Structure):
         ("q", c_double_p),
         ("D1", c_double_p),
         ("D2", c_double_p),
+        ("omega", ctypes.c_double),
     ]
 
 
@@ -83,6 +84,9 @@ _SIGS = {
     "fi_precond_apply_timed": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, ctypes.c_int, c_double_p]),
     "fi_precond_bytes": (ctypes.c_longlong, [c_void_p]),
     "fi_precond_set_refine": (ctypes.c_int, [c_void_p, ctypes.c_int]),
+    "fi_precond_create_ex": (ctypes.c_int, [c_void_p, ctypes.c_longlong, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                             ctypes.POINTER(c_void_p)]),
+    "fi_precond_inner": (ctypes.c_int, [c_void_p]),
     "fi_build_rhs": (ctypes.c_int, [c_void_p, c_double_p, c_double_p, c_double_p]),
     "fi_forward_solve": (ctypes.c_int, [c_void_p, c_void_p, c_double_p, c_double_p, c_double_p, c_double_p]),
     "fi_gmres": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, ctypes.POINTER(GmresOpts),

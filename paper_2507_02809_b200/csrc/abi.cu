@@ -82,15 +82,22 @@ void unpack_levels(fi_ctx* ctx, const fib::Layout& L, const double* pad, double*
     FI_LAUNCHED(ctx);
 }
 
-fi_precond* build_precond(fi_system* sys, long long block_cap) {
+// mode: 0 = dense inverses (the reference's per-block direct solve), 1 = tau-PCG per block,
+//       -1 = automatic: dense up to the cap; above it, tau-PCG for 2D (the reference raises
+//       ResourceLimitError there), ResourceLimitError for 1D as in the reference.
+fi_precond* build_precond(fi_system* sys, long long block_cap, int mode = -1, double tol = 1e-14, int maxit = 200) {
     if (block_cap <= 0) block_cap = 4096;  // BlockTriangularPreconditioner::kDefaultBlockCap
-    if (sys->L.N > block_cap)
+    if (mode < 0) mode = (sys->L.N > block_cap && fib::iterative_supported(sys->L)) ? 1 : 0;
+    if (mode == 0 && sys->L.N > block_cap)
         throw fib::Error(FI_E_RESOURCE, "BlockTriangularPreconditioner: block dimension " + std::to_string(sys->L.N) +
                                             " exceeds cap " + std::to_string(block_cap));
+    if (mode == 1 && !(sys->omega > 0.0))
+        throw fib::Error(FI_E_DOMAIN, "tau-PCG preconditioner needs fi_system_desc.omega");
     fi_precond* P = new fi_precond();
     P->sys = sys;
     try {
-        fib::precond_build(P);
+        if (mode == 1) fib::precond_build_iterative(P, tol, maxit);
+        else fib::precond_build(P);
         P->zbuf.alloc((size_t)sys->L.nI());
         P->ybuf.alloc((size_t)sys->L.nI());
         FI_CUDA(cudaStreamSynchronize(sys->ctx->stream));
@@ -195,6 +202,7 @@ int fi_system_create(fi_ctx* ctx, const fi_system_desc* desc, fi_system** out) {
             sys->eta = desc->eta;
             sys->cs = desc->scale_space;
             sys->cr = desc->scale_reg;
+            sys->omega = desc->omega;
             const int n1 = L.n1, n2 = L.n2;
             const size_t gsz = (size_t)(2 * n1 - 1) * (2 * n2 - 1);
             sys->gen_h.assign(desc->gen, desc->gen + gsz);
@@ -305,6 +313,18 @@ int fi_precond_create(fi_system* sys, long long block_cap, fi_precond** out) {
     });
 }
 
+int fi_precond_create_ex(fi_system* sys, long long block_cap, int inner, double tol, int maxit, fi_precond** out) {
+    return guard([&] {
+        require(sys && out, FI_E_DOMAIN, "fi_precond_create_ex: NULL argument");
+        require(inner >= -1 && inner <= 1, FI_E_DOMAIN, "fi_precond_create_ex: inner must be -1, 0 or 1");
+        require(tol > 0.0 && maxit > 0, FI_E_DOMAIN, "fi_precond_create_ex: tol > 0 and maxit > 0 required");
+        *out = build_precond(sys, block_cap, inner, tol, maxit);
+        sys->refs++;
+    });
+}
+
+int fi_precond_inner(const fi_precond* P) { return P ? P->mode : -1; }
+
 void fi_precond_destroy(fi_precond* P) {
     if (!P) return;
     fi_system* sys = P->sys;
@@ -391,7 +411,7 @@ int fi_forward_solve(fi_system* sys, fi_precond* P, const double* rho_host, cons
         if (!P) {
             // forward_solve assembles its blocks regardless of the preconditioner cap
             // (system.cpp:198: dense(N)), so the temporary build uses cap = N
-            own = build_precond(sys, L.N);
+            own = fib::iterative_supported(L) && L.N > 4096 ? build_precond(sys, 4096) : build_precond(sys, L.N);
             P = own;
         }
         try {

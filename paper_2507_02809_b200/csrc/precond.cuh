@@ -19,6 +19,29 @@ struct fi_precond {
     fib::DevBuf<double> pbuf;   // 2 x nb x nb x 64 partial products (pass parity)
     fib::DevBuf<unsigned> counters;  // xready[nb], pdone[nb], grid barrier
     fib::DevBuf<double> zbuf, ybuf;  // padded scratch for reference-layout applies
+
+    // ---- mode 1: substituted per-block solve (tau-preconditioned CG, precond_iter.cu)
+    int mode = 0;  // 0 = dense packed inverses, 1 = tau-PCG per level
+    double it_tol = 1e-14;
+    int it_maxit = 200;
+    int it_L1 = 0, it_L2 = 0;
+    std::vector<double> it_dmean;
+    std::vector<int> it_direct;
+    fib::DevBuf<double2> it_tw1, it_tw2, it_X;
+    fib::DevBuf<double> it_lamT, it_lamB, it_Rr, it_vec, it_partials, it_state, it_dmean_d;
+    fib::DevBuf<int> it_direct_d, it_level;
+    fib::DevBuf<unsigned> it_ticket;
+    fib::DevBuf<unsigned long long> it_kcount;  // kernels executed inside the CG graphs
+    struct GraphEntry {
+        const double* z;
+        double* y;
+        int levels;
+        const int* skip;
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+    };
+    std::vector<GraphEntry> it_graphs;
+    ~fi_precond();
 };
 
 namespace fib {
@@ -27,6 +50,10 @@ constexpr int kCounterStride = 32;
 // y = P^{-1} z on padded vectors (K2).  levels = S+1 (full P) or S (time levels only:
 // the forward solve, system.cpp:192-224).  skip: optional device flag.
 void precond_apply(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip);
+// mode 1 (2D blocks above the dense cap): build / apply of the tau-PCG per-level solve
+bool iterative_supported(const Layout& L);
+void precond_build_iterative(fi_precond* P, double tol, int maxit);
+void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip);
 void precond_build(fi_precond* P);
 // cooperative grid size of the sweep kernel for T tiles per level and Np rows
 int precond_apply_grid(fi_ctx* ctx, long long T, long long Np);

@@ -577,6 +577,10 @@ int precond_apply_grid(fi_ctx* ctx, long long T, long long Np) {
 }
 
 void precond_apply(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip) {
+    if (P->mode == 1) {
+        precond_apply_iterative(ctx, P, z, y, levels, skip);
+        return;
+    }
     const fi_system* sys = P->sys;
     const bool full = levels == sys->L.S + 1;
     // sweep 1: forward block substitution with the FP64 inverses (+ in-kernel f-block refinement)

@@ -29,7 +29,7 @@ struct fi_system {
     int refs = 1;
     fi_ctx* ctx = nullptr;
     fib::Layout L;
-    double h = 0, eta = 0, cs = 0, cr = 0;
+    double h = 0, eta = 0, cs = 0, cr = 0, omega = 0;
     std::vector<double> gen_h, e_h, b_h, q_h, D1_h, D2_h;  // host copies (reference layout)
     fib::DevBuf<double> gen, epad, D1, D2, q, e, bw;
     fib::DevBuf<double> ubuf, zbuf;  // padded scratch for reference-layout applies

@@ -381,6 +381,7 @@ class SystemOperator:
         desc.eta = spec.tgrid.eta
         desc.scale_space = self.scale_space
         desc.scale_reg = self.scale_reg
+        desc.omega = spec.orders.omega
         desc.gen, desc.e, desc.b, desc.q, desc.D1, desc.D2 = [_dp(a) for a in self._keep]
         h = ctypes.c_void_p()
         _check(lib.fi_system_create(self.ctx.handle, ctypes.byref(desc), ctypes.byref(h)))
@@ -433,11 +434,20 @@ class BlockTriangularPreconditioner:
 
     kDefaultBlockCap = 4096
 
-    def __init__(self, A: SystemOperator, block_cap: int = kDefaultBlockCap):
+    def __init__(self, A: SystemOperator, block_cap: int = kDefaultBlockCap, inner: str = "auto",
+                 tol: float = 1e-14, maxit: int = 200):
+        """inner="lu" (dense per-block solve, the reference; N > block_cap -> ResourceLimitError),
+        "pcg" (EXTENSION: tau-preconditioned CG per block), or "auto" (dense up to
+        the cap, tau-PCG above it for 2D — configs 2-4, which the reference cannot run)."""
         self.A = A
+        mode = {"auto": -1, "lu": 0, "pcg": 1}[inner]
         h = ctypes.c_void_p()
-        _check(lib.fi_precond_create(A.handle, int(block_cap), ctypes.byref(h)))
+        _check(lib.fi_precond_create_ex(A.handle, int(block_cap), mode, float(tol), int(maxit), ctypes.byref(h)))
         self.handle = h
+
+    @property
+    def inner(self) -> str:
+        return "pcg" if lib.fi_precond_inner(self.handle) == 1 else "lu"
 
     def dim(self) -> int:
         return self.A.dim()

@@ -1,0 +1,54 @@
+#!/usr/bin/env python3
+"""Run the CPU oracle once per BASELINE config and store its GMRES(50) solve as a golden file.
+
+For each config: the observation mu_eps (forward solve of f* + seeded Gaussian noise), the
+oracle's iteration count, residual history, final true residual and recovered f.  The GPU tests
+feed the same mu_eps to the device path and compare against these (iterations +-1, f <= 1e-8).
+1D blocks use the reference's dense LU (config 1: refactored per apply, 68.8 GB of factors do not
+fit in host RAM); 2D blocks use the substituted tau-PCG solve.
+Usage: python tests/golden/gen_oracle_solutions.py 2 3 ...   (writes tests/golden/oracle_config<i>.npz)
+"""
+import os
+import sys
+import time
+import warnings
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+warnings.filterwarnings("ignore")
+
+from oracle import fracinv_oracle as O  # noqa: E402
+from paper_2507_02809_b200.configs import NOISE, RESTART, SEED_BASE, TOL, baseline_problem  # noqa: E402
+
+
+def run(cfg, precond=True):
+    t0 = time.time()
+    A = O.SystemOperator(baseline_problem(O, cfg))
+    P = O.BlockTriangularPreconditioner(A, cache=(cfg != 1))
+    Pfs = P if P.inner == "pcg" else None
+    mu = O.forward_solve(A, P=Pfs).mu if cfg != 1 else O.forward_solve(A, P=P).mu
+    mu_eps = O.add_gaussian_noise(mu, NOISE[cfg], SEED_BASE + cfg)
+    z = O.build_rhs(A, mu_eps).z
+    t1 = time.time()
+    x, rep = O.gmres(A.apply, P.apply if precond else None, z, tol=TOL[cfg], restart=RESTART,
+                     maxit=0 if precond else 2000)
+    t2 = time.time()
+    f = x[-A.N:]
+    name = f"oracle_config{cfg}{'' if precond else '_unprec'}.npz"
+    np.savez_compressed(os.path.join(HERE, name), mu_eps=mu_eps, f=f, iterations=rep.iterations,
+                        history=np.array(rep.residual_history), final_true_residual=rep.final_true_residual,
+                        converged=rep.converged, recon_error=O.relative_error(A.spec.f_true, f),
+                        setup_s=t1 - t0, solve_s=t2 - t1, inner=P.inner)
+    print(f"config {cfg}: {rep.iterations} iterations, converged {rep.converged}, setup {t1 - t0:.1f}s, "
+          f"solve {t2 - t1:.1f}s -> {name}", flush=True)
+
+
+if __name__ == "__main__":
+    for arg in sys.argv[1:]:
+        if arg.endswith("u"):
+            run(int(arg[:-1]), precond=False)
+        else:
+            run(int(arg))
