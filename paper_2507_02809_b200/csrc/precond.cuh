@@ -19,6 +19,10 @@ struct fi_precond {
     fib::DevBuf<double> pbuf;   // 2 x nb x nb x 64 partial products (pass parity)
     fib::DevBuf<unsigned> counters;  // xready[nb], pdone[nb], grid barrier
     fib::DevBuf<double> zbuf, ybuf;  // padded scratch for reference-layout applies
+    // merged refinement sweep (precond_sweep_ir.cu), allocated on first use
+    fib::DevBuf<double> ir_xb;        // 3 kinds x 2 parities x Np
+    fib::DevBuf<double> ir_pb;        // 3 kinds x 2 parities x nb x nb x 64
+    fib::DevBuf<unsigned> ir_counters;  // xready[nb], pdone[3][nb]
 
     // ---- mode 1: substituted per-block solve (tau-preconditioned CG, precond_iter.cu)
     int mode = 0;  // 0 = dense packed inverses, 1 = tau-PCG per level
@@ -55,6 +59,9 @@ bool iterative_supported(const Layout& L);
 void precond_build_iterative(fi_precond* P, double tol, int maxit);
 void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip);
 void precond_build(fi_precond* P);
+// merged sweep: forward substitution + one refinement step in one persistent kernel (K2)
+bool sweep_ir_available(const fi_precond* P);
+void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip);
 // cooperative grid size of the sweep kernel for T tiles per level and Np rows
 int precond_apply_grid(fi_ctx* ctx, long long T, long long Np);
 // z_s = b_{s-1} D1_s o rho + eta q_s f (padded, levels 0..S-1): forward-solve right-hand side.

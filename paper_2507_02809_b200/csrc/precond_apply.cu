@@ -583,6 +583,11 @@ void precond_apply(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int l
     }
     const fi_system* sys = P->sys;
     const bool full = levels == sys->L.S + 1;
+    if (P->refine && sweep_ir_available(P)) {
+        // sweep + residual + refinement sweep interleaved in one persistent kernel
+        launch_sweep_ir(ctx, P, z, y, levels, skip);
+        return;
+    }
     // sweep 1: forward block substitution with the FP64 inverses (+ in-kernel f-block refinement)
     launch_sweep<double>(ctx, P, P->H.p, z, y, levels, full ? 1 : 0, skip);
     if (!P->refine) return;

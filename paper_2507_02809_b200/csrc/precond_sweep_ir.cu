@@ -1,0 +1,705 @@
+// K2 (refined) — forward block substitution AND its iterative refinement in ONE persistent sweep.
+//
+// P^{-1} z with LU-grade accuracy needs one refinement step on top of the explicit-inverse sweep
+// (DESIGN §6):  y1 = P~^{-1} z (FP64 inverses),  r = z - P y1 (exact FP64 residual),
+// d = P~^{-1} r (FP32 inverses),  y = y1 + d.  Run as separate kernels that is two sequential
+// S-level dependency chains plus an operator launch.  Here the three are interleaved with a lag in
+// one cooperative kernel that pays for ONE chain:
+//   step t:  tiles of H64_t x1_t          (sweep 1, level t)
+//            tiles of B y1_{t-1}          (residual of level t-1: B generated from its symbol)
+//            tiles of H32_{t-2} x2_{t-2}  (sweep 2, level t-2)
+//   owner at the start of step t reduces the three partial products of step t-1 and publishes
+//   x1_t, y1_{t-1}, x2_{t-2} behind one per-row-block release counter.
+// The producer warp streams the FP64 and FP32 tiles of each step with cp.async.bulk (TMA) into the
+// mbarrier ring; B tiles are generated in registers (no HBM traffic); spare warps accumulate the
+// three L1 history sums of the next step from the CTA's own rows.  Synchronisation is the same
+// dataflow as sweep_kernel (precond_apply.cu): warp-uniform acquire polls on per-row-block
+// counters, one release fence per warp and step, fixed-order (bit-reproducible) reductions.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "precond.cuh"
+
+namespace fib {
+namespace {
+
+constexpr int TB = 64;
+constexpr int TILE = TB * TB;
+constexpr int NW = 11;                  // worker warps; + 1 producer = 12 warps (3 per SMSP)
+constexpr int NWT = NW * 32;
+constexpr int THREADS = NWT + 32;
+constexpr int NST = 6;                  // ring slots of 32 KiB (an FP32 tile uses half a slot)
+constexpr int SLOT = TILE;              // doubles per slot
+constexpr int NB_W = NW - NST;          // warps for the generated B tiles and the history sums
+constexpr int RCAP = 32;   // owned rows per CTA: one per lane
+constexpr int CSTR = kCounterStride;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// streaming variant: the tiles are read once, so they are marked evict-first in L2 and do not push
+// out the sweep's small, re-read working set (x, partial products, history rows)
+__device__ __forceinline__ void tma_bulk_g2s_stream(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                                    uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void worker_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NWT) : "memory"); }
+__device__ __forceinline__ void bwarp_bar() { asm volatile("bar.sync 2, %0;\n" ::"n"(NB_W * 32) : "memory"); }
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_relaxed(unsigned* p, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// warp-uniform poll (all 32 lanes): the warp never diverges, so later shfl.sync stay cheap
+__device__ __forceinline__ void warp_spin_until(const unsigned* p, unsigned target) {
+    while (!__all_sync(0xffffffffu, ld_acquire(p) >= target)) __nanosleep(64);
+}
+__device__ __forceinline__ void tile_coords(long long t, int& bi, int& bj) {
+    int r = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while ((long long)(r + 1) * (r + 2) / 2 <= t) ++r;
+    while ((long long)r * (r + 1) / 2 > t) --r;
+    bi = r;
+    bj = (int)(t - (long long)r * (r + 1) / 2);
+}
+__device__ __forceinline__ int owners_of_block(int rb, long long R, unsigned G) {
+    const long long first = (long long)rb * TB / R;
+    const long long last = min((long long)G - 1, ((long long)rb * TB + TB - 1) / R);
+    return (int)(last - first + 1);
+}
+
+struct IrArgs {
+    const double* H64;
+    const float* H32;
+    long long T;
+    int nb, nlev, S, n1, n2, ld2, gen_stride;
+    long long Np;
+    const double* z;
+    double* y;    // output y1 + d
+    double* Y1;   // sweep-1 result, all levels
+    double* DL;   // sweep-2 correction, all levels
+    const double* D1;
+    const double* D2;
+    const double* d2inv;
+    const double* e;
+    const double* gen;
+    const double* epad;  // e with zero padding: epad[k] = e_k for 0 <= k < S
+    double cs, cr;
+    double* xb;   // [3 kinds][2 parities][Np]
+    double* pb;   // [3 kinds][2 parities][nb][nb][TB]
+    unsigned* xready;  // [nb] (stride CSTR)
+    unsigned* pdone;   // [3][nb] (stride CSTR)
+    const int* skip;
+    int evict_first;
+    unsigned long long* trace;  // optional [G][nsteps+1][8] phase timestamps (FI_SWEEP_TRACE=1)
+};
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Symmetric tile product for one warp: rowsums (H x_j) -> prow[0..63], colsums (H^T x_i) -> pcol.
+// Row r of the tile is fetched by hrow(r) as the lane's two columns (2 lane, 2 lane + 1).
+template <class RowFn>
+__device__ __forceinline__ void tile_product(RowFn hrow, double2 xj, const double* xi, double* prow, double* pcol,
+                                             bool diag, int lane) {
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        double pr[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            const int r = half * 32 + q;
+            const double2 hv = hrow(r);
+            pr[q] = hv.x * xj.x + hv.y * xj.y;
+            const double xr = xi[r];
+            c0 += hv.x * xr;
+            c1 += hv.y * xr;
+        }
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1) {
+            const bool upper = (lane & w) != 0;
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+                const double send = upper ? pr[i] : pr[i + w];
+                const double keep = upper ? pr[i + w] : pr[i];
+                pr[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+            }
+        }
+        prow[half * 32 + lane] = pr[0];
+    }
+    if (!diag) reinterpret_cast<double2*>(pcol)[lane] = make_double2(c0, c1);
+}
+
+__global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
+    if (a.skip && *a.skip) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* ring = reinterpret_cast<double*>(smem_raw);            // NST x SLOT
+    double* red = ring + NST * SLOT;                                // 3 x NW x 32
+    double* h1p = red + 3 * NW * 32;                                   // RCAP
+    double* hrp = h1p + RCAP;                                       // RCAP
+    double* h2p = hrp + RCAP;                                       // RCAP
+    double* bq = h2p + RCAP;                                        // RCAP: B y1 of the residual level
+    double* xis = bq + RCAP;                                        // NW x TB staging of x_i
+    double* hred = xis + NW * TB;                                   // NB_W x 96 history partials
+    double* segs = hred + NB_W * 96;                                // NB_W x 128 symbol segments
+    uint64_t* full = reinterpret_cast<uint64_t*>(segs + NB_W * 128);
+    uint64_t* empty = full + NST;
+
+    const unsigned G = gridDim.x;
+    const long long t0 = (long long)blockIdx.x * a.T / G;
+    const long long t1 = (long long)(blockIdx.x + 1) * a.T / G;
+    const long long ntiles = t1 - t0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nlev = a.nlev, S = a.S, nbb = a.nb;
+    const long long Np = a.Np;
+    const int nsteps = nlev + 2;  // tile steps 0..nlev+1; owner steps 1..nlev+2
+    const long long kstride = (long long)nbb * nbb * TB;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    auto h64_valid = [&](int t) { return t < nlev; };
+    auto h32_valid = [&](int t) { return t >= 2 && t - 2 < nlev; };
+
+    if (warp == NW) {
+        // ---------------- producer: per step, the FP64 tiles of level t then the FP32 tiles of level t-2
+        if (lane == 0) {
+            uint64_t policy;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(policy));
+            long long it = 0;
+            for (int t = 0; t < nsteps; ++t) {
+                for (int kind = 0; kind < 2; ++kind) {
+                    const bool ok = kind == 0 ? h64_valid(t) : h32_valid(t);
+                    if (!ok) continue;
+                    const int lv = kind == 0 ? t : t - 2;
+                    for (long long k = 0; k < ntiles; ++k, ++it) {
+                        const int slot = (int)(it % NST);
+                        if (it >= NST) mbar_wait(&empty[slot], (unsigned)((it / NST - 1) & 1));
+                        const long long tix = (long long)lv * a.T + t0 + k;
+                        const void* src = kind == 0 ? (const void*)(a.H64 + tix * TILE) : (const void*)(a.H32 + tix * TILE);
+                        const unsigned bytes = kind == 0 ? TILE * sizeof(double) : TILE * sizeof(float);
+                        mbar_expect_tx(&full[slot], bytes);
+                        if (a.evict_first)
+                            tma_bulk_g2s_stream(ring + slot * SLOT, src, bytes, &full[slot], policy);
+                        else
+                            tma_bulk_g2s(ring + slot * SLOT, src, bytes, &full[slot]);
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- workers
+    const long long R = (Np + G - 1) / G;
+    const long long r0 = min(Np, (long long)blockIdx.x * R);
+    const long long r1 = min(Np, r0 + R);
+    const int rb0 = (int)(r0 / TB), rb1 = r1 > r0 ? (int)((r1 - 1) / TB) : rb0 - 1;
+    long long it = 0;
+
+    // one owned row per lane (R <= 32, checked on the host)
+    const long long r = r0 + lane;
+    const bool rvalid = r < r1;
+    const long long rr = rvalid ? r : (r1 > r0 ? r0 : 0);  // clamped in-range row for inactive lanes
+    const bool pad = (int)(rr % a.ld2) >= a.n2;
+    const long long rb_own = rr / TB, ro_own = rr % TB;
+
+    for (int t = 0; t <= nsteps; ++t) {
+        unsigned long long* tr = a.trace ? a.trace + ((long long)blockIdx.x * (nsteps + 1) + t) * 8 : nullptr;
+        if (tr && threadIdx.x == 0) tr[0] = gtime();
+        // =============== owner step t: reduce the partials of step t-1 and publish
+        //   warp 0: y1_{t-1} -> Y1, x1_t and the B-tile input y1_{t-1}
+        //   warp 2: B y1_{t-2} and d_{t-3} -> DL, y, the residual r_{t-2} and x2_{t-2}
+        const bool kv0 = t >= 1 && t - 1 < nlev, kv1 = t >= 2 && t - 2 < nlev, kv2 = t >= 3 && t - 3 < nlev;
+        const bool do_x0 = t < nlev, do_x2 = t >= 2 && t - 2 < nlev;
+        // loads that do not depend on this step's partials are issued before the polls
+        double c_z = 0, c_d1 = 0, c_di = 0, c_d2 = 0, c_y = 0, c_h = 0, c_hr = 0;
+        if (warp == 0 && do_x0) {
+            if (t < S) {
+                const long long o = (long long)t * Np + rr;
+                c_z = a.z[o];
+                c_d1 = a.D1[o];
+                c_di = a.d2inv[o];
+            } else {
+                c_z = a.z[(long long)S * Np + rr];
+                c_di = a.d2inv[(long long)(S - 1) * Np + rr];
+            }
+        }
+        if (warp == 2) {
+            if (kv2) c_y = __ldcg(a.Y1 + (long long)(t - 3) * Np + rr);
+            if (do_x2) {
+                const int l = t - 2;
+                if (l < S) {
+                    const long long o = (long long)l * Np + rr;
+                    c_z = a.z[o];
+                    c_d1 = a.D1[o];
+                    c_d2 = a.D2[o];
+                    c_di = a.d2inv[o];
+                } else {
+                    const long long ol = (long long)(S - 1) * Np + rr;
+                    c_z = a.z[(long long)S * Np + rr];
+                    c_d1 = __ldcg(a.Y1 + ol);  // y1_{S-1}
+                    c_d2 = a.D2[ol];
+                    c_di = a.d2inv[ol];
+                }
+            }
+        }
+        if (t >= 1) {
+            const bool kv[3] = {kv0, kv1, kv2};
+            const unsigned target[3] = {(unsigned)(nbb * t), (unsigned)(nbb * (t - 1)), (unsigned)(nbb * (t - 2))};
+            // the (kind, row block) counters are polled by different warps in parallel
+            const int nrb = rb1 - rb0 + 1;
+            for (int q = warp; q < 3 * nrb; q += NW) {
+                const int kind = q / nrb, rb = rb0 + q % nrb;
+                if (kv[kind]) warp_spin_until(a.pdone + (kind * nbb + rb) * CSTR, target[kind]);
+            }
+            worker_bar();
+            if (tr && threadIdx.x == 0) tr[1] = gtime();
+            // history sums of step t-1 are read now: the spare warps overwrite them after the next barrier
+            if (warp == 0) c_h = h1p[lane];
+            if (warp == 2) {
+                c_h = h2p[lane];
+                c_hr = hrp[lane];
+            }
+            // every warp loads its ~nb / NW partials of all three kinds at once (fixed order)
+            const int par = (t - 1) & 1;
+#pragma unroll
+            for (int kind = 0; kind < 3; ++kind) {
+                double acc[2] = {0.0, 0.0};
+                if (kv[kind]) {
+                    const double* pbk = a.pb + (long long)(kind * 2 + par) * kstride + rb_own * nbb * TB + ro_own;
+                    int k = warp, u = 0;
+                    for (; k < nbb; k += NW, u ^= 1) acc[u] += __ldcg(pbk + (long long)k * TB);
+                }
+                red[(kind * NW + warp) * 32 + lane] = acc[0] + acc[1];
+            }
+            worker_bar();
+        }
+        if (tr && threadIdx.x == 0) tr[2] = gtime();
+        if (warp == 0) {
+            double v0 = 0.0;
+            if (kv0) {
+                for (int w = 0; w < NW; ++w) v0 += red[w * 32 + lane];
+                if (pad) v0 = 0.0;
+                if (rvalid) {
+                    a.Y1[(long long)(t - 1) * Np + r] = v0;
+                    a.xb[(long long)(1 * 2 + (t & 1)) * Np + r] = v0;
+                }
+            }
+            if (do_x0 && rvalid) {
+                double x;
+                if (t < S) {
+                    const double hist = (t >= 2 ? c_h : 0.0) + a.epad[1] * v0;  // v0 = y1_{t-1}
+                    x = (c_z - c_d1 * hist) * c_di;
+                } else {
+                    x = (c_z - v0) * c_di;  // f-level: z_f - y1_{S-1}
+                }
+                a.xb[(long long)(0 * 2 + (t & 1)) * Np + r] = pad ? 0.0 : x;
+            }
+        } else if (warp == 2) {
+            double v1 = 0.0, v2 = 0.0;
+            if (kv1) {
+                for (int w = 0; w < NW; ++w) v1 += red[(NW + w) * 32 + lane];
+                if (pad) v1 = 0.0;
+            }
+            if (kv2) {
+                for (int w = 0; w < NW; ++w) v2 += red[(2 * NW + w) * 32 + lane];
+                if (pad) v2 = 0.0;
+                if (rvalid) {
+                    const long long o = (long long)(t - 3) * Np + r;
+                    a.DL[o] = v2;
+                    a.y[o] = c_y + v2;
+                }
+            }
+            if (do_x2 && rvalid) {
+                const int l = t - 2;
+                double x;
+                if (l < S) {
+                    // r_l = z_l - (D1 o sum_{m<=l} e_{l-m} y1_m + cs D2 o B y1_l);  d_{l-1} = v2
+                    const double res = c_z - (c_d1 * c_hr + a.cs * c_d2 * v1);
+                    const double hist = (l >= 2 ? c_h : 0.0) + (l >= 1 ? a.epad[1] * v2 : 0.0);
+                    x = (res - c_d1 * hist) * c_di;
+                } else {
+                    // f-level: r_f = z_f - (y1_{S-1} + cr D2_{S-1} o B y1_S);  x2 = (r_f - d_{S-1}) / D2
+                    const double res = c_z - (c_d1 + a.cr * c_d2 * v1);
+                    x = (res - v2) * c_di;
+                }
+                a.xb[(long long)(2 * 2 + (t & 1)) * Np + r] = pad ? 0.0 : x;
+            }
+        }
+        if (t == nsteps) break;  // the last step only finishes d_{nlev-1} and y
+        // publish: warps 0 and 2 meet the spare warps (whose history sums read Y1 / DL rows just
+        // written) at a named barrier, then one release per owned row block
+        if (warp == 0 || warp == 2 || warp >= NST) {
+            asm volatile("bar.sync 3, %0;\n" ::"n"((2 + NB_W) * 32) : "memory");
+            if (threadIdx.x == 0)
+                for (int rb = rb0; rb <= rb1; ++rb) red_release(a.xready + rb * CSTR, 1u);
+        }
+        if (tr && threadIdx.x == 0) tr[3] = gtime();
+
+        // =============== spare warps, first: history sums the owner needs at step t+1 (they only
+        // read this CTA's own rows, so they fill the wait for the other CTAs' x blocks)
+        //   h1p = sum_{m<=t-1} e_{t+1-m} y1_m    (x1_{t+1}; + e1 y1_t at owner time)
+        //   hrp = sum_{m<=t-1} e_{t-1-m} y1_m    (residual of level t-1)
+        //   h2p = sum_{m<=t-3} e_{t-1-m} d_m     (x2_{t-1}; + e1 d_{t-2} at owner time)
+        // The loads are independent: 8 in flight per lane and array.
+        if (warp >= NST && t >= 1) {
+            const int hw = warp - NST;
+            const double* ep = a.epad;  // zero outside 0..S-1: no bounds tests
+            {
+                double p1[8], pr[8], p2[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) p1[u] = pr[u] = p2[u] = 0.0;
+                for (int m0 = hw; m0 <= t - 1; m0 += 8 * NB_W) {
+                    double yv[8], dv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int m = m0 + u * NB_W;
+                        yv[u] = m <= t - 1 ? __ldcg(a.Y1 + (long long)m * Np + rr) : 0.0;
+                        dv[u] = m <= t - 3 ? __ldcg(a.DL + (long long)m * Np + rr) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int m = m0 + u * NB_W;
+                        p1[u] += __ldg(ep + t + 1 - m) * yv[u];
+                        const double em = __ldg(ep + t - 1 - m);
+                        pr[u] += em * yv[u];
+                        p2[u] += em * dv[u];
+                    }
+                }
+                double* rd = hred + hw * 96;
+                rd[lane] = ((p1[0] + p1[1]) + (p1[2] + p1[3])) + ((p1[4] + p1[5]) + (p1[6] + p1[7]));
+                rd[32 + lane] = ((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
+                rd[64 + lane] = ((p2[0] + p2[1]) + (p2[2] + p2[3])) + ((p2[4] + p2[5]) + (p2[6] + p2[7]));
+                bwarp_bar();
+                if (hw == 0) {
+                    double s1 = 0.0, sr = 0.0, s2 = 0.0;
+                    for (int w = 0; w < NB_W; ++w) {
+                        s1 += hred[w * 96 + lane];
+                        sr += hred[w * 96 + 32 + lane];
+                        s2 += hred[w * 96 + 64 + lane];
+                    }
+                    h1p[lane] = s1;
+                    hrp[lane] = sr;
+                    h2p[lane] = s2;
+                }
+                bwarp_bar();
+            }
+        }
+        if (tr && threadIdx.x == NST * 32) tr[5] = gtime();
+
+        // =============== tiles of step t
+        const unsigned xtarget_step = (unsigned)(t + 1);
+        if (warp < NST) {
+            // ring items: FP64 tiles of level t, then FP32 tiles of level t-2.  Item -> warp item % NST
+            // (items k and k + NST share a ring slot, so one warp consumes them in order).
+            const long long base0 = it, base1 = it + (h64_valid(t) ? ntiles : 0);
+            const long long kk0 = ((long long)warp - base0 % NST + NST) % NST;
+            const long long kk1 = ((long long)warp - base1 % NST + NST) % NST;
+            const int n0 = h64_valid(t) && kk0 < ntiles ? (int)((ntiles - kk0 + NST - 1) / NST) : 0;
+            const int n1 = h32_valid(t) && kk1 < ntiles ? (int)((ntiles - kk1 + NST - 1) / NST) : 0;
+            const int nitems = n0 + n1;
+            auto item_of = [&](int c, int& kind, long long& kk) {
+                kind = c < n0 ? 0 : 1;
+                kk = c < n0 ? kk0 + (long long)c * NST : kk1 + (long long)(c - n0) * NST;
+            };
+            // one poll round for every x block this warp reads in this step (lane 2c: bi, 2c+1: bj)
+            for (int c0 = 0; c0 < nitems; c0 += 16) {
+                const int c = c0 + (lane >> 1);
+                const unsigned* ctr = nullptr;
+                unsigned tgt = 0;
+                if (c < nitems) {
+                    int kind, bi, bj;
+                    long long kk;
+                    item_of(c, kind, kk);
+                    tile_coords(t0 + kk, bi, bj);
+                    const int blk = (lane & 1) ? bj : bi;
+                    ctr = a.xready + blk * CSTR;
+                    tgt = (unsigned)owners_of_block(blk, R, G) * xtarget_step;
+                }
+                while (!__all_sync(0xffffffffu, ctr == nullptr || ld_acquire(ctr) >= tgt)) __nanosleep(64);
+            }
+            // x blocks of item c+1 are loaded while item c computes
+            double2 nxj = make_double2(0.0, 0.0), nxi = nxj;
+            auto load_x = [&](int c) {
+                int kind, bi, bj;
+                long long kk;
+                item_of(c, kind, kk);
+                tile_coords(t0 + kk, bi, bj);
+                const double* xb = a.xb + (long long)((kind == 0 ? 0 : 2) * 2 + (t & 1)) * Np;
+                nxj = __ldcg(reinterpret_cast<const double2*>(xb + (long long)bj * TB) + lane);
+                nxi = __ldcg(reinterpret_cast<const double2*>(xb + (long long)bi * TB) + lane);
+            };
+            if (nitems > 0) load_x(0);
+            double* xi = xis + warp * TB;
+            for (int c = 0; c < nitems; ++c) {
+                const double2 xj = nxj;
+                reinterpret_cast<double2*>(xi)[lane] = nxi;
+                if (c + 1 < nitems) load_x(c + 1);
+                __syncwarp();
+                int kind, bi, bj;
+                long long kk;
+                item_of(c, kind, kk);
+                tile_coords(t0 + kk, bi, bj);
+                const long long item = (kind == 0 ? base0 : base1) + kk;
+                double* pbk = a.pb + (long long)((kind == 0 ? 0 : 2) * 2 + (t & 1)) * kstride;
+                const int slot = (int)(item % NST);
+                mbar_wait(&full[slot], (unsigned)((item / NST) & 1));
+                double* prow = pbk + ((long long)bi * nbb + bj) * TB;
+                double* pcol = pbk + ((long long)bj * nbb + bi) * TB;
+                if (kind == 0) {
+                    const double* tile = ring + slot * SLOT;
+                    tile_product([&](int r) { return reinterpret_cast<const double2*>(tile + r * TB)[lane]; }, xj,
+                                 xi, prow, pcol, bi == bj, lane);
+                } else {
+                    const float* tile = reinterpret_cast<const float*>(ring + slot * SLOT);
+                    tile_product(
+                        [&](int r) {
+                            const float2 v = reinterpret_cast<const float2*>(tile + r * TB)[lane];
+                            return make_double2((double)v.x, (double)v.y);
+                        },
+                        xj, xi, prow, pcol, bi == bj, lane);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
+            }
+            it += (h64_valid(t) ? ntiles : 0) + (h32_valid(t) ? ntiles : 0);
+            if (tr && lane == 0) atomicMax(tr + 4, gtime());
+            // one release fence per warp and step, then bump the partial-product counters
+            __syncwarp();
+            if (lane == 0 && nitems > 0) {
+                asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+                for (int c = 0; c < nitems; ++c) {
+                    int kind, bi, bj;
+                    long long kk;
+                    item_of(c, kind, kk);
+                    tile_coords(t0 + kk, bi, bj);
+                    const int xk = kind == 0 ? 0 : 2;
+                    red_relaxed(a.pdone + (xk * nbb + bi) * CSTR, 1u);
+                    if (bi != bj) red_relaxed(a.pdone + (xk * nbb + bj) * CSTR, 1u);
+                }
+            }
+        } else if (t >= 1 && t - 1 < nlev) {
+            // generated B tiles of the residual of level t-1 (no HBM traffic): B(i, j) = a[m_i - m_j].
+            // A 64-row block lies inside one i1 row (ld2 % 64 == 0), so tile (bi, bj) needs the 127
+            // symbol entries seg[k] = a[i1 - j1][i2_0 - j2_0 + k - 63]: B(r, c) = seg[r - c + 63].
+            const int bw = warp - NST;
+            const double* xb = a.xb + (long long)(1 * 2 + (t & 1)) * Np;
+            double* pbk = a.pb + (long long)(1 * 2 + (t & 1)) * kstride;
+            double* seg = segs + bw * 128;
+            const int nitems = bw < ntiles ? (int)((ntiles - bw + NB_W - 1) / NB_W) : 0;
+            for (int c0 = 0; c0 < nitems; c0 += 16) {
+                const int c = c0 + (lane >> 1);
+                const unsigned* ctr = nullptr;
+                unsigned tgt = 0;
+                if (c < nitems) {
+                    int bi, bj;
+                    tile_coords(t0 + bw + (long long)c * NB_W, bi, bj);
+                    const int blk = (lane & 1) ? bj : bi;
+                    ctr = a.xready + blk * CSTR;
+                    tgt = (unsigned)owners_of_block(blk, R, G) * xtarget_step;
+                }
+                while (!__all_sync(0xffffffffu, ctr == nullptr || ld_acquire(ctr) >= tgt)) __nanosleep(64);
+            }
+            double2 nxj = make_double2(0.0, 0.0), nxi = nxj;
+            double ng[4];
+            auto load_b = [&](int c) {
+                int bi, bj;
+                tile_coords(t0 + bw + (long long)c * NB_W, bi, bj);
+                const long long i0 = (long long)bi * TB, j0 = (long long)bj * TB;
+                const int i1 = (int)(i0 / a.ld2), i2 = (int)(i0 % a.ld2);
+                const int j1 = (int)(j0 / a.ld2), j2 = (int)(j0 % a.ld2);
+                const double* g = a.gen + (long long)(i1 - j1 + a.n1 - 1) * a.gen_stride + a.ld2 + i2 - j2 - 63;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) ng[u] = (lane + 32 * u < 127) ? __ldg(g + lane + 32 * u) : 0.0;
+                nxj = __ldcg(reinterpret_cast<const double2*>(xb + j0) + lane);
+                nxi = __ldcg(reinterpret_cast<const double2*>(xb + i0) + lane);
+            };
+            if (nitems > 0) load_b(0);
+            double* xi = xis + warp * TB;
+            for (int c = 0; c < nitems; ++c) {
+                const double2 xj = nxj;
+                reinterpret_cast<double2*>(xi)[lane] = nxi;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) seg[lane + 32 * u] = ng[u];
+                if (c + 1 < nitems) load_b(c + 1);
+                __syncwarp();
+                int bi, bj;
+                tile_coords(t0 + bw + (long long)c * NB_W, bi, bj);
+                // pad columns meet zero entries of x; pad rows are zeroed by the owner
+                tile_product([&](int r) { return make_double2(seg[r - 2 * lane + 63], seg[r - 2 * lane + 62]); },
+                             xj, xi, pbk + ((long long)bi * nbb + bj) * TB, pbk + ((long long)bj * nbb + bi) * TB,
+                             bi == bj, lane);
+                __syncwarp();
+            }
+            if (lane == 0 && nitems > 0) {
+                asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+                for (int c = 0; c < nitems; ++c) {
+                    int bi, bj;
+                    tile_coords(t0 + bw + (long long)c * NB_W, bi, bj);
+                    red_relaxed(a.pdone + (1 * nbb + bi) * CSTR, 1u);
+                    if (bi != bj) red_relaxed(a.pdone + (1 * nbb + bj) * CSTR, 1u);
+                }
+            }
+            if (tr && lane == 0) atomicMax(tr + 6, gtime());
+        }
+    }
+}
+
+int sweep_ir_smem_bytes() {
+    return NST * SLOT * (int)sizeof(double) +
+           (3 * NW * 32 + 4 * RCAP + NW * TB + NB_W * 96 + NB_W * 128) * (int)sizeof(double) +
+           2 * NST * (int)sizeof(uint64_t);
+}
+
+}  // namespace
+
+bool sweep_ir_available(const fi_precond* P) {
+    static const int env = [] {
+        const char* v = getenv("FI_SWEEP_IR");
+        return v ? atoi(v) : 1;
+    }();
+    return env != 0 && P->mode == 0 && P->Hf.p != nullptr && (P->sys->L.Np + P->G - 1) / P->G <= RCAP;
+}
+
+void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip) {
+    static bool configured = false;
+    const int smem = sweep_ir_smem_bytes();
+    if (!configured) {
+        FI_CUDA(cudaFuncSetAttribute(sweep_ir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0;
+        FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_ir_kernel, THREADS, smem));
+        if (per_sm < 1) throw Error(FI_E_CUDA, "sweep_ir_kernel cannot be resident");
+        configured = true;
+    }
+    const fi_system* sys = P->sys;
+    const Layout& L = sys->L;
+    if ((L.Np + P->G - 1) / P->G > RCAP) throw Error(FI_E_RESOURCE, "sweep_ir: too many rows per CTA");
+    if (!P->ir_xb.p) {
+        P->ir_xb.alloc((size_t)6 * L.Np);
+        P->ir_pb.alloc((size_t)6 * P->nb * P->nb * TB);
+        P->ir_counters.alloc((size_t)4 * P->nb * CSTR);
+    }
+    IrArgs a;
+    a.H64 = P->H.p;
+    a.H32 = P->Hf.p;
+    a.T = P->T;
+    a.nb = P->nb;
+    a.nlev = levels;
+    a.S = L.S;
+    a.n1 = L.n1;
+    a.n2 = L.n2;
+    a.ld2 = L.ld2;
+    a.gen_stride = 2 * L.ld2 + 8;
+    a.Np = L.Np;
+    a.z = z;
+    a.y = y;
+    a.Y1 = P->rbuf.p;
+    a.DL = P->dbuf.p;
+    a.D1 = sys->D1.p;
+    a.D2 = sys->D2.p;
+    a.d2inv = P->d2inv.p;
+    a.e = sys->e.p;
+    a.epad = sys->epad.p + kEOFF;
+    a.gen = sys->gen.p;
+    a.cs = sys->cs;
+    a.cr = sys->cr;
+    a.xb = P->ir_xb.p;
+    a.pb = P->ir_pb.p;
+    a.xready = P->ir_counters.p;
+    a.pdone = P->ir_counters.p + (size_t)P->nb * CSTR;
+    a.skip = skip;
+    static const int evict = [] {
+        const char* v = std::getenv("FI_IR_EVICT");
+        return v ? std::atoi(v) : 1;
+    }();
+    a.evict_first = evict;
+    a.trace = nullptr;
+    static const bool tracing = std::getenv("FI_SWEEP_TRACE") != nullptr;
+    const int nst1 = levels + 3;
+    DevBuf<unsigned long long> trace;
+    if (tracing) {
+        trace.alloc((size_t)P->G * nst1 * 8);
+        FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
+        a.trace = trace.p;
+    }
+    FI_CUDA(cudaMemsetAsync(P->ir_counters.p, 0, P->ir_counters.bytes(), ctx->stream));
+    void* args[] = {&a};
+    FI_CUDA(cudaLaunchCooperativeKernel((const void*)sweep_ir_kernel, dim3(P->G), dim3(THREADS), args, (size_t)smem,
+                                        ctx->stream));
+    FI_LAUNCHED(ctx);
+    if (tracing) {
+        // per step (averaged over CTAs and steps): pdone wait, reduce, x, ring tiles, history, B tiles
+        std::vector<unsigned long long> h(trace.n);
+        FI_CUDA(cudaMemcpyAsync(h.data(), trace.p, trace.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+        FI_CUDA(cudaStreamSynchronize(ctx->stream));
+        auto ph = [&](int c, int t, int i) { return (double)h[((size_t)c * nst1 + t) * 8 + i]; };
+        for (int lo : {1, nst1 / 2, nst1 - 40}) {
+            double acc[6] = {0, 0, 0, 0, 0, 0};
+            int cnt = 0;
+            for (int c = 0; c < P->G; ++c)
+                for (int t = lo; t < lo + 32 && t < nst1 - 3; ++t) {
+                    acc[0] += ph(c, t, 1) - ph(c, t, 0);
+                    acc[1] += ph(c, t, 2) - ph(c, t, 1);
+                    acc[2] += ph(c, t, 3) - ph(c, t, 2);
+                    acc[3] += ph(c, t, 4) - ph(c, t, 3);
+                    acc[4] += ph(c, t, 5) - ph(c, t, 3);
+                    acc[5] += ph(c, t, 6) - ph(c, t, 3);
+                    ++cnt;
+                }
+            const double step = (ph(0, std::min(lo + 32, nst1 - 3), 0) - ph(0, lo, 0)) / 32;
+            std::fprintf(stderr,
+                         "[sweep_ir] steps %3d+: step %6.2f us | wait %6.2f | reduce %6.2f | x %6.2f | ring %6.2f | "
+                         "hist %6.2f | btiles %6.2f\n",
+                         lo, step * 1e-3, acc[0] / cnt * 1e-3, acc[1] / cnt * 1e-3, acc[2] / cnt * 1e-3,
+                         acc[3] / cnt * 1e-3, acc[4] / cnt * 1e-3, acc[5] / cnt * 1e-3);
+        }
+    }
+}
+
+}  // namespace fib

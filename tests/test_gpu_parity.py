@@ -154,7 +154,7 @@ def test_precond_config1_backward_error_and_levels():
     A, Ao = F.SystemOperator(config_problem(F, 1)), O.SystemOperator(config_problem(O, 1))
     P = F.BlockTriangularPreconditioner(A)
     Po = O.BlockTriangularPreconditioner.__new__(O.BlockTriangularPreconditioner)
-    Po.A, Po.N, Po.S, Po.cache = Ao, Ao.N, Ao.steps, False
+    Po.A, Po.N, Po.S, Po.cache, Po.inner = Ao, Ao.N, Ao.steps, False, "lu"
     Po.Bd = Ao.laplacian.dense(Ao.N)
     z = RandomVectors(11).vector(A.dim())
     y = P.apply(z)

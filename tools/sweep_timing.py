@@ -26,8 +26,23 @@ P.set_refine(False)
 assert lib.fi_precond_apply_timed(P.handle, y.data_ptr(), out.data_ptr(), 5, ctypes.byref(ms)) == 0
 res["sweep_ms"] = ms.value
 P.set_refine(True)
-assert lib.fi_precond_apply_timed(P.handle, y.data_ptr(), out.data_ptr(), 5, ctypes.byref(ms)) == 0
+rc = lib.fi_precond_apply_timed(P.handle, y.data_ptr(), out.data_ptr(), 5, ctypes.byref(ms))
+assert rc == 0, lib.fi_last_error()
 res["papply_ms"] = ms.value
 assert lib.fi_system_apply_timed(A.handle, y.data_ptr(), out.data_ptr(), 5, ctypes.byref(ms)) == 0
 res["op_ms"] = ms.value
 print(json.dumps(res), flush=True)
+if os.environ.get("BWD"):
+    # backward error of P^{-1} y against the oracle's P (and a dump for cross-setting comparisons)
+    from oracle import fracinv_oracle as O  # noqa: E402
+    Ao = O.SystemOperator(baseline_problem(O, cfg))
+    yh = y.cpu().numpy()
+    x = P.apply(yh)
+    r = Ao.apply_precond_matrix(x) - yh
+    N = A.N
+    res2 = {"cfg": cfg, "ir": os.environ.get("FI_SWEEP_IR", "1"),
+            "bwd": float(np.linalg.norm(r) / np.linalg.norm(yh)),
+            "bwd_f": float(np.linalg.norm(r[-N:]) / np.linalg.norm(yh[-N:]))}
+    os.makedirs("gpurun_out", exist_ok=True)
+    np.save(f"gpurun_out/papply_cfg{cfg}_ir{res2['ir']}.npy", x)
+    print(json.dumps(res2), flush=True)
