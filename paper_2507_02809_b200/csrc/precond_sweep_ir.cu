@@ -35,6 +35,8 @@ constexpr int SLOT = TILE;              // doubles per slot
 constexpr int NB_W = NW - NST;          // warps for the generated B tiles and the history sums
 constexpr int RCAP = 32;   // owned rows per CTA: one per lane
 constexpr int CSTR = kCounterStride;
+constexpr int TCAP = 64;   // tiles per CTA and level (coordinate table)
+constexpr int KPW = 7;     // partials per warp and kind in the owner reduction: nb <= KPW * NW
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -88,8 +90,16 @@ __device__ __forceinline__ void red_release(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 // warp-uniform poll (all 32 lanes): the warp never diverges, so later shfl.sync stay cheap
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// Poll relaxed (an acquire load invalidates the SM's L1 on every iteration, evicting the symbol and
+// weight lines other warps read through L1), then one acquire load once the counter has moved.
 __device__ __forceinline__ void warp_spin_until(const unsigned* p, unsigned target) {
-    while (!__all_sync(0xffffffffu, ld_acquire(p) >= target)) __nanosleep(64);
+    while (!__all_sync(0xffffffffu, ld_relaxed(p) >= target)) __nanosleep(64);
+    (void)ld_acquire(p);
 }
 __device__ __forceinline__ void tile_coords(long long t, int& bi, int& bj) {
     int r = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
@@ -142,8 +152,8 @@ template <class RowFn>
 __device__ __forceinline__ void tile_product(RowFn hrow, double2 xj, const double* xi, double* prow, double* pcol,
                                              bool diag, int lane) {
     double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {  // not unrolled: keeps the kernel inside the instruction cache
         double pr[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
@@ -181,7 +191,8 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
     double* xis = bq + RCAP;                                        // NW x TB staging of x_i
     double* hred = xis + NW * TB;                                   // NB_W x 96 history partials
     double* segs = hred + NB_W * 96;                                // NB_W x 128 symbol segments
-    uint64_t* full = reinterpret_cast<uint64_t*>(segs + NB_W * 128);
+    int* tcs = reinterpret_cast<int*>(segs + NB_W * 128);            // TCAP packed (bi << 16 | bj)
+    uint64_t* full = reinterpret_cast<uint64_t*>(tcs + TCAP);
     uint64_t* empty = full + NST;
 
     const unsigned G = gridDim.x;
@@ -194,6 +205,11 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
     const int nsteps = nlev + 2;  // tile steps 0..nlev+1; owner steps 1..nlev+2
     const long long kstride = (long long)nbb * nbb * TB;
 
+    for (long long k = threadIdx.x; k < ntiles; k += blockDim.x) {
+        int bi, bj;
+        tile_coords(t0 + k, bi, bj);
+        tcs[k] = (bi << 16) | bj;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
@@ -250,7 +266,7 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
     const long long rb_own = rr / TB, ro_own = rr % TB;
 
     for (int t = 0; t <= nsteps; ++t) {
-        unsigned long long* tr = a.trace ? a.trace + ((long long)blockIdx.x * (nsteps + 1) + t) * 8 : nullptr;
+        unsigned long long* tr = a.trace ? a.trace + ((long long)blockIdx.x * (nsteps + 1) + t) * 12 : nullptr;
         if (tr && threadIdx.x == 0) tr[0] = gtime();
         // =============== owner step t: reduce the partials of step t-1 and publish
         //   warp 0: y1_{t-1} -> Y1, x1_t and the B-tile input y1_{t-1}
@@ -308,15 +324,22 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
             }
             // every warp loads its ~nb / NW partials of all three kinds at once (fixed order)
             const int par = (t - 1) & 1;
+            double pv[3][KPW];
 #pragma unroll
             for (int kind = 0; kind < 3; ++kind) {
-                double acc[2] = {0.0, 0.0};
-                if (kv[kind]) {
-                    const double* pbk = a.pb + (long long)(kind * 2 + par) * kstride + rb_own * nbb * TB + ro_own;
-                    int k = warp, u = 0;
-                    for (; k < nbb; k += NW, u ^= 1) acc[u] += __ldcg(pbk + (long long)k * TB);
+                const double* pbk = a.pb + (long long)(kind * 2 + par) * kstride + rb_own * nbb * TB + ro_own;
+#pragma unroll
+                for (int u = 0; u < KPW; ++u) {
+                    const int k = warp + u * NW;
+                    pv[kind][u] = kv[kind] && k < nbb ? __ldcg(pbk + (long long)k * TB) : 0.0;
                 }
-                red[(kind * NW + warp) * 32 + lane] = acc[0] + acc[1];
+            }
+#pragma unroll
+            for (int kind = 0; kind < 3; ++kind) {
+                double s0 = 0.0;
+#pragma unroll
+                for (int u = 0; u < KPW; ++u) s0 += pv[kind][u];
+                red[(kind * NW + warp) * 32 + lane] = s0;
             }
             worker_bar();
         }
@@ -457,26 +480,31 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                     int kind, bi, bj;
                     long long kk;
                     item_of(c, kind, kk);
-                    tile_coords(t0 + kk, bi, bj);
+                    bi = tcs[kk] >> 16;
+                    bj = tcs[kk] & 0xffff;
                     const int blk = (lane & 1) ? bj : bi;
                     ctr = a.xready + blk * CSTR;
                     tgt = (unsigned)owners_of_block(blk, R, G) * xtarget_step;
                 }
-                while (!__all_sync(0xffffffffu, ctr == nullptr || ld_acquire(ctr) >= tgt)) __nanosleep(64);
+                while (!__all_sync(0xffffffffu, ctr == nullptr || ld_relaxed(ctr) >= tgt)) __nanosleep(64);
+                if (ctr) (void)ld_acquire(ctr);
             }
+            if (tr && lane == 0) atomicMax(tr + 8, gtime());
             // x blocks of item c+1 are loaded while item c computes
             double2 nxj = make_double2(0.0, 0.0), nxi = nxj;
             auto load_x = [&](int c) {
                 int kind, bi, bj;
                 long long kk;
                 item_of(c, kind, kk);
-                tile_coords(t0 + kk, bi, bj);
+                bi = tcs[kk] >> 16;
+                bj = tcs[kk] & 0xffff;
                 const double* xb = a.xb + (long long)((kind == 0 ? 0 : 2) * 2 + (t & 1)) * Np;
                 nxj = __ldcg(reinterpret_cast<const double2*>(xb + (long long)bj * TB) + lane);
                 nxi = __ldcg(reinterpret_cast<const double2*>(xb + (long long)bi * TB) + lane);
             };
             if (nitems > 0) load_x(0);
             double* xi = xis + warp * TB;
+            unsigned long long wsum = 0;
             for (int c = 0; c < nitems; ++c) {
                 const double2 xj = nxj;
                 reinterpret_cast<double2*>(xi)[lane] = nxi;
@@ -485,11 +513,14 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                 int kind, bi, bj;
                 long long kk;
                 item_of(c, kind, kk);
-                tile_coords(t0 + kk, bi, bj);
+                bi = tcs[kk] >> 16;
+                bj = tcs[kk] & 0xffff;
                 const long long item = (kind == 0 ? base0 : base1) + kk;
                 double* pbk = a.pb + (long long)((kind == 0 ? 0 : 2) * 2 + (t & 1)) * kstride;
                 const int slot = (int)(item % NST);
+                const unsigned long long tw0 = tr ? gtime() : 0;
                 mbar_wait(&full[slot], (unsigned)((item / NST) & 1));
+                if (tr) wsum += gtime() - tw0;
                 double* prow = pbk + ((long long)bi * nbb + bj) * TB;
                 double* pcol = pbk + ((long long)bj * nbb + bi) * TB;
                 if (kind == 0) {
@@ -509,7 +540,10 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                 if (lane == 0) mbar_arrive(&empty[slot]);
             }
             it += (h64_valid(t) ? ntiles : 0) + (h32_valid(t) ? ntiles : 0);
-            if (tr && lane == 0) atomicMax(tr + 4, gtime());
+            if (tr && lane == 0) {
+                atomicMax(tr + 4, gtime());
+                atomicAdd(tr + 7, wsum);
+            }
             // one release fence per warp and step, then bump the partial-product counters
             __syncwarp();
             if (lane == 0 && nitems > 0) {
@@ -518,7 +552,8 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                     int kind, bi, bj;
                     long long kk;
                     item_of(c, kind, kk);
-                    tile_coords(t0 + kk, bi, bj);
+                    bi = tcs[kk] >> 16;
+                    bj = tcs[kk] & 0xffff;
                     const int xk = kind == 0 ? 0 : 2;
                     red_relaxed(a.pdone + (xk * nbb + bi) * CSTR, 1u);
                     if (bi != bj) red_relaxed(a.pdone + (xk * nbb + bj) * CSTR, 1u);
@@ -539,18 +574,22 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                 unsigned tgt = 0;
                 if (c < nitems) {
                     int bi, bj;
-                    tile_coords(t0 + bw + (long long)c * NB_W, bi, bj);
+                    bi = tcs[bw + (long long)c * NB_W] >> 16;
+                    bj = tcs[bw + (long long)c * NB_W] & 0xffff;
                     const int blk = (lane & 1) ? bj : bi;
                     ctr = a.xready + blk * CSTR;
                     tgt = (unsigned)owners_of_block(blk, R, G) * xtarget_step;
                 }
-                while (!__all_sync(0xffffffffu, ctr == nullptr || ld_acquire(ctr) >= tgt)) __nanosleep(64);
+                while (!__all_sync(0xffffffffu, ctr == nullptr || ld_relaxed(ctr) >= tgt)) __nanosleep(64);
+                if (ctr) (void)ld_acquire(ctr);
             }
+            if (tr && lane == 0) atomicMax(tr + 9, gtime());
             double2 nxj = make_double2(0.0, 0.0), nxi = nxj;
             double ng[4];
             auto load_b = [&](int c) {
                 int bi, bj;
-                tile_coords(t0 + bw + (long long)c * NB_W, bi, bj);
+                bi = tcs[bw + (long long)c * NB_W] >> 16;
+                bj = tcs[bw + (long long)c * NB_W] & 0xffff;
                 const long long i0 = (long long)bi * TB, j0 = (long long)bj * TB;
                 const int i1 = (int)(i0 / a.ld2), i2 = (int)(i0 % a.ld2);
                 const int j1 = (int)(j0 / a.ld2), j2 = (int)(j0 % a.ld2);
@@ -570,7 +609,8 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                 if (c + 1 < nitems) load_b(c + 1);
                 __syncwarp();
                 int bi, bj;
-                tile_coords(t0 + bw + (long long)c * NB_W, bi, bj);
+                bi = tcs[bw + (long long)c * NB_W] >> 16;
+                bj = tcs[bw + (long long)c * NB_W] & 0xffff;
                 // pad columns meet zero entries of x; pad rows are zeroed by the owner
                 tile_product([&](int r) { return make_double2(seg[r - 2 * lane + 63], seg[r - 2 * lane + 62]); },
                              xj, xi, pbk + ((long long)bi * nbb + bj) * TB, pbk + ((long long)bj * nbb + bi) * TB,
@@ -581,7 +621,8 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                 asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
                 for (int c = 0; c < nitems; ++c) {
                     int bi, bj;
-                    tile_coords(t0 + bw + (long long)c * NB_W, bi, bj);
+                    bi = tcs[bw + (long long)c * NB_W] >> 16;
+                    bj = tcs[bw + (long long)c * NB_W] & 0xffff;
                     red_relaxed(a.pdone + (1 * nbb + bi) * CSTR, 1u);
                     if (bi != bj) red_relaxed(a.pdone + (1 * nbb + bj) * CSTR, 1u);
                 }
@@ -593,7 +634,7 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
 
 int sweep_ir_smem_bytes() {
     return NST * SLOT * (int)sizeof(double) +
-           (3 * NW * 32 + 4 * RCAP + NW * TB + NB_W * 96 + NB_W * 128) * (int)sizeof(double) +
+           (3 * NW * 32 + 4 * RCAP + NW * TB + NB_W * 96 + NB_W * 128) * (int)sizeof(double) + TCAP * (int)sizeof(int) +
            2 * NST * (int)sizeof(uint64_t);
 }
 
@@ -604,7 +645,8 @@ bool sweep_ir_available(const fi_precond* P) {
         const char* v = getenv("FI_SWEEP_IR");
         return v ? atoi(v) : 1;
     }();
-    return env != 0 && P->mode == 0 && P->Hf.p != nullptr && (P->sys->L.Np + P->G - 1) / P->G <= RCAP;
+    return env != 0 && P->mode == 0 && P->Hf.p != nullptr && (P->sys->L.Np + P->G - 1) / P->G <= RCAP &&
+           P->nb <= KPW * NW && (P->T + P->G - 1) / P->G <= TCAP;
 }
 
 void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip) {
@@ -664,7 +706,7 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
     const int nst1 = levels + 3;
     DevBuf<unsigned long long> trace;
     if (tracing) {
-        trace.alloc((size_t)P->G * nst1 * 8);
+        trace.alloc((size_t)P->G * nst1 * 12);
         FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
         a.trace = trace.p;
     }
@@ -678,9 +720,9 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
         std::vector<unsigned long long> h(trace.n);
         FI_CUDA(cudaMemcpyAsync(h.data(), trace.p, trace.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
-        auto ph = [&](int c, int t, int i) { return (double)h[((size_t)c * nst1 + t) * 8 + i]; };
+        auto ph = [&](int c, int t, int i) { return (double)h[((size_t)c * nst1 + t) * 12 + i]; };
         for (int lo : {1, nst1 / 2, nst1 - 40}) {
-            double acc[6] = {0, 0, 0, 0, 0, 0};
+            double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
             int cnt = 0;
             for (int c = 0; c < P->G; ++c)
                 for (int t = lo; t < lo + 32 && t < nst1 - 3; ++t) {
@@ -690,14 +732,17 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
                     acc[3] += ph(c, t, 4) - ph(c, t, 3);
                     acc[4] += ph(c, t, 5) - ph(c, t, 3);
                     acc[5] += ph(c, t, 6) - ph(c, t, 3);
+                    acc[6] += ph(c, t, 7) / NST;
+                    acc[7] += ph(c, t, 8) - ph(c, t, 3);
+                    acc[8] += ph(c, t, 9) - ph(c, t, 3);
                     ++cnt;
                 }
             const double step = (ph(0, std::min(lo + 32, nst1 - 3), 0) - ph(0, lo, 0)) / 32;
             std::fprintf(stderr,
                          "[sweep_ir] steps %3d+: step %6.2f us | wait %6.2f | reduce %6.2f | x %6.2f | ring %6.2f | "
-                         "hist %6.2f | btiles %6.2f\n",
+                         "hist %6.2f | btiles %6.2f | ring data wait/warp %6.2f | ring x-poll %6.2f | b x-poll %6.2f\n",
                          lo, step * 1e-3, acc[0] / cnt * 1e-3, acc[1] / cnt * 1e-3, acc[2] / cnt * 1e-3,
-                         acc[3] / cnt * 1e-3, acc[4] / cnt * 1e-3, acc[5] / cnt * 1e-3);
+                         acc[3] / cnt * 1e-3, acc[4] / cnt * 1e-3, acc[5] / cnt * 1e-3, acc[6] / cnt * 1e-3, acc[7] / cnt * 1e-3, acc[8] / cnt * 1e-3);
         }
     }
 }
