@@ -30,8 +30,9 @@ constexpr int TILE = TB * TB;
 constexpr int NW = 11;                  // worker warps; + 1 producer = 12 warps (3 per SMSP)
 constexpr int NWT = NW * 32;
 constexpr int THREADS = NWT + 32;
-constexpr int NST = 6;                  // ring slots of 32 KiB (an FP32 tile uses half a slot)
-constexpr int SLOT = TILE;              // doubles per slot
+constexpr int NST = 6;                  // ring warps (tile item k -> warp k % NST)
+constexpr int NHS = 2 * NST;            // ring half-slots of 16 KiB: a tile streams as two row halves
+constexpr int HSLOT = TILE / 2;         // doubles per half-slot
 constexpr int NB_W = NW - NST;          // warps for the generated B tiles and the history sums
 constexpr int RCAP = 32;   // owned rows per CTA: one per lane
 constexpr int CSTR = kCounterStride;
@@ -75,6 +76,9 @@ __device__ __forceinline__ void tma_bulk_g2s_stream(void* dst, const void* src, 
             "r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void worker_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NWT) : "memory"); }
 __device__ __forceinline__ void bwarp_bar() { asm volatile("bar.sync 2, %0;\n" ::"n"(NB_W * 32) : "memory"); }
@@ -137,6 +141,7 @@ struct IrArgs {
     unsigned* pdone;   // [3][nb] (stride CSTR)
     const int* skip;
     int evict_first;
+    int pf_items;  // L2 prefetch distance in ring items (0 = off)
     unsigned long long* trace;  // optional [G][nsteps+1][8] phase timestamps (FI_SWEEP_TRACE=1)
 };
 
@@ -147,23 +152,26 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 
 // Symmetric tile product for one warp: rowsums (H x_j) -> prow[0..63], colsums (H^T x_i) -> pcol.
-// Row r of the tile is fetched by hrow(r) as the lane's two columns (2 lane, 2 lane + 1).
-template <class RowFn>
-__device__ __forceinline__ void tile_product(RowFn hrow, double2 xj, const double* xi, double* prow, double* pcol,
-                                             bool diag, int lane) {
+// hrow(half, q) fetches row 32 half + q as the lane's two columns (2 lane, 2 lane + 1); begin(half) /
+// end(half) bracket the rows of a half (ring-slot wait / release: a half-slot is freed as soon as its
+// rows are read, before the reduction).
+template <class Begin, class RowFn, class End>
+__device__ __forceinline__ void tile_product(Begin begin, RowFn hrow, End end, double2 xj, const double* xi,
+                                             double* prow, double* pcol, bool diag, int lane) {
     double c0 = 0.0, c1 = 0.0;
 #pragma unroll 1
     for (int half = 0; half < 2; ++half) {  // not unrolled: keeps the kernel inside the instruction cache
         double pr[32];
+        begin(half);
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
-            const int r = half * 32 + q;
-            const double2 hv = hrow(r);
+            const double2 hv = hrow(half, q);
             pr[q] = hv.x * xj.x + hv.y * xj.y;
-            const double xr = xi[r];
+            const double xr = xi[half * 32 + q];
             c0 += hv.x * xr;
             c1 += hv.y * xr;
         }
+        end(half);
 #pragma unroll
         for (int w = 16; w >= 1; w >>= 1) {
             const bool upper = (lane & w) != 0;
@@ -179,11 +187,46 @@ __device__ __forceinline__ void tile_product(RowFn hrow, double2 xj, const doubl
     if (!diag) reinterpret_cast<double2*>(pcol)[lane] = make_double2(c0, c1);
 }
 
+// FP32 variant for the refinement sweep (H32 tiles): the correction d ~ 1e-12 |y| needs only a few
+// significant digits, so the products and sums run in FP32 (no F64<->F32 conversions per element,
+// 32-bit shuffles); the partial products are stored in FP64 for the owner's reduction.
+template <class Begin, class RowFn, class End>
+__device__ __forceinline__ void tile_product_f32(Begin begin, RowFn hrow, End end, float2 xj, const float* xi,
+                                                 double* prow, double* pcol, bool diag, int lane) {
+    float c0 = 0.f, c1 = 0.f;
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+        float pr[32];
+        begin(half);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            const float2 hv = hrow(half, q);
+            pr[q] = fmaf(hv.x, xj.x, hv.y * xj.y);
+            const float xr = xi[half * 32 + q];
+            c0 = fmaf(hv.x, xr, c0);
+            c1 = fmaf(hv.y, xr, c1);
+        }
+        end(half);
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1) {
+            const bool upper = (lane & w) != 0;
+#pragma unroll
+            for (int i = 0; i < w; ++i) {
+                const float send = upper ? pr[i] : pr[i + w];
+                const float keep = upper ? pr[i + w] : pr[i];
+                pr[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+            }
+        }
+        prow[half * 32 + lane] = (double)pr[0];
+    }
+    if (!diag) reinterpret_cast<double2*>(pcol)[lane] = make_double2((double)c0, (double)c1);
+}
+
 __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
     if (a.skip && *a.skip) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* ring = reinterpret_cast<double*>(smem_raw);            // NST x SLOT
-    double* red = ring + NST * SLOT;                                // 3 x NW x 32
+    double* ring = reinterpret_cast<double*>(smem_raw);            // NHS x HSLOT
+    double* red = ring + NHS * HSLOT;                               // 3 x NW x 32
     double* h1p = red + 3 * NW * 32;                                   // RCAP
     double* hrp = h1p + RCAP;                                       // RCAP
     double* h2p = hrp + RCAP;                                       // RCAP
@@ -193,7 +236,7 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
     double* segs = hred + NB_W * 96;                                // NB_W x 128 symbol segments
     int* tcs = reinterpret_cast<int*>(segs + NB_W * 128);            // TCAP packed (bi << 16 | bj)
     uint64_t* full = reinterpret_cast<uint64_t*>(tcs + TCAP);
-    uint64_t* empty = full + NST;
+    uint64_t* empty = full + NHS;
 
     const unsigned G = gridDim.x;
     const long long t0 = (long long)blockIdx.x * a.T / G;
@@ -211,7 +254,7 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
         tcs[k] = (bi << 16) | bj;
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NST; ++s) {
+        for (int s = 0; s < NHS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -227,25 +270,60 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
         if (lane == 0) {
             uint64_t policy;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(policy));
-            long long it = 0;
-            for (int t = 0; t < nsteps; ++t) {
-                for (int kind = 0; kind < 2; ++kind) {
-                    const bool ok = kind == 0 ? h64_valid(t) : h32_valid(t);
-                    if (!ok) continue;
-                    const int lv = kind == 0 ? t : t - 2;
-                    for (long long k = 0; k < ntiles; ++k, ++it) {
-                        const int slot = (int)(it % NST);
-                        if (it >= NST) mbar_wait(&empty[slot], (unsigned)((it / NST - 1) & 1));
-                        const long long tix = (long long)lv * a.T + t0 + k;
-                        const void* src = kind == 0 ? (const void*)(a.H64 + tix * TILE) : (const void*)(a.H32 + tix * TILE);
-                        const unsigned bytes = kind == 0 ? TILE * sizeof(double) : TILE * sizeof(float);
-                        mbar_expect_tx(&full[slot], bytes);
-                        if (a.evict_first)
-                            tma_bulk_g2s_stream(ring + slot * SLOT, src, bytes, &full[slot], policy);
-                        else
-                            tma_bulk_g2s(ring + slot * SLOT, src, bytes, &full[slot]);
+            // item cursor: (step, kind, tile); a second cursor pf items ahead feeds L2 prefetches
+            struct Cur {
+                int t, kind;
+                long long k;
+            };
+            auto valid = [&](const Cur& c) { return c.kind == 0 ? h64_valid(c.t) : h32_valid(c.t); };
+            auto settle = [&](Cur& c) {
+                while (c.t < nsteps && (ntiles == 0 || !valid(c))) {
+                    if (c.kind == 0) {
+                        c.kind = 1;
+                    } else {
+                        c.kind = 0;
+                        ++c.t;
                     }
                 }
+            };
+            auto advance = [&](Cur& c) {
+                if (++c.k == ntiles) {
+                    c.k = 0;
+                    if (c.kind == 0) {
+                        c.kind = 1;
+                    } else {
+                        c.kind = 0;
+                        ++c.t;
+                    }
+                    settle(c);
+                }
+            };
+            auto src_of = [&](const Cur& c) -> const void* {
+                const long long tix = (long long)(c.kind == 0 ? c.t : c.t - 2) * a.T + t0 + c.k;
+                return c.kind == 0 ? (const void*)(a.H64 + tix * TILE) : (const void*)(a.H32 + tix * TILE);
+            };
+            Cur c{0, 0, 0};
+            settle(c);
+            Cur pc = c;
+            for (int i = 0; i < a.pf_items && pc.t < nsteps; ++i) advance(pc);
+            for (long long it = 0; c.t < nsteps; ++it) {
+                const unsigned hbytes = c.kind == 0 ? TILE / 2 * sizeof(double) : TILE / 2 * sizeof(float);
+                for (int h = 0; h < 2; ++h) {
+                    const long long j = 2 * it + h;
+                    const int slot = (int)(j % NHS);
+                    if (j >= NHS) mbar_wait(&empty[slot], (unsigned)((j / NHS - 1) & 1));
+                    const char* src = (const char*)src_of(c) + h * hbytes;
+                    mbar_expect_tx(&full[slot], hbytes);
+                    if (a.evict_first)
+                        tma_bulk_g2s_stream(ring + slot * HSLOT, src, hbytes, &full[slot], policy);
+                    else
+                        tma_bulk_g2s(ring + slot * HSLOT, src, hbytes, &full[slot]);
+                }
+                if (a.pf_items > 0 && pc.t < nsteps) {
+                    prefetch_l2(src_of(pc), pc.kind == 0 ? TILE * sizeof(double) : TILE * sizeof(float));
+                    advance(pc);
+                }
+                advance(c);
             }
         }
         return;
@@ -504,45 +582,61 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
             };
             if (nitems > 0) load_x(0);
             double* xi = xis + warp * TB;
-            unsigned long long wsum = 0;
+            float* xif = reinterpret_cast<float*>(xi);
+            unsigned long long wsum = 0, csum = 0;
             for (int c = 0; c < nitems; ++c) {
-                const double2 xj = nxj;
-                reinterpret_cast<double2*>(xi)[lane] = nxi;
-                if (c + 1 < nitems) load_x(c + 1);
-                __syncwarp();
+                const unsigned long long tc0 = tr ? gtime() : 0;
                 int kind, bi, bj;
                 long long kk;
                 item_of(c, kind, kk);
+                const double2 xj = nxj;
+                if (kind == 0)
+                    reinterpret_cast<double2*>(xi)[lane] = nxi;
+                else
+                    reinterpret_cast<float2*>(xif)[lane] = make_float2((float)nxi.x, (float)nxi.y);
+                if (c + 1 < nitems) load_x(c + 1);
+                __syncwarp();
                 bi = tcs[kk] >> 16;
                 bj = tcs[kk] & 0xffff;
                 const long long item = (kind == 0 ? base0 : base1) + kk;
                 double* pbk = a.pb + (long long)((kind == 0 ? 0 : 2) * 2 + (t & 1)) * kstride;
-                const int slot = (int)(item % NST);
-                const unsigned long long tw0 = tr ? gtime() : 0;
-                mbar_wait(&full[slot], (unsigned)((item / NST) & 1));
-                if (tr) wsum += gtime() - tw0;
                 double* prow = pbk + ((long long)bi * nbb + bj) * TB;
                 double* pcol = pbk + ((long long)bj * nbb + bi) * TB;
+                const int hs0 = (int)((2 * item) % NHS);  // half-slots 2 item, 2 item + 1 (mod NHS)
+                auto begin = [&](int h) {
+                    const long long j = 2 * item + h;
+                    const unsigned long long tw0 = tr ? gtime() : 0;
+                    mbar_wait(&full[j % NHS], (unsigned)((j / NHS) & 1));
+                    if (tr) wsum += gtime() - tw0;
+                };
+                auto end = [&](int h) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[(2 * item + h) % NHS]);
+                };
                 if (kind == 0) {
-                    const double* tile = ring + slot * SLOT;
-                    tile_product([&](int r) { return reinterpret_cast<const double2*>(tile + r * TB)[lane]; }, xj,
-                                 xi, prow, pcol, bi == bj, lane);
-                } else {
-                    const float* tile = reinterpret_cast<const float*>(ring + slot * SLOT);
                     tile_product(
-                        [&](int r) {
-                            const float2 v = reinterpret_cast<const float2*>(tile + r * TB)[lane];
-                            return make_double2((double)v.x, (double)v.y);
+                        begin,
+                        [&](int h, int q) {
+                            return reinterpret_cast<const double2*>(ring + (hs0 + h) * HSLOT + q * TB)[lane];
                         },
-                        xj, xi, prow, pcol, bi == bj, lane);
+                        end, xj, xi, prow, pcol, bi == bj, lane);
+                } else {
+                    const float* ringf = reinterpret_cast<const float*>(ring);
+                    tile_product_f32(
+                        begin,
+                        [&](int h, int q) {
+                            return reinterpret_cast<const float2*>(ringf + (hs0 + h) * (2 * HSLOT) + q * TB)[lane];
+                        },
+                        end, make_float2((float)xj.x, (float)xj.y), xif, prow, pcol, bi == bj, lane);
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[slot]);
+                if (tr) csum += gtime() - tc0;
             }
             it += (h64_valid(t) ? ntiles : 0) + (h32_valid(t) ? ntiles : 0);
             if (tr && lane == 0) {
                 atomicMax(tr + 4, gtime());
                 atomicAdd(tr + 7, wsum);
+                atomicAdd(tr + 10, csum);
             }
             // one release fence per warp and step, then bump the partial-product counters
             __syncwarp();
@@ -612,9 +706,13 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                 bi = tcs[bw + (long long)c * NB_W] >> 16;
                 bj = tcs[bw + (long long)c * NB_W] & 0xffff;
                 // pad columns meet zero entries of x; pad rows are zeroed by the owner
-                tile_product([&](int r) { return make_double2(seg[r - 2 * lane + 63], seg[r - 2 * lane + 62]); },
-                             xj, xi, pbk + ((long long)bi * nbb + bj) * TB, pbk + ((long long)bj * nbb + bi) * TB,
-                             bi == bj, lane);
+                tile_product([](int) {},
+                             [&](int h, int q) {
+                                 const int r = h * 32 + q;
+                                 return make_double2(seg[r - 2 * lane + 63], seg[r - 2 * lane + 62]);
+                             },
+                             [](int) {}, xj, xi, pbk + ((long long)bi * nbb + bj) * TB,
+                             pbk + ((long long)bj * nbb + bi) * TB, bi == bj, lane);
                 __syncwarp();
             }
             if (lane == 0 && nitems > 0) {
@@ -633,9 +731,9 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
 }
 
 int sweep_ir_smem_bytes() {
-    return NST * SLOT * (int)sizeof(double) +
+    return NHS * HSLOT * (int)sizeof(double) +
            (3 * NW * 32 + 4 * RCAP + NW * TB + NB_W * 96 + NB_W * 128) * (int)sizeof(double) + TCAP * (int)sizeof(int) +
-           2 * NST * (int)sizeof(uint64_t);
+           2 * NHS * (int)sizeof(uint64_t);
 }
 
 }  // namespace
@@ -701,6 +799,11 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
         return v ? std::atoi(v) : 1;
     }();
     a.evict_first = evict;
+    static const int pf = [] {
+        const char* v = std::getenv("FI_IR_PF");
+        return v ? std::atoi(v) : 0;
+    }();
+    a.pf_items = pf;
     a.trace = nullptr;
     static const bool tracing = std::getenv("FI_SWEEP_TRACE") != nullptr;
     const int nst1 = levels + 3;
@@ -722,7 +825,7 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
         auto ph = [&](int c, int t, int i) { return (double)h[((size_t)c * nst1 + t) * 12 + i]; };
         for (int lo : {1, nst1 / 2, nst1 - 40}) {
-            double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
             int cnt = 0;
             for (int c = 0; c < P->G; ++c)
                 for (int t = lo; t < lo + 32 && t < nst1 - 3; ++t) {
@@ -735,14 +838,15 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
                     acc[6] += ph(c, t, 7) / NST;
                     acc[7] += ph(c, t, 8) - ph(c, t, 3);
                     acc[8] += ph(c, t, 9) - ph(c, t, 3);
+                    acc[9] += ph(c, t, 10) / NST;
                     ++cnt;
                 }
             const double step = (ph(0, std::min(lo + 32, nst1 - 3), 0) - ph(0, lo, 0)) / 32;
             std::fprintf(stderr,
                          "[sweep_ir] steps %3d+: step %6.2f us | wait %6.2f | reduce %6.2f | x %6.2f | ring %6.2f | "
-                         "hist %6.2f | btiles %6.2f | ring data wait/warp %6.2f | ring x-poll %6.2f | b x-poll %6.2f\n",
+                         "hist %6.2f | btiles %6.2f | ring data wait/warp %6.2f | ring x-poll %6.2f | b x-poll %6.2f | ring item loop/warp %6.2f\n",
                          lo, step * 1e-3, acc[0] / cnt * 1e-3, acc[1] / cnt * 1e-3, acc[2] / cnt * 1e-3,
-                         acc[3] / cnt * 1e-3, acc[4] / cnt * 1e-3, acc[5] / cnt * 1e-3, acc[6] / cnt * 1e-3, acc[7] / cnt * 1e-3, acc[8] / cnt * 1e-3);
+                         acc[3] / cnt * 1e-3, acc[4] / cnt * 1e-3, acc[5] / cnt * 1e-3, acc[6] / cnt * 1e-3, acc[7] / cnt * 1e-3, acc[8] / cnt * 1e-3, acc[9] / cnt * 1e-3);
         }
     }
 }
