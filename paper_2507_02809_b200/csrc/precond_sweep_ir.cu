@@ -127,7 +127,7 @@ struct IrArgs {
     const double* z;
     double* y;    // output y1 + d
     double* Y1;   // sweep-1 result, all levels
-    double* DL;   // sweep-2 correction, all levels
+    float* DLf;   // sweep-2 correction, all levels (FP32 copy: only its history sums read it)
     const double* D1;
     const double* D2;
     const double* d2inv;
@@ -330,7 +330,7 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
     }
 
     // ---------------- workers
-    const long long R = (Np + G - 1) / G;
+    const long long R = ((Np + G - 1) / G + 3) / 4 * 4;  // multiple of 4: vector history loads
     const long long r0 = min(Np, (long long)blockIdx.x * R);
     const long long r1 = min(Np, r0 + R);
     const int rb0 = (int)(r0 / TB), rb1 = r1 > r0 ? (int)((r1 - 1) / TB) : rb0 - 1;
@@ -453,7 +453,7 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                 if (pad) v2 = 0.0;
                 if (rvalid) {
                     const long long o = (long long)(t - 3) * Np + r;
-                    a.DL[o] = v2;
+                    a.DLf[o] = (float)v2;
                     a.y[o] = c_y + v2;
                 }
             }
@@ -488,49 +488,87 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
         //   h1p = sum_{m<=t-1} e_{t+1-m} y1_m    (x1_{t+1}; + e1 y1_t at owner time)
         //   hrp = sum_{m<=t-1} e_{t-1-m} y1_m    (residual of level t-1)
         //   h2p = sum_{m<=t-3} e_{t-1-m} d_m     (x2_{t-1}; + e1 d_{t-2} at owner time)
-        // The loads are independent: 8 in flight per lane and array.
+        // These loads are latency-bound, so each instruction carries several levels: y1 as double2
+        // (2 rows per lane, 2 levels per load), d as float4 of its FP32 copy (4 rows, 4 levels), and
+        // 4 independent loads per lane and array are kept in flight.
         if (warp >= NST && t >= 1) {
             const int hw = warp - NST;
-            const double* ep = a.epad;  // zero outside 0..S-1: no bounds tests
-            {
-                double p1[8], pr[8], p2[8];
+            const double* ep = a.epad;  // zero outside 0..S-1
+            const int py = lane & 15, gy = lane >> 4;
+            const long long ry = r0 + 2 * py;
+            const bool vy = ry < r1;  // r1 - r0 is a multiple of 4
+            double2 a1 = make_double2(0.0, 0.0), ar = a1;
+            const int pd = lane & 7, gd = lane >> 3;
+            const long long rdr = r0 + 4 * pd;
+            const bool vd = rdr < r1;
+            double a2[4] = {0.0, 0.0, 0.0, 0.0};
+            // one round trip per iteration covers 80 levels of each array (8 double2 + 4 float4 loads)
+            for (int i0 = 0; i0 <= t - 1; i0 += 80) {
+                double2 yv[8];
+                float4 dv[4];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) p1[u] = pr[u] = p2[u] = 0.0;
-                for (int m0 = hw; m0 <= t - 1; m0 += 8 * NB_W) {
-                    double yv[8], dv[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int m = m0 + u * NB_W;
-                        yv[u] = m <= t - 1 ? __ldcg(a.Y1 + (long long)m * Np + rr) : 0.0;
-                        dv[u] = m <= t - 3 ? __ldcg(a.DL + (long long)m * Np + rr) : 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int m = m0 + u * NB_W;
-                        p1[u] += __ldg(ep + t + 1 - m) * yv[u];
-                        const double em = __ldg(ep + t - 1 - m);
-                        pr[u] += em * yv[u];
-                        p2[u] += em * dv[u];
-                    }
+                for (int u = 0; u < 8; ++u) {
+                    const int m = i0 + 2 * hw + gy + u * 2 * NB_W;
+                    yv[u] = vy && m <= t - 1 ? __ldcg(reinterpret_cast<const double2*>(a.Y1 + (long long)m * Np + ry))
+                                             : make_double2(0.0, 0.0);
                 }
-                double* rd = hred + hw * 96;
-                rd[lane] = ((p1[0] + p1[1]) + (p1[2] + p1[3])) + ((p1[4] + p1[5]) + (p1[6] + p1[7]));
-                rd[32 + lane] = ((pr[0] + pr[1]) + (pr[2] + pr[3])) + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
-                rd[64 + lane] = ((p2[0] + p2[1]) + (p2[2] + p2[3])) + ((p2[4] + p2[5]) + (p2[6] + p2[7]));
-                bwarp_bar();
-                if (hw == 0) {
-                    double s1 = 0.0, sr = 0.0, s2 = 0.0;
-                    for (int w = 0; w < NB_W; ++w) {
-                        s1 += hred[w * 96 + lane];
-                        sr += hred[w * 96 + 32 + lane];
-                        s2 += hred[w * 96 + 64 + lane];
-                    }
-                    h1p[lane] = s1;
-                    hrp[lane] = sr;
-                    h2p[lane] = s2;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int m = i0 + 4 * hw + gd + u * 4 * NB_W;
+                    dv[u] = vd && m <= t - 3 ? __ldcg(reinterpret_cast<const float4*>(a.DLf + (long long)m * Np + rdr))
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
-                bwarp_bar();
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int m = i0 + 2 * hw + gy + u * 2 * NB_W;
+                    const double e1 = __ldg(ep + t + 1 - m), er = __ldg(ep + t - 1 - m);
+                    a1.x += e1 * yv[u].x;
+                    a1.y += e1 * yv[u].y;
+                    ar.x += er * yv[u].x;
+                    ar.y += er * yv[u].y;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double em = __ldg(ep + t - 1 - (i0 + 4 * hw + gd + u * 4 * NB_W));
+                    a2[0] += em * dv[u].x;
+                    a2[1] += em * dv[u].y;
+                    a2[2] += em * dv[u].z;
+                    a2[3] += em * dv[u].w;
+                }
             }
+            // fold the level groups (lanes 16 apart for y1; 8 and 16 apart for d)
+            a1.x += __shfl_down_sync(0xffffffffu, a1.x, 16);
+            a1.y += __shfl_down_sync(0xffffffffu, a1.y, 16);
+            ar.x += __shfl_down_sync(0xffffffffu, ar.x, 16);
+            ar.y += __shfl_down_sync(0xffffffffu, ar.y, 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                a2[i] += __shfl_down_sync(0xffffffffu, a2[i], 16);
+                a2[i] += __shfl_down_sync(0xffffffffu, a2[i], 8);
+            }
+            double* rd = hred + hw * 96;
+            if (lane < 16) {
+                rd[2 * lane] = a1.x;
+                rd[2 * lane + 1] = a1.y;
+                rd[32 + 2 * lane] = ar.x;
+                rd[32 + 2 * lane + 1] = ar.y;
+            }
+            if (lane < 8)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) rd[64 + 4 * lane + i] = a2[i];
+            bwarp_bar();
+            if (hw == 0) {
+                double s1 = 0.0, sr = 0.0, s2 = 0.0;
+                for (int w = 0; w < NB_W; ++w) {
+                    s1 += hred[w * 96 + lane];
+                    sr += hred[w * 96 + 32 + lane];
+                    s2 += hred[w * 96 + 64 + lane];
+                }
+                h1p[lane] = s1;
+                hrp[lane] = sr;
+                h2p[lane] = s2;
+            }
+            bwarp_bar();
         }
         if (tr && threadIdx.x == NST * 32) tr[5] = gtime();
 
@@ -743,7 +781,7 @@ bool sweep_ir_available(const fi_precond* P) {
         const char* v = getenv("FI_SWEEP_IR");
         return v ? atoi(v) : 1;
     }();
-    return env != 0 && P->mode == 0 && P->Hf.p != nullptr && (P->sys->L.Np + P->G - 1) / P->G <= RCAP &&
+    return env != 0 && P->mode == 0 && P->Hf.p != nullptr && ((P->sys->L.Np + P->G - 1) / P->G + 3) / 4 * 4 <= RCAP &&
            P->nb <= KPW * NW && (P->T + P->G - 1) / P->G <= TCAP;
 }
 
@@ -759,7 +797,7 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
     }
     const fi_system* sys = P->sys;
     const Layout& L = sys->L;
-    if ((L.Np + P->G - 1) / P->G > RCAP) throw Error(FI_E_RESOURCE, "sweep_ir: too many rows per CTA");
+    if (((L.Np + P->G - 1) / P->G + 3) / 4 * 4 > RCAP) throw Error(FI_E_RESOURCE, "sweep_ir: too many rows per CTA");
     if (!P->ir_xb.p) {
         P->ir_xb.alloc((size_t)6 * L.Np);
         P->ir_pb.alloc((size_t)6 * P->nb * P->nb * TB);
@@ -780,7 +818,7 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
     a.z = z;
     a.y = y;
     a.Y1 = P->rbuf.p;
-    a.DL = P->dbuf.p;
+    a.DLf = reinterpret_cast<float*>(P->dbuf.p);
     a.D1 = sys->D1.p;
     a.D2 = sys->D2.p;
     a.d2inv = P->d2inv.p;

@@ -1,0 +1,40 @@
+"""End-to-end parity against the CPU oracle's GMRES(50) solves of the BASELINE configurations
+(tests/golden/oracle_config<i>.npz, made by tests/golden/gen_oracle_solutions.py on the identical
+seeded observation mu_eps).  The north star's bar: iteration count +-1, recovered f <= 1e-8."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2507_02809_b200.configs import RESTART, TOL, baseline_problem
+
+pytestmark = pytest.mark.gpu
+F = pytest.importorskip("paper_2507_02809_b200.fracinv")
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+def test_solve_matches_oracle_golden(cfg):
+    path = os.path.join(GOLDEN, f"oracle_config{cfg}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"oracle golden for config {cfg} not generated")
+    g = np.load(path)
+    A = F.SystemOperator(baseline_problem(F, cfg))
+    P = F.BlockTriangularPreconditioner(A)
+    z = F.build_rhs(A, g["mu_eps"]).z
+    x, rep = F.gmres(A, P, z, F.GmresOptions(TOL[cfg], 0, RESTART))
+    f = x[-A.N:]
+    print(f"config{cfg} ({P.inner}): {rep.iterations} iterations (oracle {int(g['iterations'])}), "
+          f"f parity {_rel(f, g['f']):.3e}, recon error {F.relative_error(A.spec.f_true, f):.3e} "
+          f"(oracle {float(g['recon_error']):.3e})")
+    assert rep.converged == bool(g["converged"])
+    assert abs(rep.iterations - int(g["iterations"])) <= 1
+    assert _rel(f, g["f"]) <= 1e-8
+    # the residual history follows the oracle's step by step (same Krylov space, same arithmetic order)
+    h, ho = np.asarray(rep.residual_history), np.asarray(g["history"])
+    k = min(len(h), len(ho))
+    assert np.allclose(h[:k], ho[:k], rtol=1e-4, atol=1e-14)
