@@ -101,8 +101,13 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
 }
 // Poll relaxed (an acquire load invalidates the SM's L1 on every iteration, evicting the symbol and
 // weight lines other warps read through L1), then one acquire load once the counter has moved.
+// Spin bound: a dataflow wait that exceeds ~seconds is a bug; trap instead of hanging the GPU.
+constexpr unsigned kSpinLimit = 1u << 25;
 __device__ __forceinline__ void warp_spin_until(const unsigned* p, unsigned target) {
-    while (!__all_sync(0xffffffffu, ld_relaxed(p) >= target)) __nanosleep(64);
+    for (unsigned n = 0; !__all_sync(0xffffffffu, ld_relaxed(p) >= target); ++n) {
+        __nanosleep(64);
+        if (n == kSpinLimit) __trap();
+    }
     (void)ld_acquire(p);
 }
 __device__ __forceinline__ void tile_coords(long long t, int& bi, int& bj) {
@@ -602,7 +607,10 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                     ctr = a.xready + blk * CSTR;
                     tgt = (unsigned)owners_of_block(blk, R, G) * xtarget_step;
                 }
-                while (!__all_sync(0xffffffffu, ctr == nullptr || ld_relaxed(ctr) >= tgt)) __nanosleep(64);
+                for (unsigned n = 0; !__all_sync(0xffffffffu, ctr == nullptr || ld_relaxed(ctr) >= tgt); ++n) {
+                    __nanosleep(64);
+                    if (n == kSpinLimit) __trap();
+                }
                 if (ctr) (void)ld_acquire(ctr);
             }
             if (tr && lane == 0) atomicMax(tr + 8, gtime());
@@ -712,7 +720,10 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                     ctr = a.xready + blk * CSTR;
                     tgt = (unsigned)owners_of_block(blk, R, G) * xtarget_step;
                 }
-                while (!__all_sync(0xffffffffu, ctr == nullptr || ld_relaxed(ctr) >= tgt)) __nanosleep(64);
+                for (unsigned n = 0; !__all_sync(0xffffffffu, ctr == nullptr || ld_relaxed(ctr) >= tgt); ++n) {
+                    __nanosleep(64);
+                    if (n == kSpinLimit) __trap();
+                }
                 if (ctr) (void)ld_acquire(ctr);
             }
             if (tr && lane == 0) atomicMax(tr + 9, gtime());
