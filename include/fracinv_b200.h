@@ -107,9 +107,10 @@ int fi_system_apply_host(fi_system* sys, const double* y_host, double* z_host);
 
 /* ------------------------------------------------------------------ preconditioner
  * Replaces BlockTriangularPreconditioner (krylov.hpp:33-50, krylov.cpp:24-70).
- * block_cap <= 0 selects the reference default 4096 (kDefaultBlockCap); N > block_cap
- * returns FI_E_RESOURCE like the reference.  Singular blocks return FI_E_SINGULAR with
- * the 1-based time index (S+1 = regularisation block). */
+ * block_cap <= 0 selects the reference default 4096 (kDefaultBlockCap).  N > block_cap returns
+ * FI_E_RESOURCE like the reference for 1D; for 2D it selects the substituted tau-PCG block solve
+ * (see fi_precond_create_ex), where the reference cannot run at all.  Singular blocks return
+ * FI_E_SINGULAR with the 1-based time index (S+1 = regularisation block). */
 int fi_precond_create(fi_system* sys, long long block_cap, fi_precond** out);
 /* Explicit choice of the per-block solve.  inner = 0: dense (the reference's direct solve, above
  * block_cap -> FI_E_RESOURCE); inner = 1: tau-preconditioned CG per block to relative residual

@@ -222,9 +222,18 @@ private:
 class BlockTriangularPreconditioner {
 public:
     static constexpr int64_t kDefaultBlockCap = 4096;
+    // per-block solve: Auto = the reference's dense solve up to block_cap, and above it (2D only)
+    // the substituted tau-preconditioned CG; Dense / TauPCG force one (fi_precond_create_ex)
+    enum class Inner : int { Auto = -1, Dense = 0, TauPCG = 1 };
     explicit BlockTriangularPreconditioner(const SystemOperator& A, int64_t block_cap = kDefaultBlockCap) : A_(&A) {
         check(fi_precond_create(A.handle(), block_cap, &h_));
     }
+    BlockTriangularPreconditioner(const SystemOperator& A, int64_t block_cap, Inner inner, double tol = 1e-14,
+                                  int maxit = 200)
+        : A_(&A) {
+        check(fi_precond_create_ex(A.handle(), block_cap, static_cast<int>(inner), tol, maxit, &h_));
+    }
+    Inner inner() const { return static_cast<Inner>(fi_precond_inner(h_)); }
     ~BlockTriangularPreconditioner() { fi_precond_destroy(h_); }
     BlockTriangularPreconditioner(const BlockTriangularPreconditioner&) = delete;
     BlockTriangularPreconditioner& operator=(const BlockTriangularPreconditioner&) = delete;

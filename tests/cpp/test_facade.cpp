@@ -61,9 +61,37 @@ int main(int argc, char** argv) {
     } catch (const DimensionError&) {
         dim_error = true;
     }
+    // the substituted 2D block solve (tau-PCG) against the dense inverses on a 15x15 grid
+    double tau_vs_dense = 1.0;
+    int tau_inner = -1;
+    {
+        SpaceGrid g2({15, 15}, {0.0, 0.0}, {1.0, 1.0});
+        const auto nodes2 = g2.nodes();
+        std::vector<double> rho2(nodes2.size(), 0.0), f2(nodes2.size());
+        for (size_t j = 0; j < nodes2.size(); ++j) f2[j] = std::sin(pi * nodes2[j][0]) * std::sin(pi * nodes2[j][1]);
+        ProblemSpec s2{0.3, 1.2, g2, 8, 1.0,
+                       [](const std::vector<double>& x, double) { return 1 + x[0] * x[1]; },
+                       [](const std::vector<double>& x, double t) { return 1 + x[0] * (1 + t); },
+                       [](double t) { return 1 + t * t; }, rho2, f2, 1e-3, 0.01};
+        SystemOperator A2(ctx, s2);
+        using Inner = BlockTriangularPreconditioner::Inner;
+        BlockTriangularPreconditioner Pt(A2, 4096, Inner::TauPCG), Pd(A2, 4096, Inner::Dense);
+        tau_inner = static_cast<int>(Pt.inner());
+        std::vector<double> v((size_t)A2.dim());
+        for (size_t i = 0; i < v.size(); ++i) v[i] = std::sin(0.37 * (double)i) + 0.25;
+        const auto yt = Pt.apply(v), yd = Pd.apply(v);
+        double num = 0.0, den = 0.0;
+        for (size_t i = 0; i < v.size(); ++i) {
+            num += (yt[i] - yd[i]) * (yt[i] - yd[i]);
+            den += yd[i] * yd[i];
+        }
+        tau_vs_dense = std::sqrt(num / den);
+    }
     std::printf("{\"iterations\": %d, \"converged\": %s, \"final_true_residual\": %.17g, \"recon_error\": %.17g, "
-                "\"singular_index\": %d, \"dimension_error\": %s, \"history_len\": %zu}\n",
+                "\"singular_index\": %d, \"dimension_error\": %s, \"history_len\": %zu, \"tau_inner\": %d, "
+                "\"tau_vs_dense\": %.17g}\n",
                 rep.iterations, rep.converged ? "true" : "false", rep.final_true_residual,
-                relative_error(f, frec), singular_index, dim_error ? "true" : "false", rep.residual_history.size());
+                relative_error(f, frec), singular_index, dim_error ? "true" : "false", rep.residual_history.size(),
+                tau_inner, tau_vs_dense);
     return 0;
 }

@@ -33,3 +33,4 @@ def test_cpp_facade_config0(tmp_path):
     assert rep["history_len"] == rep["iterations"] + 1
     assert np.linalg.norm(f - xo[-255:]) / np.linalg.norm(xo[-255:]) <= 1e-8
     assert rep["singular_index"] == 3 and rep["dimension_error"]
+    assert rep["tau_inner"] == 1 and rep["tau_vs_dense"] <= 1e-12  # substituted 2D block solve
