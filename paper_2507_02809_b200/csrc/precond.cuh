@@ -36,6 +36,9 @@ struct fi_precond {
     fib::DevBuf<int> it_direct_d, it_level;
     fib::DevBuf<unsigned> it_ticket;
     fib::DevBuf<unsigned long long> it_kcount;  // kernels executed inside the CG graphs
+    int it_fgrid = 0;                            // fused kernel: cooperative grid size
+    fib::DevBuf<double> it_fparts;               // fused kernel: 2 x grid block partials
+    fib::DevBuf<unsigned> it_fbar;               // fused kernel: grid-barrier counter
     struct GraphEntry {
         const double* z;
         double* y;

@@ -14,7 +14,10 @@
 // Control flow never returns to the host inside an apply: the whole forward substitution is ONE
 // CUDA graph — a conditional WHILE node over levels whose body holds a conditional WHILE node over
 // CG steps; the kernels set the loop conditions on the device (cudaGraphSetConditional).
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "precond.cuh"
@@ -22,7 +25,8 @@
 namespace fib {
 namespace {
 
-constexpr int CB = 4;  // columns per column-FFT CTA
+constexpr int CB = 4;   // columns per column-FFT CTA (graph path)
+constexpr int CBF = 2;  // columns per column group (fused kernel: 2 CTAs per SM, L2 / 2 groups)
 
 struct IterScalars {
     double bnorm2, rnorm2, rz, pap, alpha, beta;
@@ -442,6 +446,323 @@ __global__ void fft_cols_to_spec(ItArgs a, double* lamB) {
     }
 }
 
+// ------------------------------------------------------------------ fused persistent solve
+// The whole forward substitution of a tau-PCG preconditioner apply in ONE cooperative kernel: the
+// level loop and the CG loop run on the device, the FFT passes of a CG step are phases separated
+// by grid barriers (6 per step instead of 7 dependent kernel launches), the scalars of the
+// recurrence (alpha, beta, rz, ...) live in every CTA's registers, and the global dot products are
+// summed in a fixed order (every CTA obtains the identical, bit-reproducible value).
+struct FusedCtl {
+    unsigned* bar;    // monotone grid-barrier counter (zeroed before the launch)
+    double* parts;    // 2 x G block partials (ping-pong by reduction index)
+    unsigned long long* trace;  // optional [8] per-phase time sums of CTA 0 (FI_ITER_TRACE=1)
+};
+__device__ __forceinline__ unsigned long long gtime_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
+    if (skipped(a)) return;
+    extern __shared__ double2 sm[];
+    __shared__ double wred[8];
+    __shared__ double bcast;
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
+    const long long Np = a.Np;
+    unsigned target = 0;
+    int rk = 0;
+    unsigned long long tlast = 0;
+    auto stamp = [&](int ph) {
+        if (ctl.trace && cta == 0 && tid == 0) {
+            const unsigned long long now = gtime_ns();
+            if (tlast) ctl.trace[ph] += now - tlast;
+            tlast = now;
+        }
+    };
+    auto gsync = [&]() {
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned long long t0 = ctl.trace && cta == 0 ? gtime_ns() : 0;
+            target += (unsigned)G;
+            __threadfence();
+            atomicAdd(ctl.bar, 1u);
+            unsigned n = 0;
+            while (ld_acquire_u32(ctl.bar) < target) {
+                __nanosleep(32);
+                if (++n == (1u << 26)) __trap();
+            }
+            if (ctl.trace && cta == 0) {
+                ctl.trace[8] += gtime_ns() - t0;
+                ctl.trace[9] += 1;
+            }
+        }
+        __syncthreads();
+    };
+    // deterministic grid sum: block partials in fixed order, every CTA gets the same total
+    auto greduce = [&](double v) -> double {
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) wred[warp] = v;
+        __syncthreads();
+        double* pp = ctl.parts + (rk & 1) * G;
+        if (tid == 0) {
+            double b = 0.0;
+            for (int w = 0; w < nwarp; ++w) b += wred[w];
+            __stcg(pp + cta, b);
+        }
+        gsync();
+        if (warp == 0) {
+            double t = 0.0;
+            for (int k = lane; k < G; k += 32) t += __ldcg(pp + k);
+            for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+            if (lane == 0) bcast = t;
+        }
+        __syncthreads();
+        ++rk;
+        return bcast;
+    };
+    const double sc1 = sqrt(2.0 / (a.n1 + 1)) * -0.5, sc2 = sqrt(2.0 / (a.n2 + 1)) * -0.5;
+    double2* u = sm;
+    double2* v = sm + max(a.L2, CBF * a.L1);  // ping-pong halves: row phases use L2, column phases CBF x L1
+
+    // rows n1..L1-1 of the embedded B input stay zero for the whole apply
+    for (long long q = (long long)cta * nthr + tid; q < (long long)(a.L1 - a.n1) * a.L2; q += (long long)G * nthr)
+        a.X[(long long)a.n1 * a.L2 + q] = make_double2(0.0, 0.0);
+
+    // DST-I of `src` rows (stride sstride, n2 values) into Rr rows; returns nothing
+    auto dst_row = [&](const double* src, int i1, double* out, long long ostride) {
+        for (int j = tid; j < a.L2; j += nthr) {
+            double val = 0.0;
+            if (j >= 1 && j <= a.n2) val = src[j - 1];
+            else if (j >= a.n2 + 2) val = -src[a.L2 - j - 1];
+            u[j] = make_double2(val, 0.0);
+        }
+        __syncthreads();
+        const double2* U = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, false, tid, nthr);
+        for (int k = tid; k < a.n2; k += nthr) out[(long long)i1 * ostride + k] = sc2 * U[k + 1].y;
+        __syncthreads();
+    };
+    // column pass of the tau solve: DST along columns, divide by the tau eigenvalues, DST back
+    auto tau_cols_phase = [&](int lv) {
+        const double c = level_c(a, lv), dmean = level_dmean(a, lv);
+        const int ngroups = (a.n2 + CBF - 1) / CBF;
+        for (int g = cta; g < ngroups; g += G) {
+            const int k0 = g * CBF, nc = min(CBF, a.n2 - k0);
+            for (int q = tid; q < CBF * a.L1; q += nthr) {
+                const int cc = q / a.L1, j = q - cc * a.L1;
+                double val = 0.0;
+                if (cc < nc) {
+                    if (j >= 1 && j <= a.n1) val = a.Rr[(long long)(j - 1) * a.n2 + k0 + cc];
+                    else if (j >= a.n1 + 2) val = -a.Rr[(long long)(a.L1 - j - 1) * a.n2 + k0 + cc];
+                }
+                u[q] = make_double2(val, 0.0);
+            }
+            __syncthreads();
+            double2* U = fft_smem(u, v, CBF, a.L1, a.lg1, a.tw1, false, tid, nthr);
+            double2* W = U == u ? v : u;
+            for (int q = tid; q < CBF * a.L1; q += nthr) {
+                const int cc = q / a.L1, j = q - cc * a.L1;
+                double val = 0.0;
+                if (cc < nc) {
+                    int k = -1;
+                    double sgn = 1.0;
+                    if (j >= 1 && j <= a.n1) k = j;
+                    else if (j >= a.n1 + 2) {
+                        k = a.L1 - j;
+                        sgn = -1.0;
+                    }
+                    if (k > 0) {
+                        const double coef = sc1 * U[cc * a.L1 + k].y;
+                        const double lam = c * a.lamT[(long long)(k - 1) * a.n2 + k0 + cc] + dmean;
+                        val = sgn * coef / lam;
+                    }
+                }
+                W[q] = make_double2(val, 0.0);
+            }
+            __syncthreads();
+            double2* V = W == u ? v : u;
+            const double2* R = fft_smem(W, V, CBF, a.L1, a.lg1, a.tw1, false, tid, nthr);
+            for (int q = tid; q < nc * a.n1; q += nthr) {
+                const int cc = q / a.n1, k = q - cc * a.n1;
+                a.Rr[(long long)k * a.n2 + k0 + cc] = sc1 * R[cc * a.L1 + k + 1].y;
+            }
+            __syncthreads();
+        }
+    };
+    // final row pass of the tau solve: zz = DST rows of Rr, returns the partial r.zz; init: p = zz
+    auto tau_out_phase = [&](bool init) -> double {
+        double part = 0.0;
+        for (int i1 = cta; i1 < a.n1; i1 += G) {
+            const double* src = a.Rr + (long long)i1 * a.n2;
+            for (int j = tid; j < a.L2; j += nthr) {
+                double val = 0.0;
+                if (j >= 1 && j <= a.n2) val = src[j - 1];
+                else if (j >= a.n2 + 2) val = -src[a.L2 - j - 1];
+                u[j] = make_double2(val, 0.0);
+            }
+            __syncthreads();
+            const double2* U = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, false, tid, nthr);
+            const long long base = (long long)i1 * a.ld2;
+            for (int k = tid; k < a.n2; k += nthr) {
+                const double zv = sc2 * U[k + 1].y;
+                a.zz[base + k] = zv;
+                if (init) a.p[base + k] = zv;
+                part += a.r[base + k] * zv;
+            }
+            __syncthreads();
+        }
+        return part;
+    };
+
+    for (int lv = 0; lv < a.levels; ++lv) {
+        // ---- level setup: rhs (forward substitution, krylov.cpp:55-68), b = rhs / D2, x = 0
+        const bool direct = lv < a.S && a.direct[lv];
+        double* x = a.y + (long long)lv * Np;
+        double part = 0.0;
+        for (long long i = (long long)cta * nthr + tid; i < Np; i += (long long)G * nthr) {
+            const int i2 = (int)(i % a.ld2);
+            double b = 0.0, xv = 0.0;
+            if (i2 < a.n2) {
+                if (lv < a.S) {
+                    double h[4] = {0.0, 0.0, 0.0, 0.0};
+                    int m = 0;
+                    for (; m + 3 < lv; m += 4)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) h[q] += a.e[lv - m - q] * a.y[(long long)(m + q) * Np + i];
+                    for (; m < lv; ++m) h[0] += a.e[lv - m] * a.y[(long long)m * Np + i];
+                    const double hist = (h[0] + h[1]) + (h[2] + h[3]);
+                    const long long o = (long long)lv * Np + i;
+                    const double rhs = a.z_in[o] - a.D1[o] * hist;
+                    if (direct) xv = rhs / (a.e0 * a.D1[o]);
+                    else b = rhs * a.d2inv[o];
+                } else {
+                    const double rhs = a.z_in[(long long)a.S * Np + i] - a.y[(long long)(a.S - 1) * Np + i];
+                    b = rhs * a.d2inv[(long long)(a.S - 1) * Np + i];
+                }
+            }
+            a.r[i] = b;
+            a.p[i] = 0.0;
+            x[i] = xv;
+            part += b * b;
+        }
+        stamp(7);
+        const double bn2 = greduce(part);
+        stamp(0);
+        bool conv = bn2 == 0.0 || direct;
+        if (conv) continue;
+        const double c = level_c(a, lv);
+        // ---- initial tau solve: zz = tau^{-1} r, p = zz, rz = r.zz
+        for (int i1 = cta; i1 < a.n1; i1 += G) dst_row(a.r + (long long)i1 * a.ld2, i1, a.Rr, a.n2);
+        gsync();
+        tau_cols_phase(lv);
+        gsync();
+        double rz = greduce(tau_out_phase(true));
+        stamp(1);
+        double beta = 0.0;
+        int it = 0;
+        while (true) {
+            // B1: p = zz + beta p (after the first step), row FFT of the embedded p
+            for (int i1 = cta; i1 < a.n1; i1 += G) {
+                const long long base = (long long)i1 * a.ld2;
+                for (int j = tid; j < a.L2; j += nthr) {
+                    double val = 0.0;
+                    if (j < a.n2) {
+                        val = a.p[base + j];
+                        if (it > 0) {
+                            val = a.zz[base + j] + beta * val;
+                            a.p[base + j] = val;
+                        }
+                    }
+                    u[j] = make_double2(val, 0.0);
+                }
+                __syncthreads();
+                const double2* U = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, false, tid, nthr);
+                double2* Xrow = a.X + (long long)i1 * a.L2;
+                for (int j = tid; j < a.L2; j += nthr) Xrow[j] = U[j];
+                __syncthreads();
+            }
+            gsync();
+            stamp(2);
+            // B2: column FFT, times the circulant spectrum, inverse column FFT
+            for (int g = cta; g < a.L2 / CBF; g += G) {
+                const int k0 = g * CBF;
+                for (int q = tid; q < CBF * a.L1; q += nthr) {
+                    const int cc = q / a.L1, j = q - cc * a.L1;
+                    u[q] = a.X[(long long)j * a.L2 + k0 + cc];
+                }
+                __syncthreads();
+                double2* U = fft_smem(u, v, CBF, a.L1, a.lg1, a.tw1, false, tid, nthr);
+                for (int q = tid; q < CBF * a.L1; q += nthr) {
+                    const int cc = q / a.L1, j = q - cc * a.L1;
+                    const double lam = a.lamB[(long long)j * a.L2 + k0 + cc];
+                    U[q] = make_double2(U[q].x * lam, U[q].y * lam);
+                }
+                __syncthreads();
+                double2* W = U == u ? v : u;
+                const double2* Y = fft_smem(U, W, CBF, a.L1, a.lg1, a.tw1, true, tid, nthr);
+                for (int q = tid; q < CBF * a.L1; q += nthr) {
+                    const int cc = q / a.L1, j = q - cc * a.L1;
+                    if (j < a.n1) a.X[(long long)j * a.L2 + k0 + cc] = Y[q];
+                }
+                __syncthreads();
+            }
+            gsync();
+            stamp(3);
+            // B3: inverse row FFT, Ap = c B p + delta o p, p.Ap
+            part = 0.0;
+            for (int i1 = cta; i1 < a.n1; i1 += G) {
+                const double2* Xrow = a.X + (long long)i1 * a.L2;
+                for (int j = tid; j < a.L2; j += nthr) u[j] = Xrow[j];
+                __syncthreads();
+                const double2* Y = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, true, tid, nthr);
+                const long long base = (long long)i1 * a.ld2;
+                const long long lo = (long long)min(lv, a.S - 1) * Np + base;
+                for (int j = tid; j < a.n2; j += nthr) {
+                    const double pv = a.p[base + j];
+                    const double delta = lv < a.S ? a.e0 * a.D1[lo + j] * a.d2inv[lo + j] : 0.0;
+                    const double ap = c * (Y[j].x * a.inv_LL) + delta * pv;
+                    a.Ap[base + j] = ap;
+                    part += pv * ap;
+                }
+                __syncthreads();
+            }
+            const double alpha = rz / greduce(part);
+            stamp(4);
+            // U + T1: x += alpha p, r -= alpha Ap, ||r||^2, and the DST rows of the new r
+            part = 0.0;
+            for (int i1 = cta; i1 < a.n1; i1 += G) {
+                const long long base = (long long)i1 * a.ld2;
+                for (int j = tid; j < a.n2; j += nthr) {
+                    x[base + j] += alpha * a.p[base + j];
+                    const double rv = a.r[base + j] - alpha * a.Ap[base + j];
+                    a.r[base + j] = rv;
+                    part += rv * rv;
+                }
+                __syncthreads();
+                dst_row(a.r + base, i1, a.Rr, a.n2);
+            }
+            const double rn2 = greduce(part);
+            stamp(5);
+            ++it;
+            if (sqrt(rn2) <= a.tol * sqrt(bn2) || it >= a.maxit) break;
+            tau_cols_phase(lv);
+            gsync();
+            stamp(6);
+            const double rz_new = greduce(tau_out_phase(false));
+            stamp(7);
+            beta = rz_new / rz;
+            rz = rz_new;
+        }
+    }
+}
+
 int ilog2(int v) {
     int l = 0;
     while ((1 << l) < v) ++l;
@@ -688,6 +1009,55 @@ void precond_build_iterative(fi_precond* P, double tol, int maxit) {
 }
 
 void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip) {
+    static const bool use_graph = [] {
+        const char* v = std::getenv("FI_ITER_GRAPH");
+        return v && std::atoi(v) != 0;
+    }();
+    if (!use_graph) {
+        // one cooperative kernel for the whole substitution (tau_pcg_fused)
+        ItArgs a = make_args(P);
+        a.z_in = z;
+        a.y = y;
+        a.levels = levels;
+        a.skip = skip;
+        const size_t smem = 2 * (size_t)std::max(a.L2, CBF * a.L1) * sizeof(double2);
+        static size_t configured = 0;
+        if (smem > configured) {
+            FI_CUDA(cudaFuncSetAttribute(tau_pcg_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            configured = smem;
+        }
+        if (P->it_fgrid == 0) {
+            int per_sm = 0;
+            FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tau_pcg_fused, 256, smem));
+            if (per_sm < 1) throw Error(FI_E_CUDA, "tau_pcg_fused cannot be resident");
+            P->it_fgrid = ctx->sm_count * std::min(per_sm, 2);
+            P->it_fparts.alloc((size_t)2 * P->it_fgrid);
+            P->it_fbar.alloc(1);
+        }
+        static const bool tracing = std::getenv("FI_ITER_TRACE") != nullptr;
+        DevBuf<unsigned long long> trace;
+        if (tracing) {
+            trace.alloc(10);
+            FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
+        }
+        FusedCtl ctl{P->it_fbar.p, P->it_fparts.p, tracing ? trace.p : nullptr};
+        FI_CUDA(cudaMemsetAsync(P->it_fbar.p, 0, sizeof(unsigned), ctx->stream));
+        void* args[] = {&a, &ctl};
+        FI_CUDA(cudaLaunchCooperativeKernel((const void*)tau_pcg_fused, dim3(P->it_fgrid), dim3(256), args, smem,
+                                            ctx->stream));
+        FI_LAUNCHED(ctx);
+        if (tracing) {
+            unsigned long long h[10];
+            FI_CUDA(cudaMemcpyAsync(h, trace.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+            FI_CUDA(cudaStreamSynchronize(ctx->stream));
+            std::fprintf(stderr,
+                         "[tau_pcg_fused] ms: setup %.3f | tau0 %.3f | B1 %.3f | B2 %.3f | B3+red %.3f | U+T1+red %.3f | "
+                         "T2 %.3f | T3+red %.3f | barrier wait (CTA 0) %.3f over %llu barriers\n",
+                         h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6, h[4] * 1e-6, h[5] * 1e-6, h[6] * 1e-6,
+                         h[7] * 1e-6, h[8] * 1e-6, h[9]);
+        }
+        return;
+    }
     cudaGraphExec_t exec = nullptr;
     for (auto& gE : P->it_graphs)
         if (gE.z == z && gE.y == y && gE.levels == levels && gE.skip == skip) exec = gE.exec;
