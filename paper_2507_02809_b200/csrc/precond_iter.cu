@@ -101,6 +101,74 @@ __device__ double2* fft_smem(double2* src, double2* dst, int cnt, int L, int lg,
     return src;
 }
 
+// Radix-4 Stockham variant for the fused kernel: half the passes (and __syncthreads) of fft_smem,
+// power-of-two index arithmetic, twiddles from a shared-memory copy of the half table
+// (tw[t] = exp(-2 pi i t / L), t < L/2; t >= L/2 uses -tw[t - L/2]).  Same transform as fft_smem.
+__device__ __forceinline__ double2 tw_at(const double2* tw, int t, int half) {
+    if (t < half) return tw[t];
+    const double2 w = tw[t - half];
+    return make_double2(-w.x, -w.y);
+}
+__device__ double2* fft4_smem(double2* src, double2* dst, int cnt, int L, int lg, const double2* tw, bool inverse,
+                              int tid, int nthr) {
+    const int half = L >> 1;
+    int s = 0, p = 1;
+    if (lg & 1) {  // one radix-2 pass first (p = 1: no twiddles)
+        for (int q = tid; q < cnt * half; q += nthr) {
+            const int c = q >> (lg - 1), j = q & (half - 1);
+            const double2* sc = src + c * L;
+            double2* dc = dst + c * L;
+            const double2 x0 = sc[j], x1 = sc[j + half];
+            dc[2 * j] = make_double2(x0.x + x1.x, x0.y + x1.y);
+            dc[2 * j + 1] = make_double2(x0.x - x1.x, x0.y - x1.y);
+        }
+        __syncthreads();
+        double2* t = src;
+        src = dst;
+        dst = t;
+        s = 1;
+        p = 2;
+    }
+    const int quarter = L >> 2;
+    for (; s < lg; s += 2, p <<= 2) {
+        const int lgp = s;  // p = 2^s
+        const int tstep = L >> (lgp + 2);  // L / (4p)
+        for (int q = tid; q < cnt * quarter; q += nthr) {
+            const int c = q >> (lg - 2), j = q & (quarter - 1);
+            const int k = j & (p - 1);
+            const double2* sc = src + c * L;
+            double2* dc = dst + c * L;
+            double2 a0 = sc[j], a1 = sc[j + quarter], a2 = sc[j + 2 * quarter], a3 = sc[j + 3 * quarter];
+            if (k) {
+                double2 w1 = tw_at(tw, k * tstep, half), w2 = tw_at(tw, 2 * k * tstep, half),
+                        w3 = tw_at(tw, 3 * k * tstep, half);
+                if (inverse) {
+                    w1.y = -w1.y;
+                    w2.y = -w2.y;
+                    w3.y = -w3.y;
+                }
+                a1 = cmul(a1, w1);
+                a2 = cmul(a2, w2);
+                a3 = cmul(a3, w3);
+            }
+            const double2 s02 = make_double2(a0.x + a2.x, a0.y + a2.y), d02 = make_double2(a0.x - a2.x, a0.y - a2.y);
+            const double2 s13 = make_double2(a1.x + a3.x, a1.y + a3.y), d13 = make_double2(a1.x - a3.x, a1.y - a3.y);
+            // forward: y1 = d02 - i d13, y3 = d02 + i d13 (inverse: signs of i swapped)
+            const double2 id13 = inverse ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x);  // -/+ i d13
+            const int o = 4 * (j - k) + k;
+            dc[o] = make_double2(s02.x + s13.x, s02.y + s13.y);
+            dc[o + p] = make_double2(d02.x + id13.x, d02.y + id13.y);
+            dc[o + 2 * p] = make_double2(s02.x - s13.x, s02.y - s13.y);
+            dc[o + 3 * p] = make_double2(d02.x - id13.x, d02.y - id13.y);
+        }
+        __syncthreads();
+        double2* t = src;
+        src = dst;
+        dst = t;
+    }
+    return src;
+}
+
 // ------------------------------------------------------------------ deterministic grid reduction
 // Block-reduce v, write the block partial; thread 0 of the last block to finish returns true with
 // the grid total summed in fixed block order.
@@ -529,8 +597,14 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         return bcast;
     };
     const double sc1 = sqrt(2.0 / (a.n1 + 1)) * -0.5, sc2 = sqrt(2.0 / (a.n2 + 1)) * -0.5;
+    const int hs = max(a.L2, CBF * a.L1);
     double2* u = sm;
-    double2* v = sm + max(a.L2, CBF * a.L1);  // ping-pong halves: row phases use L2, column phases CBF x L1
+    double2* v = sm + hs;  // ping-pong halves: row phases use L2, column phases CBF x L1
+    double2* tws1 = sm + 2 * hs;  // twiddle half tables in shared memory
+    double2* tws2 = tws1 + a.L1 / 2;
+    for (int t = tid; t < a.L1 / 2; t += nthr) tws1[t] = a.tw1[t];
+    for (int t = tid; t < a.L2 / 2; t += nthr) tws2[t] = a.tw2[t];
+    __syncthreads();
 
     // rows n1..L1-1 of the embedded B input stay zero for the whole apply
     for (long long q = (long long)cta * nthr + tid; q < (long long)(a.L1 - a.n1) * a.L2; q += (long long)G * nthr)
@@ -545,7 +619,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
             u[j] = make_double2(val, 0.0);
         }
         __syncthreads();
-        const double2* U = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, false, tid, nthr);
+        const double2* U = fft4_smem(u, v, 1, a.L2, a.lg2, tws2, false, tid, nthr);
         for (int k = tid; k < a.n2; k += nthr) out[(long long)i1 * ostride + k] = sc2 * U[k + 1].y;
         __syncthreads();
     };
@@ -565,7 +639,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                 u[q] = make_double2(val, 0.0);
             }
             __syncthreads();
-            double2* U = fft_smem(u, v, CBF, a.L1, a.lg1, a.tw1, false, tid, nthr);
+            double2* U = fft4_smem(u, v, CBF, a.L1, a.lg1, tws1, false, tid, nthr);
             double2* W = U == u ? v : u;
             for (int q = tid; q < CBF * a.L1; q += nthr) {
                 const int cc = q / a.L1, j = q - cc * a.L1;
@@ -588,7 +662,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
             }
             __syncthreads();
             double2* V = W == u ? v : u;
-            const double2* R = fft_smem(W, V, CBF, a.L1, a.lg1, a.tw1, false, tid, nthr);
+            const double2* R = fft4_smem(W, V, CBF, a.L1, a.lg1, tws1, false, tid, nthr);
             for (int q = tid; q < nc * a.n1; q += nthr) {
                 const int cc = q / a.n1, k = q - cc * a.n1;
                 a.Rr[(long long)k * a.n2 + k0 + cc] = sc1 * R[cc * a.L1 + k + 1].y;
@@ -608,7 +682,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                 u[j] = make_double2(val, 0.0);
             }
             __syncthreads();
-            const double2* U = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, false, tid, nthr);
+            const double2* U = fft4_smem(u, v, 1, a.L2, a.lg2, tws2, false, tid, nthr);
             const long long base = (long long)i1 * a.ld2;
             for (int k = tid; k < a.n2; k += nthr) {
                 const double zv = sc2 * U[k + 1].y;
@@ -683,7 +757,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                     u[j] = make_double2(val, 0.0);
                 }
                 __syncthreads();
-                const double2* U = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, false, tid, nthr);
+                const double2* U = fft4_smem(u, v, 1, a.L2, a.lg2, tws2, false, tid, nthr);
                 double2* Xrow = a.X + (long long)i1 * a.L2;
                 for (int j = tid; j < a.L2; j += nthr) Xrow[j] = U[j];
                 __syncthreads();
@@ -698,7 +772,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                     u[q] = a.X[(long long)j * a.L2 + k0 + cc];
                 }
                 __syncthreads();
-                double2* U = fft_smem(u, v, CBF, a.L1, a.lg1, a.tw1, false, tid, nthr);
+                double2* U = fft4_smem(u, v, CBF, a.L1, a.lg1, tws1, false, tid, nthr);
                 for (int q = tid; q < CBF * a.L1; q += nthr) {
                     const int cc = q / a.L1, j = q - cc * a.L1;
                     const double lam = a.lamB[(long long)j * a.L2 + k0 + cc];
@@ -706,7 +780,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                 }
                 __syncthreads();
                 double2* W = U == u ? v : u;
-                const double2* Y = fft_smem(U, W, CBF, a.L1, a.lg1, a.tw1, true, tid, nthr);
+                const double2* Y = fft4_smem(U, W, CBF, a.L1, a.lg1, tws1, true, tid, nthr);
                 for (int q = tid; q < CBF * a.L1; q += nthr) {
                     const int cc = q / a.L1, j = q - cc * a.L1;
                     if (j < a.n1) a.X[(long long)j * a.L2 + k0 + cc] = Y[q];
@@ -721,7 +795,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                 const double2* Xrow = a.X + (long long)i1 * a.L2;
                 for (int j = tid; j < a.L2; j += nthr) u[j] = Xrow[j];
                 __syncthreads();
-                const double2* Y = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, true, tid, nthr);
+                const double2* Y = fft4_smem(u, v, 1, a.L2, a.lg2, tws2, true, tid, nthr);
                 const long long base = (long long)i1 * a.ld2;
                 const long long lo = (long long)min(lv, a.S - 1) * Np + base;
                 for (int j = tid; j < a.n2; j += nthr) {
@@ -1020,7 +1094,7 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
         a.y = y;
         a.levels = levels;
         a.skip = skip;
-        const size_t smem = 2 * (size_t)std::max(a.L2, CBF * a.L1) * sizeof(double2);
+        const size_t smem = (2 * (size_t)std::max(a.L2, CBF * a.L1) + a.L1 / 2 + a.L2 / 2) * sizeof(double2);
         static size_t configured = 0;
         if (smem > configured) {
             FI_CUDA(cudaFuncSetAttribute(tau_pcg_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
