@@ -742,7 +742,9 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         double beta = 0.0;
         int it = 0;
         while (true) {
-            // B1: p = zz + beta p (after the first step), row FFT of the embedded p
+            // B1: p = zz + beta p (after the first step), row FFT of the embedded p; partial delta p.p
+            const long long lo_lv = (long long)min(lv, a.S - 1) * Np;  // D1, 1/D2 rows of the level
+            double pdp = 0.0;
             for (int i1 = cta; i1 < a.n1; i1 += G) {
                 const long long base = (long long)i1 * a.ld2;
                 for (int j = tid; j < a.L2; j += nthr) {
@@ -753,6 +755,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                             val = a.zz[base + j] + beta * val;
                             a.p[base + j] = val;
                         }
+                        if (lv < a.S) pdp += a.e0 * a.D1[lo_lv + base + j] * a.d2inv[lo_lv + base + j] * val * val;
                     }
                     u[j] = make_double2(val, 0.0);
                 }
@@ -764,32 +767,48 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
             }
             gsync();
             stamp(2);
-            // B2: column FFT, times the circulant spectrum, inverse column FFT
+            // B2: column FFT, times the circulant spectrum, inverse column FFT.  By Parseval the
+            // spectrum also gives p.Bp = sum lam |P^|^2 / (L1 L2), so p.Ap = c p.Bp + p.delta.p is
+            // known here and the inverse row pass can update x and r at once.
+            double pbp = 0.0;
             for (int g = cta; g < a.L2 / CBF; g += G) {
                 const int k0 = g * CBF;
-                for (int q = tid; q < CBF * a.L1; q += nthr) {
-                    const int cc = q / a.L1, j = q - cc * a.L1;
-                    u[q] = a.X[(long long)j * a.L2 + k0 + cc];
+                // element q = (row j, column cc) with the column fastest: CBF adjacent values per row
+                double lamv[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int q = tid + t * nthr;
+                    const int cc = q & (CBF - 1), j = q / CBF;
+                    if (q < CBF * a.L1) {
+                        u[cc * a.L1 + j] = a.X[(long long)j * a.L2 + k0 + cc];
+                        lamv[t] = a.lamB[(long long)j * a.L2 + k0 + cc];
+                    }
                 }
                 __syncthreads();
                 double2* U = fft4_smem(u, v, CBF, a.L1, a.lg1, tws1, false, tid, nthr);
-                for (int q = tid; q < CBF * a.L1; q += nthr) {
-                    const int cc = q / a.L1, j = q - cc * a.L1;
-                    const double lam = a.lamB[(long long)j * a.L2 + k0 + cc];
-                    U[q] = make_double2(U[q].x * lam, U[q].y * lam);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int q = tid + t * nthr;
+                    const int cc = q & (CBF - 1), j = q / CBF;
+                    if (q < CBF * a.L1) {
+                        const double2 w = U[cc * a.L1 + j];
+                        pbp += lamv[t] * (w.x * w.x + w.y * w.y);
+                        U[cc * a.L1 + j] = make_double2(w.x * lamv[t], w.y * lamv[t]);
+                    }
                 }
                 __syncthreads();
                 double2* W = U == u ? v : u;
                 const double2* Y = fft4_smem(U, W, CBF, a.L1, a.lg1, tws1, true, tid, nthr);
-                for (int q = tid; q < CBF * a.L1; q += nthr) {
-                    const int cc = q / a.L1, j = q - cc * a.L1;
-                    if (j < a.n1) a.X[(long long)j * a.L2 + k0 + cc] = Y[q];
+                for (int q = tid; q < CBF * a.n1; q += nthr) {
+                    const int cc = q & (CBF - 1), j = q / CBF;
+                    a.X[(long long)j * a.L2 + k0 + cc] = Y[cc * a.L1 + j];
                 }
                 __syncthreads();
             }
-            gsync();
+            const double alpha = rz / greduce(c * a.inv_LL * pbp + pdp);
             stamp(3);
-            // B3: inverse row FFT, Ap = c B p + delta o p, p.Ap
+            // B3: inverse row FFT, Ap = c B p + delta o p; x += alpha p, r -= alpha Ap, ||r||^2, and
+            // the DST rows of the new r (first pass of the next tau solve)
             part = 0.0;
             for (int i1 = cta; i1 < a.n1; i1 += G) {
                 const double2* Xrow = a.X + (long long)i1 * a.L2;
@@ -797,33 +816,21 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                 __syncthreads();
                 const double2* Y = fft4_smem(u, v, 1, a.L2, a.lg2, tws2, true, tid, nthr);
                 const long long base = (long long)i1 * a.ld2;
-                const long long lo = (long long)min(lv, a.S - 1) * Np + base;
                 for (int j = tid; j < a.n2; j += nthr) {
                     const double pv = a.p[base + j];
-                    const double delta = lv < a.S ? a.e0 * a.D1[lo + j] * a.d2inv[lo + j] : 0.0;
+                    const double delta = lv < a.S ? a.e0 * a.D1[lo_lv + base + j] * a.d2inv[lo_lv + base + j] : 0.0;
                     const double ap = c * (Y[j].x * a.inv_LL) + delta * pv;
-                    a.Ap[base + j] = ap;
-                    part += pv * ap;
-                }
-                __syncthreads();
-            }
-            const double alpha = rz / greduce(part);
-            stamp(4);
-            // U + T1: x += alpha p, r -= alpha Ap, ||r||^2, and the DST rows of the new r
-            part = 0.0;
-            for (int i1 = cta; i1 < a.n1; i1 += G) {
-                const long long base = (long long)i1 * a.ld2;
-                for (int j = tid; j < a.n2; j += nthr) {
-                    x[base + j] += alpha * a.p[base + j];
-                    const double rv = a.r[base + j] - alpha * a.Ap[base + j];
+                    x[base + j] += alpha * pv;
+                    const double rv = a.r[base + j] - alpha * ap;
                     a.r[base + j] = rv;
                     part += rv * rv;
                 }
                 __syncthreads();
                 dst_row(a.r + base, i1, a.Rr, a.n2);
             }
+            stamp(4);
             const double rn2 = greduce(part);
-            stamp(5);
+            stamp(5);  // (the reduction of B3)
             ++it;
             if (sqrt(rn2) <= a.tol * sqrt(bn2) || it >= a.maxit) break;
             tau_cols_phase(lv);
