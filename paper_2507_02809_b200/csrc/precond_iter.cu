@@ -26,7 +26,6 @@ namespace fib {
 namespace {
 
 constexpr int CB = 4;   // columns per column-FFT CTA (graph path)
-constexpr int CBF = 2;  // columns per column group (fused kernel: 2 CTAs per SM, L2 / 2 groups)
 
 struct IterScalars {
     double bnorm2, rnorm2, rz, pap, alpha, beta;
@@ -523,7 +522,10 @@ __global__ void fft_cols_to_spec(ItArgs a, double* lamB) {
 struct FusedCtl {
     unsigned* bar;    // monotone grid-barrier counter (zeroed before the launch)
     double* parts;    // 2 x G block partials (ping-pong by reduction index)
-    unsigned long long* trace;  // optional [8] per-phase time sums of CTA 0 (FI_ITER_TRACE=1)
+    unsigned long long* trace;  // optional [10] per-phase time sums of CTA 0 (FI_ITER_TRACE=1)
+    int rpc;    // rows per CTA in the row passes (G * rpc >= n1)
+    int cbf;    // columns per CTA in the column passes (power of two, cbf * L1 <= 8 * 256)
+    int lgcbf;
 };
 __device__ __forceinline__ unsigned long long gtime_ns() {
     unsigned long long t;
@@ -545,6 +547,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
     const long long Np = a.Np;
+    const int rpc = ctl.rpc, cbf = ctl.cbf, lgc = ctl.lgcbf;
     unsigned target = 0;
     int rk = 0;
     unsigned long long tlast = 0;
@@ -597,52 +600,60 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         return bcast;
     };
     const double sc1 = sqrt(2.0 / (a.n1 + 1)) * -0.5, sc2 = sqrt(2.0 / (a.n2 + 1)) * -0.5;
-    const int hs = max(a.L2, CBF * a.L1);
+    const int hs = max(rpc * a.L2, cbf * a.L1);
     double2* u = sm;
-    double2* v = sm + hs;  // ping-pong halves: row phases use L2, column phases CBF x L1
-    double2* tws1 = sm + 2 * hs;  // twiddle half tables in shared memory
+    double2* v = sm + hs;           // ping-pong halves
+    double2* tws1 = sm + 2 * hs;    // twiddle half tables in shared memory
     double2* tws2 = tws1 + a.L1 / 2;
     for (int t = tid; t < a.L1 / 2; t += nthr) tws1[t] = a.tw1[t];
     for (int t = tid; t < a.L2 / 2; t += nthr) tws2[t] = a.tw2[t];
     __syncthreads();
+    // this CTA's rows for every row pass (G * rpc >= n1): r0 .. r0 + nr - 1, transformed together
+    const int r0 = cta * rpc, nr = max(0, min(rpc, a.n1 - r0));
 
     // rows n1..L1-1 of the embedded B input stay zero for the whole apply
     for (long long q = (long long)cta * nthr + tid; q < (long long)(a.L1 - a.n1) * a.L2; q += (long long)G * nthr)
         a.X[(long long)a.n1 * a.L2 + q] = make_double2(0.0, 0.0);
 
-    // DST-I of `src` rows (stride sstride, n2 values) into Rr rows; returns nothing
-    auto dst_row = [&](const double* src, int i1, double* out, long long ostride) {
-        for (int j = tid; j < a.L2; j += nthr) {
+    // DST-I along this CTA's rows of `src` (row stride sstride, n2 values) into the same rows of Rr
+    auto dst_rows = [&](const double* src, long long sstride) {
+        if (nr == 0) return;
+        for (int q = tid; q < nr * a.L2; q += nthr) {
+            const int i = q >> a.lg2, j = q & (a.L2 - 1);
+            const double* row = src + (long long)(r0 + i) * sstride;
             double val = 0.0;
-            if (j >= 1 && j <= a.n2) val = src[j - 1];
-            else if (j >= a.n2 + 2) val = -src[a.L2 - j - 1];
-            u[j] = make_double2(val, 0.0);
+            if (j >= 1 && j <= a.n2) val = row[j - 1];
+            else if (j >= a.n2 + 2) val = -row[a.L2 - j - 1];
+            u[q] = make_double2(val, 0.0);
         }
         __syncthreads();
-        const double2* U = fft4_smem(u, v, 1, a.L2, a.lg2, tws2, false, tid, nthr);
-        for (int k = tid; k < a.n2; k += nthr) out[(long long)i1 * ostride + k] = sc2 * U[k + 1].y;
+        const double2* U = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, false, tid, nthr);
+        for (int q = tid; q < nr * a.n2; q += nthr) {
+            const int i = q / a.n2, k = q - i * a.n2;
+            a.Rr[(long long)(r0 + i) * a.n2 + k] = sc2 * U[i * a.L2 + k + 1].y;
+        }
         __syncthreads();
     };
     // column pass of the tau solve: DST along columns, divide by the tau eigenvalues, DST back
     auto tau_cols_phase = [&](int lv) {
         const double c = level_c(a, lv), dmean = level_dmean(a, lv);
-        const int ngroups = (a.n2 + CBF - 1) / CBF;
+        const int ngroups = (a.n2 + cbf - 1) / cbf;
         for (int g = cta; g < ngroups; g += G) {
-            const int k0 = g * CBF, nc = min(CBF, a.n2 - k0);
-            for (int q = tid; q < CBF * a.L1; q += nthr) {
-                const int cc = q / a.L1, j = q - cc * a.L1;
+            const int k0 = g * cbf, nc = min(cbf, a.n2 - k0);
+            for (int q = tid; q < cbf * a.L1; q += nthr) {
+                const int cc = q & (cbf - 1), j = q >> lgc;  // column fastest: adjacent loads
                 double val = 0.0;
                 if (cc < nc) {
                     if (j >= 1 && j <= a.n1) val = a.Rr[(long long)(j - 1) * a.n2 + k0 + cc];
                     else if (j >= a.n1 + 2) val = -a.Rr[(long long)(a.L1 - j - 1) * a.n2 + k0 + cc];
                 }
-                u[q] = make_double2(val, 0.0);
+                u[cc * a.L1 + j] = make_double2(val, 0.0);
             }
             __syncthreads();
-            double2* U = fft4_smem(u, v, CBF, a.L1, a.lg1, tws1, false, tid, nthr);
+            double2* U = fft4_smem(u, v, cbf, a.L1, a.lg1, tws1, false, tid, nthr);
             double2* W = U == u ? v : u;
-            for (int q = tid; q < CBF * a.L1; q += nthr) {
-                const int cc = q / a.L1, j = q - cc * a.L1;
+            for (int q = tid; q < cbf * a.L1; q += nthr) {
+                const int cc = q & (cbf - 1), j = q >> lgc;
                 double val = 0.0;
                 if (cc < nc) {
                     int k = -1;
@@ -658,13 +669,13 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                         val = sgn * coef / lam;
                     }
                 }
-                W[q] = make_double2(val, 0.0);
+                W[cc * a.L1 + j] = make_double2(val, 0.0);
             }
             __syncthreads();
             double2* V = W == u ? v : u;
-            const double2* R = fft4_smem(W, V, CBF, a.L1, a.lg1, tws1, false, tid, nthr);
+            const double2* R = fft4_smem(W, V, cbf, a.L1, a.lg1, tws1, false, tid, nthr);
             for (int q = tid; q < nc * a.n1; q += nthr) {
-                const int cc = q / a.n1, k = q - cc * a.n1;
+                const int cc = q % nc, k = q / nc;
                 a.Rr[(long long)k * a.n2 + k0 + cc] = sc1 * R[cc * a.L1 + k + 1].y;
             }
             __syncthreads();
@@ -673,25 +684,26 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
     // final row pass of the tau solve: zz = DST rows of Rr, returns the partial r.zz; init: p = zz
     auto tau_out_phase = [&](bool init) -> double {
         double part = 0.0;
-        for (int i1 = cta; i1 < a.n1; i1 += G) {
-            const double* src = a.Rr + (long long)i1 * a.n2;
-            for (int j = tid; j < a.L2; j += nthr) {
-                double val = 0.0;
-                if (j >= 1 && j <= a.n2) val = src[j - 1];
-                else if (j >= a.n2 + 2) val = -src[a.L2 - j - 1];
-                u[j] = make_double2(val, 0.0);
-            }
-            __syncthreads();
-            const double2* U = fft4_smem(u, v, 1, a.L2, a.lg2, tws2, false, tid, nthr);
-            const long long base = (long long)i1 * a.ld2;
-            for (int k = tid; k < a.n2; k += nthr) {
-                const double zv = sc2 * U[k + 1].y;
-                a.zz[base + k] = zv;
-                if (init) a.p[base + k] = zv;
-                part += a.r[base + k] * zv;
-            }
-            __syncthreads();
+        if (nr == 0) return part;
+        for (int q = tid; q < nr * a.L2; q += nthr) {
+            const int i = q >> a.lg2, j = q & (a.L2 - 1);
+            const double* src = a.Rr + (long long)(r0 + i) * a.n2;
+            double val = 0.0;
+            if (j >= 1 && j <= a.n2) val = src[j - 1];
+            else if (j >= a.n2 + 2) val = -src[a.L2 - j - 1];
+            u[q] = make_double2(val, 0.0);
         }
+        __syncthreads();
+        const double2* U = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, false, tid, nthr);
+        for (int q = tid; q < nr * a.n2; q += nthr) {
+            const int i = q / a.n2, k = q - i * a.n2;
+            const long long o = (long long)(r0 + i) * a.ld2 + k;
+            const double zv = sc2 * U[i * a.L2 + k + 1].y;
+            a.zz[o] = zv;
+            if (init) a.p[o] = zv;
+            part += a.r[o] * zv;
+        }
+        __syncthreads();
         return part;
     };
 
@@ -729,11 +741,12 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         stamp(7);
         const double bn2 = greduce(part);
         stamp(0);
-        bool conv = bn2 == 0.0 || direct;
+        const bool conv = bn2 == 0.0 || direct;
         if (conv) continue;
         const double c = level_c(a, lv);
+        const long long lo_lv = (long long)min(lv, a.S - 1) * Np;  // D1, 1/D2 rows of the level
         // ---- initial tau solve: zz = tau^{-1} r, p = zz, rz = r.zz
-        for (int i1 = cta; i1 < a.n1; i1 += G) dst_row(a.r + (long long)i1 * a.ld2, i1, a.Rr, a.n2);
+        dst_rows(a.r, a.ld2);
         gsync();
         tau_cols_phase(lv);
         gsync();
@@ -743,26 +756,26 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         int it = 0;
         while (true) {
             // B1: p = zz + beta p (after the first step), row FFT of the embedded p; partial delta p.p
-            const long long lo_lv = (long long)min(lv, a.S - 1) * Np;  // D1, 1/D2 rows of the level
             double pdp = 0.0;
-            for (int i1 = cta; i1 < a.n1; i1 += G) {
-                const long long base = (long long)i1 * a.ld2;
-                for (int j = tid; j < a.L2; j += nthr) {
+            if (nr > 0) {
+                for (int q = tid; q < nr * a.L2; q += nthr) {
+                    const int i = q >> a.lg2, j = q & (a.L2 - 1);
                     double val = 0.0;
                     if (j < a.n2) {
-                        val = a.p[base + j];
+                        const long long o = (long long)(r0 + i) * a.ld2 + j;
+                        val = a.p[o];
                         if (it > 0) {
-                            val = a.zz[base + j] + beta * val;
-                            a.p[base + j] = val;
+                            val = a.zz[o] + beta * val;
+                            a.p[o] = val;
                         }
-                        if (lv < a.S) pdp += a.e0 * a.D1[lo_lv + base + j] * a.d2inv[lo_lv + base + j] * val * val;
+                        if (lv < a.S) pdp += a.e0 * a.D1[lo_lv + o] * a.d2inv[lo_lv + o] * val * val;
                     }
-                    u[j] = make_double2(val, 0.0);
+                    u[q] = make_double2(val, 0.0);
                 }
                 __syncthreads();
-                const double2* U = fft4_smem(u, v, 1, a.L2, a.lg2, tws2, false, tid, nthr);
-                double2* Xrow = a.X + (long long)i1 * a.L2;
-                for (int j = tid; j < a.L2; j += nthr) Xrow[j] = U[j];
+                const double2* U = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, false, tid, nthr);
+                double2* Xr = a.X + (long long)r0 * a.L2;
+                for (int q = tid; q < nr * a.L2; q += nthr) Xr[q] = U[q];
                 __syncthreads();
             }
             gsync();
@@ -771,26 +784,26 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
             // spectrum also gives p.Bp = sum lam |P^|^2 / (L1 L2), so p.Ap = c p.Bp + p.delta.p is
             // known here and the inverse row pass can update x and r at once.
             double pbp = 0.0;
-            for (int g = cta; g < a.L2 / CBF; g += G) {
-                const int k0 = g * CBF;
-                // element q = (row j, column cc) with the column fastest: CBF adjacent values per row
+            for (int g = cta; g < a.L2 / cbf; g += G) {
+                const int k0 = g * cbf;
+                // element q = (row j, column cc) with the column fastest: cbf adjacent values per row
                 double lamv[8];
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
                     const int q = tid + t * nthr;
-                    const int cc = q & (CBF - 1), j = q / CBF;
-                    if (q < CBF * a.L1) {
+                    const int cc = q & (cbf - 1), j = q >> lgc;
+                    if (q < cbf * a.L1) {
                         u[cc * a.L1 + j] = a.X[(long long)j * a.L2 + k0 + cc];
                         lamv[t] = a.lamB[(long long)j * a.L2 + k0 + cc];
                     }
                 }
                 __syncthreads();
-                double2* U = fft4_smem(u, v, CBF, a.L1, a.lg1, tws1, false, tid, nthr);
+                double2* U = fft4_smem(u, v, cbf, a.L1, a.lg1, tws1, false, tid, nthr);
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
                     const int q = tid + t * nthr;
-                    const int cc = q & (CBF - 1), j = q / CBF;
-                    if (q < CBF * a.L1) {
+                    const int cc = q & (cbf - 1), j = q >> lgc;
+                    if (q < cbf * a.L1) {
                         const double2 w = U[cc * a.L1 + j];
                         pbp += lamv[t] * (w.x * w.x + w.y * w.y);
                         U[cc * a.L1 + j] = make_double2(w.x * lamv[t], w.y * lamv[t]);
@@ -798,9 +811,9 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                 }
                 __syncthreads();
                 double2* W = U == u ? v : u;
-                const double2* Y = fft4_smem(U, W, CBF, a.L1, a.lg1, tws1, true, tid, nthr);
-                for (int q = tid; q < CBF * a.n1; q += nthr) {
-                    const int cc = q & (CBF - 1), j = q / CBF;
+                const double2* Y = fft4_smem(U, W, cbf, a.L1, a.lg1, tws1, true, tid, nthr);
+                for (int q = tid; q < cbf * a.n1; q += nthr) {
+                    const int cc = q & (cbf - 1), j = q >> lgc;
                     a.X[(long long)j * a.L2 + k0 + cc] = Y[cc * a.L1 + j];
                 }
                 __syncthreads();
@@ -810,27 +823,28 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
             // B3: inverse row FFT, Ap = c B p + delta o p; x += alpha p, r -= alpha Ap, ||r||^2, and
             // the DST rows of the new r (first pass of the next tau solve)
             part = 0.0;
-            for (int i1 = cta; i1 < a.n1; i1 += G) {
-                const double2* Xrow = a.X + (long long)i1 * a.L2;
-                for (int j = tid; j < a.L2; j += nthr) u[j] = Xrow[j];
+            if (nr > 0) {
+                const double2* Xr = a.X + (long long)r0 * a.L2;
+                for (int q = tid; q < nr * a.L2; q += nthr) u[q] = Xr[q];
                 __syncthreads();
-                const double2* Y = fft4_smem(u, v, 1, a.L2, a.lg2, tws2, true, tid, nthr);
-                const long long base = (long long)i1 * a.ld2;
-                for (int j = tid; j < a.n2; j += nthr) {
-                    const double pv = a.p[base + j];
-                    const double delta = lv < a.S ? a.e0 * a.D1[lo_lv + base + j] * a.d2inv[lo_lv + base + j] : 0.0;
-                    const double ap = c * (Y[j].x * a.inv_LL) + delta * pv;
-                    x[base + j] += alpha * pv;
-                    const double rv = a.r[base + j] - alpha * ap;
-                    a.r[base + j] = rv;
+                const double2* Y = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, true, tid, nthr);
+                for (int q = tid; q < nr * a.n2; q += nthr) {
+                    const int i = q / a.n2, j = q - i * a.n2;
+                    const long long o = (long long)(r0 + i) * a.ld2 + j;
+                    const double pv = a.p[o];
+                    const double delta = lv < a.S ? a.e0 * a.D1[lo_lv + o] * a.d2inv[lo_lv + o] : 0.0;
+                    const double ap = c * (Y[i * a.L2 + j].x * a.inv_LL) + delta * pv;
+                    x[o] += alpha * pv;
+                    const double rv = a.r[o] - alpha * ap;
+                    a.r[o] = rv;
                     part += rv * rv;
                 }
                 __syncthreads();
-                dst_row(a.r + base, i1, a.Rr, a.n2);
+                dst_rows(a.r, a.ld2);
             }
             stamp(4);
             const double rn2 = greduce(part);
-            stamp(5);  // (the reduction of B3)
+            stamp(5);
             ++it;
             if (sqrt(rn2) <= a.tol * sqrt(bn2) || it >= a.maxit) break;
             tau_cols_phase(lv);
@@ -1101,27 +1115,36 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
         a.y = y;
         a.levels = levels;
         a.skip = skip;
-        const size_t smem = (2 * (size_t)std::max(a.L2, CBF * a.L1) + a.L1 / 2 + a.L2 / 2) * sizeof(double2);
-        static size_t configured = 0;
-        if (smem > configured) {
-            FI_CUDA(cudaFuncSetAttribute(tau_pcg_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            configured = smem;
-        }
+        // grid: one row (pair of columns) per CTA when the GPU holds that many CTAs (two per SM),
+        // otherwise each CTA transforms rpc rows / cbf columns at once; every pass is one round
         if (P->it_fgrid == 0) {
+            const size_t smem_max = (2 * (size_t)std::max(4 * a.L2, 4 * a.L1) + a.L1 / 2 + a.L2 / 2) * sizeof(double2);
+            FI_CUDA(cudaFuncSetAttribute(tau_pcg_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::min<size_t>(smem_max, 227 * 1024)));
+            const size_t smem1 = (2 * (size_t)std::max(a.L2, 2 * a.L1) + a.L1 / 2 + a.L2 / 2) * sizeof(double2);
             int per_sm = 0;
-            FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tau_pcg_fused, 256, smem));
+            FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tau_pcg_fused, 256, smem1));
             if (per_sm < 1) throw Error(FI_E_CUDA, "tau_pcg_fused cannot be resident");
-            P->it_fgrid = ctx->sm_count * std::min(per_sm, 2);
+            P->it_fgrid = std::min(ctx->sm_count * std::min(per_sm, 2), std::max(a.n1, (a.L2 + 1) / 2));
             P->it_fparts.alloc((size_t)2 * P->it_fgrid);
             P->it_fbar.alloc(1);
         }
+        const int G = P->it_fgrid;
+        const int rpc = (a.n1 + G - 1) / G;
+        int cbf = 1;
+        while (cbf * G < a.L2 && cbf * 2 * a.L1 <= 8 * 256) cbf *= 2;
+        const size_t hs = (size_t)std::max(rpc * a.L2, cbf * a.L1);
+        const size_t smem = (2 * hs + a.L1 / 2 + a.L2 / 2) * sizeof(double2);
+        if (smem > 227 * 1024) throw Error(FI_E_RESOURCE, "tau_pcg_fused: shared memory");
         static const bool tracing = std::getenv("FI_ITER_TRACE") != nullptr;
         DevBuf<unsigned long long> trace;
         if (tracing) {
             trace.alloc(10);
             FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
         }
-        FusedCtl ctl{P->it_fbar.p, P->it_fparts.p, tracing ? trace.p : nullptr};
+        int lgc = 0;
+        while ((1 << lgc) < cbf) ++lgc;
+        FusedCtl ctl{P->it_fbar.p, P->it_fparts.p, tracing ? trace.p : nullptr, rpc, cbf, lgc};
         FI_CUDA(cudaMemsetAsync(P->it_fbar.p, 0, sizeof(unsigned), ctx->stream));
         void* args[] = {&a, &ctl};
         FI_CUDA(cudaLaunchCooperativeKernel((const void*)tau_pcg_fused, dim3(P->it_fgrid), dim3(256), args, smem,
