@@ -590,8 +590,16 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         }
         gsync();
         if (warp == 0) {
+            // all of a lane's partials in flight at once (G <= 320), then a fixed-order sum
+            double pv[10];
+#pragma unroll
+            for (int u2 = 0; u2 < 10; ++u2) {
+                const int k = lane + 32 * u2;
+                pv[u2] = k < G ? __ldcg(pp + k) : 0.0;
+            }
             double t = 0.0;
-            for (int k = lane; k < G; k += 32) t += __ldcg(pp + k);
+#pragma unroll
+            for (int u2 = 0; u2 < 10; ++u2) t += pv[u2];
             for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
             if (lane == 0) bcast = t;
         }
@@ -640,36 +648,50 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         const int ngroups = (a.n2 + cbf - 1) / cbf;
         for (int g = cta; g < ngroups; g += G) {
             const int k0 = g * cbf, nc = min(cbf, a.n2 - k0);
-            for (int q = tid; q < cbf * a.L1; q += nthr) {
+            // the tau eigenvalues of the element each thread divides later are loaded with the data
+            double ilam[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int q = tid + t * nthr;
                 const int cc = q & (cbf - 1), j = q >> lgc;  // column fastest: adjacent loads
-                double val = 0.0;
-                if (cc < nc) {
-                    if (j >= 1 && j <= a.n1) val = a.Rr[(long long)(j - 1) * a.n2 + k0 + cc];
-                    else if (j >= a.n1 + 2) val = -a.Rr[(long long)(a.L1 - j - 1) * a.n2 + k0 + cc];
+                ilam[t] = 0.0;
+                if (q < cbf * a.L1) {
+                    double val = 0.0;
+                    if (cc < nc) {
+                        int k = -1;
+                        if (j >= 1 && j <= a.n1) {
+                            val = a.Rr[(long long)(j - 1) * a.n2 + k0 + cc];
+                            k = j;
+                        } else if (j >= a.n1 + 2) {
+                            val = -a.Rr[(long long)(a.L1 - j - 1) * a.n2 + k0 + cc];
+                            k = a.L1 - j;
+                        }
+                        if (k > 0) ilam[t] = a.lamT[(long long)(k - 1) * a.n2 + k0 + cc];
+                    }
+                    u[cc * a.L1 + j] = make_double2(val, 0.0);
                 }
-                u[cc * a.L1 + j] = make_double2(val, 0.0);
             }
             __syncthreads();
             double2* U = fft4_smem(u, v, cbf, a.L1, a.lg1, tws1, false, tid, nthr);
             double2* W = U == u ? v : u;
-            for (int q = tid; q < cbf * a.L1; q += nthr) {
-                const int cc = q & (cbf - 1), j = q >> lgc;
-                double val = 0.0;
-                if (cc < nc) {
-                    int k = -1;
-                    double sgn = 1.0;
-                    if (j >= 1 && j <= a.n1) k = j;
-                    else if (j >= a.n1 + 2) {
-                        k = a.L1 - j;
-                        sgn = -1.0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int q = tid + t * nthr;
+                if (q < cbf * a.L1) {
+                    const int cc = q & (cbf - 1), j = q >> lgc;
+                    double val = 0.0;
+                    if (cc < nc) {
+                        int k = -1;
+                        double sgn = 1.0;
+                        if (j >= 1 && j <= a.n1) k = j;
+                        else if (j >= a.n1 + 2) {
+                            k = a.L1 - j;
+                            sgn = -1.0;
+                        }
+                        if (k > 0) val = sgn * (sc1 * U[cc * a.L1 + k].y) / (c * ilam[t] + dmean);
                     }
-                    if (k > 0) {
-                        const double coef = sc1 * U[cc * a.L1 + k].y;
-                        const double lam = c * a.lamT[(long long)(k - 1) * a.n2 + k0 + cc] + dmean;
-                        val = sgn * coef / lam;
-                    }
+                    W[cc * a.L1 + j] = make_double2(val, 0.0);
                 }
-                W[cc * a.L1 + j] = make_double2(val, 0.0);
             }
             __syncthreads();
             double2* V = W == u ? v : u;
