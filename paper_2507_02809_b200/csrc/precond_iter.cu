@@ -533,6 +533,11 @@ __device__ __forceinline__ unsigned long long gtime_ns() {
     return t;
 }
 
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -566,10 +571,12 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
             __threadfence();
             atomicAdd(ctl.bar, 1u);
             unsigned n = 0;
-            while (ld_acquire_u32(ctl.bar) < target) {
+            // relaxed polls (an acquire load invalidates the SM's L1 on every iteration), one acquire
+            while (ld_relaxed_u32(ctl.bar) < target) {
                 __nanosleep(32);
                 if (++n == (1u << 26)) __trap();
             }
+            (void)ld_acquire_u32(ctl.bar);
             if (ctl.trace && cta == 0) {
                 ctl.trace[8] += gtime_ns() - t0;
                 ctl.trace[9] += 1;
