@@ -32,22 +32,11 @@ struct fi_precond {
     std::vector<double> it_dmean;
     std::vector<int> it_direct;
     fib::DevBuf<double2> it_tw1, it_tw2, it_X;
-    fib::DevBuf<double> it_lamT, it_lamB, it_Rr, it_vec, it_partials, it_state, it_dmean_d;
-    fib::DevBuf<int> it_direct_d, it_level;
-    fib::DevBuf<unsigned> it_ticket;
-    fib::DevBuf<unsigned long long> it_kcount;  // kernels executed inside the CG graphs
+    fib::DevBuf<double> it_lamT, it_lamB, it_Rr, it_vec, it_dmean_d;
+    fib::DevBuf<int> it_direct_d;
     int it_fgrid = 0;                            // fused kernel: cooperative grid size
     fib::DevBuf<double> it_fparts;               // fused kernel: 2 x grid block partials
     fib::DevBuf<unsigned> it_fbar;               // fused kernel: grid-barrier counter
-    struct GraphEntry {
-        const double* z;
-        double* y;
-        int levels;
-        const int* skip;
-        cudaGraph_t graph;
-        cudaGraphExec_t exec;
-    };
-    std::vector<GraphEntry> it_graphs;
     ~fi_precond();
 };
 

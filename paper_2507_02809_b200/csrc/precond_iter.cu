@@ -1,4 +1,4 @@
-// K2' — the substituted per-block solve for 2D blocks too large to invert densely (configs 2-4).
+// K5 — the substituted per-block solve for 2D blocks too large to invert densely (configs 2-4).
 //
 // The reference factorises every diagonal block densely (krylov.cpp:24-46) and refuses blocks
 // above its cap of 4096 (ResourceLimitError).  For the 2D BASELINE configurations (N = 127^2,
@@ -8,12 +8,11 @@
 //   tau^{-1} = S diag(1/(c g(theta) + mean(delta))) S,   S = orthonormal 2D DST-I
 // B x is a 2D circulant-embedded convolution (forward/inverse 2D FFT of size L1 x L2 with
 // L_i = 2(n_i + 1) a power of two); the DST-I is an odd-extended FFT of the same size.  The FFTs are
-// hand-written radix-2 Stockham transforms in shared memory (row kernels: one CTA per row; column
-// kernels: CB columns per CTA), each fused with the neighbouring elementwise work and reductions.
+// hand-written Stockham transforms in shared memory.
 //
-// Control flow never returns to the host inside an apply: the whole forward substitution is ONE
-// CUDA graph — a conditional WHILE node over levels whose body holds a conditional WHILE node over
-// CG steps; the kernels set the loop conditions on the device (cudaGraphSetConditional).
+// Control flow never returns to the host inside an apply: the whole forward substitution (level
+// loop, CG loop, scalars) is ONE cooperative kernel, tau_pcg_fused, with grid barriers between the
+// row and column passes of each CG step.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -25,12 +24,7 @@
 namespace fib {
 namespace {
 
-constexpr int CB = 4;   // columns per column-FFT CTA (graph path)
-
-struct IterScalars {
-    double bnorm2, rnorm2, rz, pap, alpha, beta;
-    int conv, it;
-};
+constexpr int CB = 4;   // columns per CTA of the setup column FFT (spectrum of B)
 
 struct ItArgs {
     int n1, n2, ld2, L1, L2, lg1, lg2, S, levels, maxit;
@@ -42,7 +36,6 @@ struct ItArgs {
     const double* lamT;  // n1 x n2 tau eigenvalues g(theta)
     const double* dmean; // per level mean(delta)
     const int* direct;   // per level: D2 == 0 (G = e0 D1)
-    int* level;          // current level (device)
     const double* z_in;  // right-hand side of P (padded layout)
     double* y;           // output of P (padded layout); x of the level is y's slice
     const double* D1;
@@ -54,18 +47,10 @@ struct ItArgs {
     double* Ap;
     double2* X;   // L1 x L2 complex work
     double* Rr;   // n1 x n2 real DST work
-    double* partials;
-    unsigned* ticket;
-    IterScalars* st;
     const int* skip;
-    unsigned long long* kcount;
-    cudaGraphConditionalHandle h_level, h_cg;
 };
 
 __device__ __forceinline__ bool skipped(const ItArgs& a) { return a.skip && *a.skip; }
-__device__ __forceinline__ void count_kernel(const ItArgs& a) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.kcount, 1ull);
-}
 __device__ __forceinline__ double level_c(const ItArgs& a, int lv) { return lv < a.S ? a.cs : a.cr; }
 __device__ __forceinline__ double level_dmean(const ItArgs& a, int lv) { return lv < a.S ? a.dmean[lv] : 0.0; }
 
@@ -166,312 +151,6 @@ __device__ double2* fft4_smem(double2* src, double2* dst, int cnt, int L, int lg
         dst = t;
     }
     return src;
-}
-
-// ------------------------------------------------------------------ deterministic grid reduction
-// Block-reduce v, write the block partial; thread 0 of the last block to finish returns true with
-// the grid total summed in fixed block order.
-__device__ bool grid_sum(double v, double* partials, unsigned* ticket, double& total) {
-    __shared__ double red[32];
-    __shared__ bool last;
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double b = 0.0;
-        for (int w = 0; w < nw; ++w) b += red[w];
-        partials[blockIdx.x] = b;
-        __threadfence();
-        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last || threadIdx.x != 0) return false;
-    __threadfence();
-    double t = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(partials + b);
-    total = t;
-    *ticket = 0;
-    return true;
-}
-
-// ------------------------------------------------------------------ level control
-__global__ void it_level_reset(ItArgs a) { *a.level = 0; }
-
-__global__ void it_level_advance(ItArgs a) {
-    const int lv = *a.level + 1;
-    *a.level = lv;
-    cudaGraphSetConditional(a.h_level, (lv < a.levels && !skipped(a)) ? 1u : 0u);
-}
-
-// rhs of the level (forward substitution, krylov.cpp:55-68) and the CG start b = rhs / D2, x = 0;
-// a level with D2 == 0 (G = e0 D1) is solved here directly.
-__global__ void it_level_setup(ItArgs a) {
-    if (skipped(a)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.h_cg, 0u);
-        return;
-    }
-    count_kernel(a);
-    const long long Np = a.Np;
-    const int L = *a.level;
-    const bool direct = L < a.S && a.direct[L];
-    double* x = a.y + (long long)L * Np;
-    double part = 0.0;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < Np; i += (long long)gridDim.x * blockDim.x) {
-        const int i2 = (int)(i % a.ld2);
-        double b = 0.0, xv = 0.0;
-        if (i2 < a.n2) {
-            if (L < a.S) {
-                double hist = 0.0;
-                for (int m = 0; m < L; ++m) hist += a.e[L - m] * a.y[(long long)m * Np + i];
-                const long long o = (long long)L * Np + i;
-                const double rhs = a.z_in[o] - a.D1[o] * hist;
-                if (direct) xv = rhs / (a.e0 * a.D1[o]);
-                else b = rhs * a.d2inv[o];
-            } else {
-                const double rhs = a.z_in[(long long)a.S * Np + i] - a.y[(long long)(a.S - 1) * Np + i];
-                b = rhs * a.d2inv[(long long)(a.S - 1) * Np + i];
-            }
-        }
-        a.r[i] = b;
-        x[i] = xv;
-        part += b * b;
-    }
-    double tot;
-    if (grid_sum(part, a.partials, a.ticket, tot)) {
-        IterScalars* st = a.st;
-        st->bnorm2 = tot;
-        st->it = 0;
-        st->conv = (tot == 0.0 || direct) ? 1 : 0;
-        st->rz = 0.0;
-        st->beta = 0.0;
-        cudaGraphSetConditional(a.h_cg, st->conv ? 0u : 1u);
-    }
-}
-
-// tau solve, row pass: Rr[i1][:] = DST-I of in[i1][:]
-__global__ void tau_rows(ItArgs a, int from_r) {
-    if (skipped(a) || a.st->conv) return;
-    count_kernel(a);
-    extern __shared__ double2 sm[];
-    double2* u = sm;
-    double2* v = sm + a.L2;
-    const int i1 = blockIdx.x;
-    const double* row = (from_r ? a.r : a.zz) + (long long)i1 * a.ld2;
-    for (int j = threadIdx.x; j < a.L2; j += blockDim.x) {
-        double val = 0.0;
-        if (j >= 1 && j <= a.n2) val = row[j - 1];
-        else if (j >= a.n2 + 2) val = -row[a.L2 - j - 1];
-        u[j] = make_double2(val, 0.0);
-    }
-    __syncthreads();
-    const double2* U = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, false, threadIdx.x, blockDim.x);
-    const double sc = sqrt(2.0 / (a.n2 + 1)) * -0.5;
-    for (int k = threadIdx.x; k < a.n2; k += blockDim.x) a.Rr[(long long)i1 * a.n2 + k] = sc * U[k + 1].y;
-}
-
-// tau solve, column pass: DST-I along columns, divide by the tau eigenvalues, DST-I back
-__global__ void tau_cols(ItArgs a) {
-    if (skipped(a) || a.st->conv) return;
-    count_kernel(a);
-    extern __shared__ double2 sm[];
-    double2* u = sm;
-    double2* v = sm + CB * a.L1;
-    const int lv = *a.level;
-    const double c = level_c(a, lv), dmean = level_dmean(a, lv);
-    const int k0 = blockIdx.x * CB;
-    const int nc = min(CB, a.n2 - k0);
-    for (int q = threadIdx.x; q < CB * a.L1; q += blockDim.x) {
-        const int cc = q / a.L1, j = q - cc * a.L1;
-        double val = 0.0;
-        if (cc < nc) {
-            if (j >= 1 && j <= a.n1) val = a.Rr[(long long)(j - 1) * a.n2 + k0 + cc];
-            else if (j >= a.n1 + 2) val = -a.Rr[(long long)(a.L1 - j - 1) * a.n2 + k0 + cc];
-        }
-        u[q] = make_double2(val, 0.0);
-    }
-    __syncthreads();
-    double2* U = fft_smem(u, v, CB, a.L1, a.lg1, a.tw1, false, threadIdx.x, blockDim.x);
-    double2* W = U == u ? v : u;
-    const double sc = sqrt(2.0 / (a.n1 + 1)) * -0.5;
-    for (int q = threadIdx.x; q < CB * a.L1; q += blockDim.x) {
-        const int cc = q / a.L1, j = q - cc * a.L1;
-        double val = 0.0;
-        if (cc < nc) {
-            int k = -1;
-            double sgn = 1.0;
-            if (j >= 1 && j <= a.n1) k = j;
-            else if (j >= a.n1 + 2) {
-                k = a.L1 - j;
-                sgn = -1.0;
-            }
-            if (k > 0) {
-                const double coef = sc * U[cc * a.L1 + k].y;
-                const double lam = c * a.lamT[(long long)(k - 1) * a.n2 + k0 + cc] + dmean;
-                val = sgn * coef / lam;
-            }
-        }
-        W[q] = make_double2(val, 0.0);
-    }
-    __syncthreads();
-    double2* V = W == u ? v : u;
-    U = fft_smem(W, V, CB, a.L1, a.lg1, a.tw1, false, threadIdx.x, blockDim.x);
-    for (int q = threadIdx.x; q < nc * a.n1; q += blockDim.x) {
-        const int cc = q / a.n1, k = q - cc * a.n1;
-        a.Rr[(long long)k * a.n2 + k0 + cc] = sc * U[cc * a.L1 + k + 1].y;
-    }
-}
-
-// tau solve, final row pass: z = DST-I rows of Rr; r.z -> beta, rz; init: p = z
-__global__ void tau_rows_out(ItArgs a, int init) {
-    if (skipped(a) || a.st->conv) return;
-    count_kernel(a);
-    extern __shared__ double2 sm[];
-    double2* u = sm;
-    double2* v = sm + a.L2;
-    const int i1 = blockIdx.x;
-    const double* src = a.Rr + (long long)i1 * a.n2;
-    for (int j = threadIdx.x; j < a.L2; j += blockDim.x) {
-        double val = 0.0;
-        if (j >= 1 && j <= a.n2) val = src[j - 1];
-        else if (j >= a.n2 + 2) val = -src[a.L2 - j - 1];
-        u[j] = make_double2(val, 0.0);
-    }
-    __syncthreads();
-    const double2* U = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, false, threadIdx.x, blockDim.x);
-    const double sc = sqrt(2.0 / (a.n2 + 1)) * -0.5;
-    double part = 0.0;
-    const long long base = (long long)i1 * a.ld2;
-    for (int k = threadIdx.x; k < a.n2; k += blockDim.x) {
-        const double zv = sc * U[k + 1].y;
-        a.zz[base + k] = zv;
-        if (init) a.p[base + k] = zv;
-        part += a.r[base + k] * zv;
-    }
-    double tot;
-    if (grid_sum(part, a.partials, a.ticket, tot)) {
-        IterScalars* st = a.st;
-        st->beta = init ? 0.0 : tot / st->rz;
-        st->rz = tot;
-    }
-}
-
-// B p, row pass: p = z + beta p (after the first step), embed the row, forward FFT
-__global__ void bop_rows_fwd(ItArgs a) {
-    if (skipped(a) || a.st->conv) return;
-    count_kernel(a);
-    extern __shared__ double2 sm[];
-    double2* u = sm;
-    double2* v = sm + a.L2;
-    const int i1 = blockIdx.x;
-    double2* Xrow = a.X + (long long)i1 * a.L2;
-    if (i1 >= a.n1) {
-        for (int j = threadIdx.x; j < a.L2; j += blockDim.x) Xrow[j] = make_double2(0.0, 0.0);
-        return;
-    }
-    const long long base = (long long)i1 * a.ld2;
-    const bool upd = a.st->it > 0;
-    const double beta = a.st->beta;
-    for (int j = threadIdx.x; j < a.L2; j += blockDim.x) {
-        double val = 0.0;
-        if (j < a.n2) {
-            val = a.p[base + j];
-            if (upd) {
-                val = a.zz[base + j] + beta * val;
-                a.p[base + j] = val;
-            }
-        }
-        u[j] = make_double2(val, 0.0);
-    }
-    __syncthreads();
-    const double2* U = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, false, threadIdx.x, blockDim.x);
-    for (int j = threadIdx.x; j < a.L2; j += blockDim.x) Xrow[j] = U[j];
-}
-
-// B p, column pass: forward FFT along columns, times the circulant spectrum, inverse FFT
-__global__ void bop_cols(ItArgs a) {
-    if (skipped(a) || a.st->conv) return;
-    count_kernel(a);
-    extern __shared__ double2 sm[];
-    double2* u = sm;
-    double2* v = sm + CB * a.L1;
-    const int k0 = blockIdx.x * CB;
-    for (int q = threadIdx.x; q < CB * a.L1; q += blockDim.x) {
-        const int c = q / a.L1, j = q - c * a.L1;
-        u[q] = a.X[(long long)j * a.L2 + k0 + c];
-    }
-    __syncthreads();
-    double2* U = fft_smem(u, v, CB, a.L1, a.lg1, a.tw1, false, threadIdx.x, blockDim.x);
-    for (int q = threadIdx.x; q < CB * a.L1; q += blockDim.x) {
-        const int c = q / a.L1, j = q - c * a.L1;
-        const double lam = a.lamB[(long long)j * a.L2 + k0 + c];
-        U[q] = make_double2(U[q].x * lam, U[q].y * lam);
-    }
-    __syncthreads();
-    double2* W = U == u ? v : u;
-    const double2* Y = fft_smem(U, W, CB, a.L1, a.lg1, a.tw1, true, threadIdx.x, blockDim.x);
-    for (int q = threadIdx.x; q < CB * a.L1; q += blockDim.x) {
-        const int c = q / a.L1, j = q - c * a.L1;
-        if (j < a.n1) a.X[(long long)j * a.L2 + k0 + c] = Y[q];
-    }
-}
-
-// B p, final row pass: inverse FFT along rows, Ap = c B p + delta o p, p.Ap -> alpha
-__global__ void bop_rows_inv(ItArgs a) {
-    if (skipped(a) || a.st->conv) return;
-    count_kernel(a);
-    extern __shared__ double2 sm[];
-    double2* u = sm;
-    double2* v = sm + a.L2;
-    const int i1 = blockIdx.x;
-    const int lv = *a.level;
-    const double c = level_c(a, lv);
-    const double2* Xrow = a.X + (long long)i1 * a.L2;
-    for (int j = threadIdx.x; j < a.L2; j += blockDim.x) u[j] = Xrow[j];
-    __syncthreads();
-    const double2* Y = fft_smem(u, v, 1, a.L2, a.lg2, a.tw2, true, threadIdx.x, blockDim.x);
-    const long long base = (long long)i1 * a.ld2;
-    const long long lo = (long long)min(lv, a.S - 1) * a.Np + base;  // D1, 1/D2 row of the level
-    double part = 0.0;
-    for (int j = threadIdx.x; j < a.n2; j += blockDim.x) {
-        const double pv = a.p[base + j];
-        const double delta = lv < a.S ? a.e0 * a.D1[lo + j] * a.d2inv[lo + j] : 0.0;
-        const double ap = c * (Y[j].x * a.inv_LL) + delta * pv;
-        a.Ap[base + j] = ap;
-        part += pv * ap;
-    }
-    double tot;
-    if (grid_sum(part, a.partials, a.ticket, tot)) {
-        a.st->pap = tot;
-        a.st->alpha = a.st->rz / tot;
-    }
-}
-
-// x += alpha p, r -= alpha Ap, stop when ||r|| <= tol ||b|| (or maxit steps)
-__global__ void it_update(ItArgs a) {
-    if (skipped(a) || a.st->conv) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.h_cg, 0u);
-        return;
-    }
-    count_kernel(a);
-    const double alpha = a.st->alpha;
-    double* x = a.y + (long long)(*a.level) * a.Np;
-    double part = 0.0;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.Np;
-         i += (long long)gridDim.x * blockDim.x) {
-        x[i] += alpha * a.p[i];
-        const double rv = a.r[i] - alpha * a.Ap[i];
-        a.r[i] = rv;
-        part += rv * rv;
-    }
-    double tot;
-    if (grid_sum(part, a.partials, a.ticket, tot)) {
-        IterScalars* st = a.st;
-        st->rnorm2 = tot;
-        st->it += 1;
-        if (sqrt(tot) <= a.tol * sqrt(st->bnorm2) || st->it >= a.maxit) st->conv = 1;
-        cudaGraphSetConditional(a.h_cg, st->conv ? 0u : 1u);
-    }
 }
 
 // circulant spectrum of the embedded B: lamB = Re FFT2(c), c[k1][k2] = a[l1][l2]
@@ -898,8 +577,6 @@ void allow_column_smem() {
     static bool done = false;
     if (done) return;
     const int bytes = 2 * CB * 1024 * (int)sizeof(double2);
-    FI_CUDA(cudaFuncSetAttribute(tau_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    FI_CUDA(cudaFuncSetAttribute(bop_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     FI_CUDA(cudaFuncSetAttribute(fft_cols_to_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     done = true;
 }
@@ -930,7 +607,6 @@ ItArgs make_args(fi_precond* P) {
     a.lamT = P->it_lamT.p;
     a.dmean = P->it_dmean_d.p;
     a.direct = P->it_direct_d.p;
-    a.level = P->it_level.p;
     a.D1 = sys->D1.p;
     a.d2inv = P->d2inv.p;
     a.e = sys->e.p;
@@ -940,87 +616,7 @@ ItArgs make_args(fi_precond* P) {
     a.Ap = P->it_vec.p + 3 * Np;
     a.X = P->it_X.p;
     a.Rr = P->it_Rr.p;
-    a.partials = P->it_partials.p;
-    a.ticket = P->it_ticket.p;
-    a.st = reinterpret_cast<IterScalars*>(P->it_state.p);
-    a.kcount = P->it_kcount.p;
     return a;
-}
-
-void check_graph(cudaError_t e, const char* what) {
-    if (e != cudaSuccess)
-        throw Error(FI_E_CUDA, std::string("precond graph: ") + what + ": " + cudaGetErrorString(e));
-}
-
-// Build the forward-substitution graph: reset; while(level) { setup; tau; while(cg) { step }; advance }
-cudaGraphExec_t build_graph(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip,
-                            cudaGraph_t& graph_out) {
-    ItArgs a = make_args(P);
-    a.z_in = z;
-    a.y = y;
-    a.levels = levels;
-    a.skip = skip;
-    const int rowthr = std::min(a.L2 / 2, 256);
-    const size_t rowsm = 2 * (size_t)a.L2 * sizeof(double2);
-    const size_t colsm = 2 * (size_t)CB * a.L1 * sizeof(double2);
-    const int vgrid = ctx->sm_count * 2;
-    cudaStream_t cs;
-    check_graph(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream");
-    cudaGraph_t g;
-    check_graph(cudaGraphCreate(&g, 0), "create");
-    check_graph(cudaGraphConditionalHandleCreate(&a.h_level, g, 1, cudaGraphCondAssignDefault), "level handle");
-    // top: reset node, then the level loop
-    check_graph(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed), "cap top");
-    it_level_reset<<<1, 1, 0, cs>>>(a);
-    cudaStreamCaptureStatus cst;
-    const cudaGraphNode_t* deps = nullptr;
-    size_t ndeps = 0;
-    cudaGraph_t capg;
-    check_graph(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &capg, &deps, &ndeps), "capture info");
-    cudaGraphNodeParams lp = {};
-    lp.type = cudaGraphNodeTypeConditional;
-    lp.conditional.handle = a.h_level;
-    lp.conditional.type = cudaGraphCondTypeWhile;
-    lp.conditional.size = 1;
-    cudaGraphNode_t lnode;
-    check_graph(cudaGraphAddNode(&lnode, capg, deps, ndeps, &lp), "level node");
-    check_graph(cudaStreamUpdateCaptureDependencies(cs, &lnode, 1, cudaStreamSetCaptureDependencies), "deps");
-    check_graph(cudaStreamEndCapture(cs, &g), "end top");
-    cudaGraph_t lbody = lp.conditional.phGraph_out[0];
-    check_graph(cudaGraphConditionalHandleCreate(&a.h_cg, lbody, 1, cudaGraphCondAssignDefault), "cg handle");
-    // level body: setup, initial tau solve, the CG loop, advance
-    check_graph(cudaStreamBeginCaptureToGraph(cs, lbody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed), "cap lv");
-    it_level_setup<<<vgrid, 256, 0, cs>>>(a);
-    tau_rows<<<a.n1, rowthr, rowsm, cs>>>(a, 1);
-    tau_cols<<<(a.n2 + CB - 1) / CB, 256, colsm, cs>>>(a);
-    tau_rows_out<<<a.n1, rowthr, rowsm, cs>>>(a, 1);
-    check_graph(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &capg, &deps, &ndeps), "capture info 2");
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = a.h_cg;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t cnode;
-    check_graph(cudaGraphAddNode(&cnode, capg, deps, ndeps, &cp), "cg node");
-    check_graph(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies), "deps 2");
-    it_level_advance<<<1, 1, 0, cs>>>(a);
-    check_graph(cudaStreamEndCapture(cs, &lbody), "end lv");
-    // CG step body
-    cudaGraph_t cbody = cp.conditional.phGraph_out[0];
-    check_graph(cudaStreamBeginCaptureToGraph(cs, cbody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed), "cap cg");
-    bop_rows_fwd<<<a.L1, rowthr, rowsm, cs>>>(a);
-    bop_cols<<<a.L2 / CB, 256, colsm, cs>>>(a);
-    bop_rows_inv<<<a.n1, rowthr, rowsm, cs>>>(a);
-    it_update<<<vgrid, 256, 0, cs>>>(a);
-    tau_rows<<<a.n1, rowthr, rowsm, cs>>>(a, 1);
-    tau_cols<<<(a.n2 + CB - 1) / CB, 256, colsm, cs>>>(a);
-    tau_rows_out<<<a.n1, rowthr, rowsm, cs>>>(a, 0);
-    check_graph(cudaStreamEndCapture(cs, &cbody), "end cg");
-    cudaGraphExec_t exec;
-    check_graph(cudaGraphInstantiate(&exec, g, 0), "instantiate");
-    check_graph(cudaStreamDestroy(cs), "stream destroy");
-    graph_out = g;
-    return exec;
 }
 
 }  // namespace
@@ -1088,9 +684,6 @@ void precond_build_iterative(fi_precond* P, double tol, int maxit) {
     FI_CUDA(cudaMemcpy(P->it_dmean_d.p, dmean.data(), dmean.size() * sizeof(double), cudaMemcpyHostToDevice));
     P->it_direct_d.alloc(direct.size());
     FI_CUDA(cudaMemcpy(P->it_direct_d.p, direct.data(), direct.size() * sizeof(int), cudaMemcpyHostToDevice));
-    P->it_level.alloc(1);
-    P->it_kcount.alloc(1);
-    FI_CUDA(cudaMemset(P->it_kcount.p, 0, sizeof(unsigned long long)));
     // twiddles exp(-2 pi i k / L)
     std::vector<double2> t1((size_t)L1 / 2), t2((size_t)L2 / 2);
     for (int k = 0; k < L1 / 2; ++k)
@@ -1116,10 +709,6 @@ void precond_build_iterative(fi_precond* P, double tol, int maxit) {
     P->it_lamB.alloc((size_t)L1 * L2);
     P->it_vec.alloc((size_t)4 * Np);  // r, z, p, Ap
     FI_CUDA(cudaMemset(P->it_vec.p, 0, P->it_vec.bytes()));
-    P->it_partials.alloc((size_t)std::max(L1, 2 * ctx->sm_count) + 64);
-    P->it_ticket.alloc(1);
-    FI_CUDA(cudaMemset(P->it_ticket.p, 0, sizeof(unsigned)));
-    P->it_state.alloc(sizeof(IterScalars) / sizeof(double) + 2);
     // circulant spectrum of B with the same FFT kernels
     allow_column_smem();
     ItArgs a = make_args(P);
@@ -1133,11 +722,7 @@ void precond_build_iterative(fi_precond* P, double tol, int maxit) {
 }
 
 void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip) {
-    static const bool use_graph = [] {
-        const char* v = std::getenv("FI_ITER_GRAPH");
-        return v && std::atoi(v) != 0;
-    }();
-    if (!use_graph) {
+    {
         // one cooperative kernel for the whole substitution (tau_pcg_fused)
         ItArgs a = make_args(P);
         a.z_in = z;
@@ -1189,25 +774,9 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
                          h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6, h[4] * 1e-6, h[5] * 1e-6, h[6] * 1e-6,
                          h[7] * 1e-6, h[8] * 1e-6, h[9]);
         }
-        return;
     }
-    cudaGraphExec_t exec = nullptr;
-    for (auto& gE : P->it_graphs)
-        if (gE.z == z && gE.y == y && gE.levels == levels && gE.skip == skip) exec = gE.exec;
-    if (!exec) {
-        cudaGraph_t g;
-        exec = build_graph(ctx, P, z, y, levels, skip, g);
-        P->it_graphs.push_back({z, y, levels, skip, g, exec});
-    }
-    FI_CUDA(cudaGraphLaunch(exec, ctx->stream));
-    ctx->launches += 1;  // one graph launch; kernels executed inside are counted in it_kcount
 }
 
 }  // namespace fib
 
-fi_precond::~fi_precond() {
-    for (auto& g : it_graphs) {
-        cudaGraphExecDestroy(g.exec);
-        cudaGraphDestroy(g.graph);
-    }
-}
+fi_precond::~fi_precond() = default;
