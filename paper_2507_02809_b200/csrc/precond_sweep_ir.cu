@@ -1,20 +1,21 @@
-// K2 (refined) — forward block substitution AND its iterative refinement in ONE persistent sweep.
+// K2 — P^{-1} z: forward block substitution AND its iterative refinement in ONE persistent kernel.
 //
 // P^{-1} z with LU-grade accuracy needs one refinement step on top of the explicit-inverse sweep
 // (DESIGN §6):  y1 = P~^{-1} z (FP64 inverses),  r = z - P y1 (exact FP64 residual),
 // d = P~^{-1} r (FP32 inverses),  y = y1 + d.  Run as separate kernels that is two sequential
-// S-level dependency chains plus an operator launch.  Here the three are interleaved with a lag in
-// one cooperative kernel that pays for ONE chain:
-//   step t:  tiles of H64_t x1_t          (sweep 1, level t)
-//            tiles of B y1_{t-1}          (residual of level t-1: B generated from its symbol)
-//            tiles of H32_{t-2} x2_{t-2}  (sweep 2, level t-2)
-//   owner at the start of step t reduces the three partial products of step t-1 and publishes
-//   x1_t, y1_{t-1}, x2_{t-2} behind one per-row-block release counter.
-// The producer warp streams the FP64 and FP32 tiles of each step with cp.async.bulk (TMA) into the
-// mbarrier ring; B tiles are generated in registers (no HBM traffic); spare warps accumulate the
-// three L1 history sums of the next step from the CTA's own rows.  Synchronisation is the same
-// dataflow as sweep_kernel (precond_apply.cu): warp-uniform acquire polls on per-row-block
-// counters, one release fence per warp and step, fixed-order (bit-reproducible) reductions.
+// S-level dependency chains plus an operator launch.  Here they are interleaved with a lag:
+//   step t:  tiles of H64_t x1_t          (chain 1: sweep 1, level t)
+//            tiles of B y1_{t-1}          (chain 2: residual of level t-1, B generated from its symbol)
+//            tiles of H32_{t-2} x2_{t-2}  (chain 2: sweep 2, level t-2)
+// and the chains are decoupled: each has its own owner phase and its own per-row-block release
+// counter, run by dedicated warps, so the ring warps never sit in an owner phase — while chain 1's
+// owners publish x1_{t+1}, the ring streams the FP32 tiles of step t, and while chain 2's owners
+// publish x2_{t-1}, it streams the FP64 tiles of step t+1.
+// Warps (12, 168 registers): a producer (cp.async.bulk / TMA into an mbarrier ring of half-tile
+// slots, evict-first in L2), 6 ring warps (FP64 and FP32 tile products), 3 owner warps (both
+// chains' reductions, the x vectors, the L1 history sums) and 2 B-tile warps.  Dataflow: warp-uniform
+// relaxed polls on per-row-block counters, one release fence per warp and phase, fixed-order
+// (bit-reproducible) reductions, bounded spins.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -28,16 +29,13 @@ namespace {
 constexpr int TB = 64;
 constexpr int TILE = TB * TB;
 constexpr int NW = 11;                  // worker warps; + 1 producer = 12 warps (3 per SMSP)
-constexpr int NWT = NW * 32;
-constexpr int THREADS = NWT + 32;
+constexpr int THREADS = NW * 32 + 32;
 constexpr int NST = 6;                  // ring warps (tile item k -> warp k % NST)
 constexpr int NHS = 2 * NST;            // ring half-slots of 16 KiB: a tile streams as two row halves
 constexpr int HSLOT = TILE / 2;         // doubles per half-slot
-constexpr int NB_W = NW - NST;          // warps for the generated B tiles and the history sums
 constexpr int RCAP = 32;   // owned rows per CTA: one per lane
 constexpr int CSTR = kCounterStride;
 constexpr int TCAP = 64;   // tiles per CTA and level (coordinate table)
-constexpr int KPW = 7;     // partials per warp and kind in the owner reduction: nb <= KPW * NW
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -77,11 +75,6 @@ __device__ __forceinline__ void tma_bulk_g2s_stream(void* dst, const void* src, 
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
-__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void worker_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(NWT) : "memory"); }
-__device__ __forceinline__ void bwarp_bar() { asm volatile("bar.sync 2, %0;\n" ::"n"(NB_W * 32) : "memory"); }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -147,7 +140,6 @@ struct IrArgs {
     unsigned* pdone;   // [3][nb] (stride CSTR)
     const int* skip;
     int evict_first;
-    int pf_items;  // L2 prefetch distance in ring items (0 = off)
     unsigned long long* trace;  // optional [G][nsteps+1][8] phase timestamps (FI_SWEEP_TRACE=1)
 };
 
@@ -228,570 +220,12 @@ __device__ __forceinline__ void tile_product_f32(Begin begin, RowFn hrow, End en
     if (!diag) reinterpret_cast<double2*>(pcol)[lane] = make_double2((double)c0, (double)c1);
 }
 
-__global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
-    if (a.skip && *a.skip) return;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* ring = reinterpret_cast<double*>(smem_raw);            // NHS x HSLOT
-    double* red = ring + NHS * HSLOT;                               // 3 x NW x 32
-    double* h1p = red + 3 * NW * 32;                                   // RCAP
-    double* hrp = h1p + RCAP;                                       // RCAP
-    double* h2p = hrp + RCAP;                                       // RCAP
-    double* bq = h2p + RCAP;                                        // RCAP: B y1 of the residual level
-    double* xis = bq + RCAP;                                        // NW x TB staging of x_i
-    double* hred = xis + NW * TB;                                   // NB_W x 96 history partials
-    double* segs = hred + NB_W * 96;                                // NB_W x 128 symbol segments
-    int* tcs = reinterpret_cast<int*>(segs + NB_W * 128);            // TCAP packed (bi << 16 | bj)
-    uint64_t* full = reinterpret_cast<uint64_t*>(tcs + TCAP);
-    uint64_t* empty = full + NHS;
-
-    const unsigned G = gridDim.x;
-    const long long t0 = (long long)blockIdx.x * a.T / G;
-    const long long t1 = (long long)(blockIdx.x + 1) * a.T / G;
-    const long long ntiles = t1 - t0;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nlev = a.nlev, S = a.S, nbb = a.nb;
-    const long long Np = a.Np;
-    const int nsteps = nlev + 2;  // tile steps 0..nlev+1; owner steps 1..nlev+2
-    const long long kstride = (long long)nbb * nbb * TB;
-
-    for (long long k = threadIdx.x; k < ntiles; k += blockDim.x) {
-        int bi, bj;
-        tile_coords(t0 + k, bi, bj);
-        tcs[k] = (bi << 16) | bj;
-    }
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NHS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-
-    auto h64_valid = [&](int t) { return t < nlev; };
-    auto h32_valid = [&](int t) { return t >= 2 && t - 2 < nlev; };
-
-    if (warp == NW) {
-        // ---------------- producer: per step, the FP64 tiles of level t then the FP32 tiles of level t-2
-        if (lane == 0) {
-            uint64_t policy;
-            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(policy));
-            // item cursor: (step, kind, tile); a second cursor pf items ahead feeds L2 prefetches
-            struct Cur {
-                int t, kind;
-                long long k;
-            };
-            auto valid = [&](const Cur& c) { return c.kind == 0 ? h64_valid(c.t) : h32_valid(c.t); };
-            auto settle = [&](Cur& c) {
-                while (c.t < nsteps && (ntiles == 0 || !valid(c))) {
-                    if (c.kind == 0) {
-                        c.kind = 1;
-                    } else {
-                        c.kind = 0;
-                        ++c.t;
-                    }
-                }
-            };
-            auto advance = [&](Cur& c) {
-                if (++c.k == ntiles) {
-                    c.k = 0;
-                    if (c.kind == 0) {
-                        c.kind = 1;
-                    } else {
-                        c.kind = 0;
-                        ++c.t;
-                    }
-                    settle(c);
-                }
-            };
-            auto src_of = [&](const Cur& c) -> const void* {
-                const long long tix = (long long)(c.kind == 0 ? c.t : c.t - 2) * a.T + t0 + c.k;
-                return c.kind == 0 ? (const void*)(a.H64 + tix * TILE) : (const void*)(a.H32 + tix * TILE);
-            };
-            Cur c{0, 0, 0};
-            settle(c);
-            Cur pc = c;
-            for (int i = 0; i < a.pf_items && pc.t < nsteps; ++i) advance(pc);
-            for (long long it = 0; c.t < nsteps; ++it) {
-                const unsigned hbytes = c.kind == 0 ? TILE / 2 * sizeof(double) : TILE / 2 * sizeof(float);
-                for (int h = 0; h < 2; ++h) {
-                    const long long j = 2 * it + h;
-                    const int slot = (int)(j % NHS);
-                    if (j >= NHS) mbar_wait(&empty[slot], (unsigned)((j / NHS - 1) & 1));
-                    const char* src = (const char*)src_of(c) + h * hbytes;
-                    mbar_expect_tx(&full[slot], hbytes);
-                    if (a.evict_first)
-                        tma_bulk_g2s_stream(ring + slot * HSLOT, src, hbytes, &full[slot], policy);
-                    else
-                        tma_bulk_g2s(ring + slot * HSLOT, src, hbytes, &full[slot]);
-                }
-                if (a.pf_items > 0 && pc.t < nsteps) {
-                    prefetch_l2(src_of(pc), pc.kind == 0 ? TILE * sizeof(double) : TILE * sizeof(float));
-                    advance(pc);
-                }
-                advance(c);
-            }
-        }
-        return;
-    }
-
-    // ---------------- workers
-    const long long R = ((Np + G - 1) / G + 3) / 4 * 4;  // multiple of 4: vector history loads
-    const long long r0 = min(Np, (long long)blockIdx.x * R);
-    const long long r1 = min(Np, r0 + R);
-    const int rb0 = (int)(r0 / TB), rb1 = r1 > r0 ? (int)((r1 - 1) / TB) : rb0 - 1;
-    long long it = 0;
-
-    // one owned row per lane (R <= 32, checked on the host)
-    const long long r = r0 + lane;
-    const bool rvalid = r < r1;
-    const long long rr = rvalid ? r : (r1 > r0 ? r0 : 0);  // clamped in-range row for inactive lanes
-    const bool pad = (int)(rr % a.ld2) >= a.n2;
-    const long long rb_own = rr / TB, ro_own = rr % TB;
-
-    for (int t = 0; t <= nsteps; ++t) {
-        unsigned long long* tr = a.trace ? a.trace + ((long long)blockIdx.x * (nsteps + 1) + t) * 12 : nullptr;
-        if (tr && threadIdx.x == 0) tr[0] = gtime();
-        // =============== owner step t: reduce the partials of step t-1 and publish
-        //   warp 0: y1_{t-1} -> Y1, x1_t and the B-tile input y1_{t-1}
-        //   warp 2: B y1_{t-2} and d_{t-3} -> DL, y, the residual r_{t-2} and x2_{t-2}
-        const bool kv0 = t >= 1 && t - 1 < nlev, kv1 = t >= 2 && t - 2 < nlev, kv2 = t >= 3 && t - 3 < nlev;
-        const bool do_x0 = t < nlev, do_x2 = t >= 2 && t - 2 < nlev;
-        // loads that do not depend on this step's partials are issued before the polls
-        double c_z = 0, c_d1 = 0, c_di = 0, c_d2 = 0, c_y = 0, c_h = 0, c_hr = 0;
-        if (warp == 0 && do_x0) {
-            if (t < S) {
-                const long long o = (long long)t * Np + rr;
-                c_z = a.z[o];
-                c_d1 = a.D1[o];
-                c_di = a.d2inv[o];
-            } else {
-                c_z = a.z[(long long)S * Np + rr];
-                c_di = a.d2inv[(long long)(S - 1) * Np + rr];
-            }
-        }
-        if (warp == 2) {
-            if (kv2) c_y = __ldcg(a.Y1 + (long long)(t - 3) * Np + rr);
-            if (do_x2) {
-                const int l = t - 2;
-                if (l < S) {
-                    const long long o = (long long)l * Np + rr;
-                    c_z = a.z[o];
-                    c_d1 = a.D1[o];
-                    c_d2 = a.D2[o];
-                    c_di = a.d2inv[o];
-                } else {
-                    const long long ol = (long long)(S - 1) * Np + rr;
-                    c_z = a.z[(long long)S * Np + rr];
-                    c_d1 = __ldcg(a.Y1 + ol);  // y1_{S-1}
-                    c_d2 = a.D2[ol];
-                    c_di = a.d2inv[ol];
-                }
-            }
-        }
-        if (t >= 1) {
-            const bool kv[3] = {kv0, kv1, kv2};
-            const unsigned target[3] = {(unsigned)(nbb * t), (unsigned)(nbb * (t - 1)), (unsigned)(nbb * (t - 2))};
-            // the (kind, row block) counters are polled by different warps in parallel
-            const int nrb = rb1 - rb0 + 1;
-            for (int q = warp; q < 3 * nrb; q += NW) {
-                const int kind = q / nrb, rb = rb0 + q % nrb;
-                if (kv[kind]) warp_spin_until(a.pdone + (kind * nbb + rb) * CSTR, target[kind]);
-            }
-            worker_bar();
-            if (tr && threadIdx.x == 0) tr[1] = gtime();
-            // history sums of step t-1 are read now: the spare warps overwrite them after the next barrier
-            if (warp == 0) c_h = h1p[lane];
-            if (warp == 2) {
-                c_h = h2p[lane];
-                c_hr = hrp[lane];
-            }
-            // every warp loads its ~nb / NW partials of all three kinds at once (fixed order)
-            const int par = (t - 1) & 1;
-            double pv[3][KPW];
-#pragma unroll
-            for (int kind = 0; kind < 3; ++kind) {
-                const double* pbk = a.pb + (long long)(kind * 2 + par) * kstride + rb_own * nbb * TB + ro_own;
-#pragma unroll
-                for (int u = 0; u < KPW; ++u) {
-                    const int k = warp + u * NW;
-                    pv[kind][u] = kv[kind] && k < nbb ? __ldcg(pbk + (long long)k * TB) : 0.0;
-                }
-            }
-#pragma unroll
-            for (int kind = 0; kind < 3; ++kind) {
-                double s0 = 0.0;
-#pragma unroll
-                for (int u = 0; u < KPW; ++u) s0 += pv[kind][u];
-                red[(kind * NW + warp) * 32 + lane] = s0;
-            }
-            worker_bar();
-        }
-        if (tr && threadIdx.x == 0) tr[2] = gtime();
-        if (warp == 0) {
-            double v0 = 0.0;
-            if (kv0) {
-                for (int w = 0; w < NW; ++w) v0 += red[w * 32 + lane];
-                if (pad) v0 = 0.0;
-                if (rvalid) {
-                    a.Y1[(long long)(t - 1) * Np + r] = v0;
-                    a.xb[(long long)(1 * 2 + (t & 1)) * Np + r] = v0;
-                }
-            }
-            if (do_x0 && rvalid) {
-                double x;
-                if (t < S) {
-                    const double hist = (t >= 2 ? c_h : 0.0) + a.epad[1] * v0;  // v0 = y1_{t-1}
-                    x = (c_z - c_d1 * hist) * c_di;
-                } else {
-                    x = (c_z - v0) * c_di;  // f-level: z_f - y1_{S-1}
-                }
-                a.xb[(long long)(0 * 2 + (t & 1)) * Np + r] = pad ? 0.0 : x;
-            }
-        } else if (warp == 2) {
-            double v1 = 0.0, v2 = 0.0;
-            if (kv1) {
-                for (int w = 0; w < NW; ++w) v1 += red[(NW + w) * 32 + lane];
-                if (pad) v1 = 0.0;
-            }
-            if (kv2) {
-                for (int w = 0; w < NW; ++w) v2 += red[(2 * NW + w) * 32 + lane];
-                if (pad) v2 = 0.0;
-                if (rvalid) {
-                    const long long o = (long long)(t - 3) * Np + r;
-                    a.DLf[o] = (float)v2;
-                    a.y[o] = c_y + v2;
-                }
-            }
-            if (do_x2 && rvalid) {
-                const int l = t - 2;
-                double x;
-                if (l < S) {
-                    // r_l = z_l - (D1 o sum_{m<=l} e_{l-m} y1_m + cs D2 o B y1_l);  d_{l-1} = v2
-                    const double res = c_z - (c_d1 * c_hr + a.cs * c_d2 * v1);
-                    const double hist = (l >= 2 ? c_h : 0.0) + (l >= 1 ? a.epad[1] * v2 : 0.0);
-                    x = (res - c_d1 * hist) * c_di;
-                } else {
-                    // f-level: r_f = z_f - (y1_{S-1} + cr D2_{S-1} o B y1_S);  x2 = (r_f - d_{S-1}) / D2
-                    const double res = c_z - (c_d1 + a.cr * c_d2 * v1);
-                    x = (res - v2) * c_di;
-                }
-                a.xb[(long long)(2 * 2 + (t & 1)) * Np + r] = pad ? 0.0 : x;
-            }
-        }
-        if (t == nsteps) break;  // the last step only finishes d_{nlev-1} and y
-        // publish: warps 0 and 2 meet the spare warps (whose history sums read Y1 / DL rows just
-        // written) at a named barrier, then one release per owned row block
-        if (warp == 0 || warp == 2 || warp >= NST) {
-            asm volatile("bar.sync 3, %0;\n" ::"n"((2 + NB_W) * 32) : "memory");
-            if (threadIdx.x == 0)
-                for (int rb = rb0; rb <= rb1; ++rb) red_release(a.xready + rb * CSTR, 1u);
-        }
-        if (tr && threadIdx.x == 0) tr[3] = gtime();
-
-        // =============== spare warps, first: history sums the owner needs at step t+1 (they only
-        // read this CTA's own rows, so they fill the wait for the other CTAs' x blocks)
-        //   h1p = sum_{m<=t-1} e_{t+1-m} y1_m    (x1_{t+1}; + e1 y1_t at owner time)
-        //   hrp = sum_{m<=t-1} e_{t-1-m} y1_m    (residual of level t-1)
-        //   h2p = sum_{m<=t-3} e_{t-1-m} d_m     (x2_{t-1}; + e1 d_{t-2} at owner time)
-        // These loads are latency-bound, so each instruction carries several levels: y1 as double2
-        // (2 rows per lane, 2 levels per load), d as float4 of its FP32 copy (4 rows, 4 levels), and
-        // 4 independent loads per lane and array are kept in flight.
-        if (warp >= NST && t >= 1) {
-            const int hw = warp - NST;
-            const double* ep = a.epad;  // zero outside 0..S-1
-            const int py = lane & 15, gy = lane >> 4;
-            const long long ry = r0 + 2 * py;
-            const bool vy = ry < r1;  // r1 - r0 is a multiple of 4
-            double2 a1 = make_double2(0.0, 0.0), ar = a1;
-            const int pd = lane & 7, gd = lane >> 3;
-            const long long rdr = r0 + 4 * pd;
-            const bool vd = rdr < r1;
-            double a2[4] = {0.0, 0.0, 0.0, 0.0};
-            // one round trip per iteration covers 80 levels of each array (8 double2 + 4 float4 loads)
-            for (int i0 = 0; i0 <= t - 1; i0 += 80) {
-                double2 yv[8];
-                float4 dv[4];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int m = i0 + 2 * hw + gy + u * 2 * NB_W;
-                    yv[u] = vy && m <= t - 1 ? __ldcg(reinterpret_cast<const double2*>(a.Y1 + (long long)m * Np + ry))
-                                             : make_double2(0.0, 0.0);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int m = i0 + 4 * hw + gd + u * 4 * NB_W;
-                    dv[u] = vd && m <= t - 3 ? __ldcg(reinterpret_cast<const float4*>(a.DLf + (long long)m * Np + rdr))
-                                             : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int m = i0 + 2 * hw + gy + u * 2 * NB_W;
-                    const double e1 = __ldg(ep + t + 1 - m), er = __ldg(ep + t - 1 - m);
-                    a1.x += e1 * yv[u].x;
-                    a1.y += e1 * yv[u].y;
-                    ar.x += er * yv[u].x;
-                    ar.y += er * yv[u].y;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const double em = __ldg(ep + t - 1 - (i0 + 4 * hw + gd + u * 4 * NB_W));
-                    a2[0] += em * dv[u].x;
-                    a2[1] += em * dv[u].y;
-                    a2[2] += em * dv[u].z;
-                    a2[3] += em * dv[u].w;
-                }
-            }
-            // fold the level groups (lanes 16 apart for y1; 8 and 16 apart for d)
-            a1.x += __shfl_down_sync(0xffffffffu, a1.x, 16);
-            a1.y += __shfl_down_sync(0xffffffffu, a1.y, 16);
-            ar.x += __shfl_down_sync(0xffffffffu, ar.x, 16);
-            ar.y += __shfl_down_sync(0xffffffffu, ar.y, 16);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                a2[i] += __shfl_down_sync(0xffffffffu, a2[i], 16);
-                a2[i] += __shfl_down_sync(0xffffffffu, a2[i], 8);
-            }
-            double* rd = hred + hw * 96;
-            if (lane < 16) {
-                rd[2 * lane] = a1.x;
-                rd[2 * lane + 1] = a1.y;
-                rd[32 + 2 * lane] = ar.x;
-                rd[32 + 2 * lane + 1] = ar.y;
-            }
-            if (lane < 8)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) rd[64 + 4 * lane + i] = a2[i];
-            bwarp_bar();
-            if (hw == 0) {
-                double s1 = 0.0, sr = 0.0, s2 = 0.0;
-                for (int w = 0; w < NB_W; ++w) {
-                    s1 += hred[w * 96 + lane];
-                    sr += hred[w * 96 + 32 + lane];
-                    s2 += hred[w * 96 + 64 + lane];
-                }
-                h1p[lane] = s1;
-                hrp[lane] = sr;
-                h2p[lane] = s2;
-            }
-            bwarp_bar();
-        }
-        if (tr && threadIdx.x == NST * 32) tr[5] = gtime();
-
-        // =============== tiles of step t
-        const unsigned xtarget_step = (unsigned)(t + 1);
-        if (warp < NST) {
-            // ring items: FP64 tiles of level t, then FP32 tiles of level t-2.  Item -> warp item % NST
-            // (items k and k + NST share a ring slot, so one warp consumes them in order).
-            const long long base0 = it, base1 = it + (h64_valid(t) ? ntiles : 0);
-            const long long kk0 = ((long long)warp - base0 % NST + NST) % NST;
-            const long long kk1 = ((long long)warp - base1 % NST + NST) % NST;
-            const int n0 = h64_valid(t) && kk0 < ntiles ? (int)((ntiles - kk0 + NST - 1) / NST) : 0;
-            const int n1 = h32_valid(t) && kk1 < ntiles ? (int)((ntiles - kk1 + NST - 1) / NST) : 0;
-            const int nitems = n0 + n1;
-            auto item_of = [&](int c, int& kind, long long& kk) {
-                kind = c < n0 ? 0 : 1;
-                kk = c < n0 ? kk0 + (long long)c * NST : kk1 + (long long)(c - n0) * NST;
-            };
-            // one poll round for every x block this warp reads in this step (lane 2c: bi, 2c+1: bj)
-            for (int c0 = 0; c0 < nitems; c0 += 16) {
-                const int c = c0 + (lane >> 1);
-                const unsigned* ctr = nullptr;
-                unsigned tgt = 0;
-                if (c < nitems) {
-                    int kind, bi, bj;
-                    long long kk;
-                    item_of(c, kind, kk);
-                    bi = tcs[kk] >> 16;
-                    bj = tcs[kk] & 0xffff;
-                    const int blk = (lane & 1) ? bj : bi;
-                    ctr = a.xready + blk * CSTR;
-                    tgt = (unsigned)owners_of_block(blk, R, G) * xtarget_step;
-                }
-                for (unsigned n = 0; !__all_sync(0xffffffffu, ctr == nullptr || ld_relaxed(ctr) >= tgt); ++n) {
-                    __nanosleep(64);
-                    if (n == kSpinLimit) __trap();
-                }
-                if (ctr) (void)ld_acquire(ctr);
-            }
-            if (tr && lane == 0) atomicMax(tr + 8, gtime());
-            // x blocks of item c+1 are loaded while item c computes
-            double2 nxj = make_double2(0.0, 0.0), nxi = nxj;
-            auto load_x = [&](int c) {
-                int kind, bi, bj;
-                long long kk;
-                item_of(c, kind, kk);
-                bi = tcs[kk] >> 16;
-                bj = tcs[kk] & 0xffff;
-                const double* xb = a.xb + (long long)((kind == 0 ? 0 : 2) * 2 + (t & 1)) * Np;
-                nxj = __ldcg(reinterpret_cast<const double2*>(xb + (long long)bj * TB) + lane);
-                nxi = __ldcg(reinterpret_cast<const double2*>(xb + (long long)bi * TB) + lane);
-            };
-            if (nitems > 0) load_x(0);
-            double* xi = xis + warp * TB;
-            float* xif = reinterpret_cast<float*>(xi);
-            unsigned long long wsum = 0, csum = 0;
-            for (int c = 0; c < nitems; ++c) {
-                const unsigned long long tc0 = tr ? gtime() : 0;
-                int kind, bi, bj;
-                long long kk;
-                item_of(c, kind, kk);
-                const double2 xj = nxj;
-                if (kind == 0)
-                    reinterpret_cast<double2*>(xi)[lane] = nxi;
-                else
-                    reinterpret_cast<float2*>(xif)[lane] = make_float2((float)nxi.x, (float)nxi.y);
-                if (c + 1 < nitems) load_x(c + 1);
-                __syncwarp();
-                bi = tcs[kk] >> 16;
-                bj = tcs[kk] & 0xffff;
-                const long long item = (kind == 0 ? base0 : base1) + kk;
-                double* pbk = a.pb + (long long)((kind == 0 ? 0 : 2) * 2 + (t & 1)) * kstride;
-                double* prow = pbk + ((long long)bi * nbb + bj) * TB;
-                double* pcol = pbk + ((long long)bj * nbb + bi) * TB;
-                const int hs0 = (int)((2 * item) % NHS);  // half-slots 2 item, 2 item + 1 (mod NHS)
-                auto begin = [&](int h) {
-                    const long long j = 2 * item + h;
-                    const unsigned long long tw0 = tr ? gtime() : 0;
-                    mbar_wait(&full[j % NHS], (unsigned)((j / NHS) & 1));
-                    if (tr) wsum += gtime() - tw0;
-                };
-                auto end = [&](int h) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[(2 * item + h) % NHS]);
-                };
-                if (kind == 0) {
-                    tile_product(
-                        begin,
-                        [&](int h, int q) {
-                            return reinterpret_cast<const double2*>(ring + (hs0 + h) * HSLOT + q * TB)[lane];
-                        },
-                        end, xj, xi, prow, pcol, bi == bj, lane);
-                } else {
-                    const float* ringf = reinterpret_cast<const float*>(ring);
-                    tile_product_f32(
-                        begin,
-                        [&](int h, int q) {
-                            return reinterpret_cast<const float2*>(ringf + (hs0 + h) * (2 * HSLOT) + q * TB)[lane];
-                        },
-                        end, make_float2((float)xj.x, (float)xj.y), xif, prow, pcol, bi == bj, lane);
-                }
-                __syncwarp();
-                if (tr) csum += gtime() - tc0;
-            }
-            it += (h64_valid(t) ? ntiles : 0) + (h32_valid(t) ? ntiles : 0);
-            if (tr && lane == 0) {
-                atomicMax(tr + 4, gtime());
-                atomicAdd(tr + 7, wsum);
-                atomicAdd(tr + 10, csum);
-            }
-            // one release fence per warp and step, then bump the partial-product counters
-            __syncwarp();
-            if (lane == 0 && nitems > 0) {
-                asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-                for (int c = 0; c < nitems; ++c) {
-                    int kind, bi, bj;
-                    long long kk;
-                    item_of(c, kind, kk);
-                    bi = tcs[kk] >> 16;
-                    bj = tcs[kk] & 0xffff;
-                    const int xk = kind == 0 ? 0 : 2;
-                    red_relaxed(a.pdone + (xk * nbb + bi) * CSTR, 1u);
-                    if (bi != bj) red_relaxed(a.pdone + (xk * nbb + bj) * CSTR, 1u);
-                }
-            }
-        } else if (t >= 1 && t - 1 < nlev) {
-            // generated B tiles of the residual of level t-1 (no HBM traffic): B(i, j) = a[m_i - m_j].
-            // A 64-row block lies inside one i1 row (ld2 % 64 == 0), so tile (bi, bj) needs the 127
-            // symbol entries seg[k] = a[i1 - j1][i2_0 - j2_0 + k - 63]: B(r, c) = seg[r - c + 63].
-            const int bw = warp - NST;
-            const double* xb = a.xb + (long long)(1 * 2 + (t & 1)) * Np;
-            double* pbk = a.pb + (long long)(1 * 2 + (t & 1)) * kstride;
-            double* seg = segs + bw * 128;
-            const int nitems = bw < ntiles ? (int)((ntiles - bw + NB_W - 1) / NB_W) : 0;
-            for (int c0 = 0; c0 < nitems; c0 += 16) {
-                const int c = c0 + (lane >> 1);
-                const unsigned* ctr = nullptr;
-                unsigned tgt = 0;
-                if (c < nitems) {
-                    int bi, bj;
-                    bi = tcs[bw + (long long)c * NB_W] >> 16;
-                    bj = tcs[bw + (long long)c * NB_W] & 0xffff;
-                    const int blk = (lane & 1) ? bj : bi;
-                    ctr = a.xready + blk * CSTR;
-                    tgt = (unsigned)owners_of_block(blk, R, G) * xtarget_step;
-                }
-                for (unsigned n = 0; !__all_sync(0xffffffffu, ctr == nullptr || ld_relaxed(ctr) >= tgt); ++n) {
-                    __nanosleep(64);
-                    if (n == kSpinLimit) __trap();
-                }
-                if (ctr) (void)ld_acquire(ctr);
-            }
-            if (tr && lane == 0) atomicMax(tr + 9, gtime());
-            double2 nxj = make_double2(0.0, 0.0), nxi = nxj;
-            double ng[4];
-            auto load_b = [&](int c) {
-                int bi, bj;
-                bi = tcs[bw + (long long)c * NB_W] >> 16;
-                bj = tcs[bw + (long long)c * NB_W] & 0xffff;
-                const long long i0 = (long long)bi * TB, j0 = (long long)bj * TB;
-                const int i1 = (int)(i0 / a.ld2), i2 = (int)(i0 % a.ld2);
-                const int j1 = (int)(j0 / a.ld2), j2 = (int)(j0 % a.ld2);
-                const double* g = a.gen + (long long)(i1 - j1 + a.n1 - 1) * a.gen_stride + a.ld2 + i2 - j2 - 63;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) ng[u] = (lane + 32 * u < 127) ? __ldg(g + lane + 32 * u) : 0.0;
-                nxj = __ldcg(reinterpret_cast<const double2*>(xb + j0) + lane);
-                nxi = __ldcg(reinterpret_cast<const double2*>(xb + i0) + lane);
-            };
-            if (nitems > 0) load_b(0);
-            double* xi = xis + warp * TB;
-            for (int c = 0; c < nitems; ++c) {
-                const double2 xj = nxj;
-                reinterpret_cast<double2*>(xi)[lane] = nxi;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) seg[lane + 32 * u] = ng[u];
-                if (c + 1 < nitems) load_b(c + 1);
-                __syncwarp();
-                int bi, bj;
-                bi = tcs[bw + (long long)c * NB_W] >> 16;
-                bj = tcs[bw + (long long)c * NB_W] & 0xffff;
-                // pad columns meet zero entries of x; pad rows are zeroed by the owner
-                tile_product([](int) {},
-                             [&](int h, int q) {
-                                 const int r = h * 32 + q;
-                                 return make_double2(seg[r - 2 * lane + 63], seg[r - 2 * lane + 62]);
-                             },
-                             [](int) {}, xj, xi, pbk + ((long long)bi * nbb + bj) * TB,
-                             pbk + ((long long)bj * nbb + bi) * TB, bi == bj, lane);
-                __syncwarp();
-            }
-            if (lane == 0 && nitems > 0) {
-                asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-                for (int c = 0; c < nitems; ++c) {
-                    int bi, bj;
-                    bi = tcs[bw + (long long)c * NB_W] >> 16;
-                    bj = tcs[bw + (long long)c * NB_W] & 0xffff;
-                    red_relaxed(a.pdone + (1 * nbb + bi) * CSTR, 1u);
-                    if (bi != bj) red_relaxed(a.pdone + (1 * nbb + bj) * CSTR, 1u);
-                }
-            }
-            if (tr && lane == 0) atomicMax(tr + 6, gtime());
-        }
-    }
-}
-
-// ============================================================================================
-// Version 2: the two chains decoupled.  Sweep 1 (FP64) and the refinement chain (B residual + FP32
-// sweep) get separate owner phases and separate release counters, run by the spare warps, so the
-// ring warps never wait in an owner phase: while the owners of chain 1 reduce step t and publish
-// x1_{t+1}, the ring warps stream the FP32 tiles of step t, and while chain 2's owners publish
-// x2_{t-1}, they stream the FP64 and B tiles of step t+1.  Per step and ring warp, in FIFO order:
-//   FP64 tiles of level t   (gate: chain-1 counter)   -> partials kind 0, one release fence
-//   B tiles of level t-1    (gate: chain-1 counter)   -> partials kind 1
-//   FP32 tiles of level t-2 (gate: chain-2 counter)   -> partials kind 2, one release fence
-// Spare warps, per step: owner1(t) (y1_{t-1}, x1_t), history of chain 1, owner2(t) (d_{t-3},
-// y = y1 + d, x2_{t-2}), history of chain 2.  The residual r_l = z_l - P y1 reuses the numerator
-// w_l = z_l - D1_l o hist1_l of x1_l (kept in shared memory), so chain 2 needs no history of y1.
+// Per step, ring warps in FIFO order: FP64 tiles of level t (gate: chain-1 counter, partials kind 0,
+// one release fence), FP32 tiles of level t-2 (gate: chain-2 counter, kind 2).  B-tile warps: B tiles
+// of level t-1 (gate: chain-1 counter, kind 1).  Owner warps: owner1(t) (y1_{t-1}, x1_t), history of
+// chain 1, owner2(t) (d_{t-3}, y = y1 + d, x2_{t-2}), history of chain 2.  The residual
+// r_l = z_l - P y1 reuses the numerator w_l = z_l - D1_l o hist1_l of x1_l (kept in shared memory),
+// so chain 2 needs no history of y1.
 constexpr int NR = NST;        // ring warps
 constexpr int NS = NW - NST;   // spare warps: NSO owner warps (owners + history), NS - NSO B-tile warps
 constexpr int NSO = 3;
@@ -799,7 +233,7 @@ constexpr int KPS = 24;        // partials per owner warp and kind: nb <= KPS * 
 __device__ __forceinline__ void spare_bar() { asm volatile("bar.sync 2, %0;\n" ::"n"(NSO * 32) : "memory"); }
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-__global__ void __maxnreg__(168) sweep_ir2_kernel(IrArgs a) {
+__global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
     if (a.skip && *a.skip) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* ring = reinterpret_cast<double*>(smem_raw);  // NHS x HSLOT
@@ -955,12 +389,7 @@ __global__ void __maxnreg__(168) sweep_ir2_kernel(IrArgs a) {
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[(2 * item + h) % NHS]);
                 };
-                if (a.pf_items == -1) {  // TIMING EXPERIMENT: stream only (FI_IR_PF=-1), no compute
-                    begin(0);
-                    end(0);
-                    begin(1);
-                    end(1);
-                } else if (kind == 0) {
+                if (kind == 0) {
                     tile_product(
                         begin,
                         [&](int h, int q) {
@@ -1302,17 +731,12 @@ __global__ void __maxnreg__(168) sweep_ir2_kernel(IrArgs a) {
     }
 }
 
-int sweep_ir2_smem_bytes() {
+int sweep_ir_smem_bytes() {
     return NHS * HSLOT * (int)sizeof(double) +
            (2 * NSO * 32 + NSO * 64 + 32 + 32 + 4 * 32 + 4 * 32 + NW * TB + NS * 128) * (int)sizeof(double) +
            TCAP * (int)sizeof(int) + 2 * NHS * (int)sizeof(uint64_t);
 }
 
-int sweep_ir_smem_bytes() {
-    return NHS * HSLOT * (int)sizeof(double) +
-           (3 * NW * 32 + 4 * RCAP + NW * TB + NB_W * 96 + NB_W * 128) * (int)sizeof(double) + TCAP * (int)sizeof(int) +
-           2 * NHS * (int)sizeof(uint64_t);
-}
 
 }  // namespace
 
@@ -1322,17 +746,13 @@ bool sweep_ir_available(const fi_precond* P) {
         return v ? atoi(v) : 1;
     }();
     return env != 0 && P->mode == 0 && P->Hf.p != nullptr && ((P->sys->L.Np + P->G - 1) / P->G + 3) / 4 * 4 <= RCAP &&
-           P->nb <= KPW * NW && P->nb <= KPS * NSO && (P->T + P->G - 1) / P->G <= TCAP;
+           P->nb <= KPS * NSO && (P->T + P->G - 1) / P->G <= TCAP;
 }
 
 void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip) {
-    static const bool v2 = [] {
-        const char* v = std::getenv("FI_SWEEP_IR2");
-        return v ? std::atoi(v) != 0 : true;
-    }();
     static bool configured = false;
-    const int smem = v2 ? sweep_ir2_smem_bytes() : sweep_ir_smem_bytes();
-    const void* kern = v2 ? (const void*)sweep_ir2_kernel : (const void*)sweep_ir_kernel;
+    const int smem = sweep_ir_smem_bytes();
+    const void* kern = (const void*)sweep_ir_kernel;
     if (!configured) {
         FI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int per_sm = 0;
@@ -1383,11 +803,6 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
         return v ? std::atoi(v) : 1;
     }();
     a.evict_first = evict;
-    static const int pf = [] {
-        const char* v = std::getenv("FI_IR_PF");
-        return v ? std::atoi(v) : 0;
-    }();
-    a.pf_items = pf;
     a.trace = nullptr;
     static const bool tracing = std::getenv("FI_SWEEP_TRACE") != nullptr;
     const int nst1 = levels + 3;
@@ -1401,7 +816,7 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
     void* args[] = {&a};
     FI_CUDA(cudaLaunchCooperativeKernel(kern, dim3(P->G), dim3(THREADS), args, (size_t)smem, ctx->stream));
     FI_LAUNCHED(ctx);
-    if (tracing && v2) {
+    if (tracing) {
         std::vector<unsigned long long> h(trace.n);
         FI_CUDA(cudaMemcpyAsync(h.data(), trace.p, trace.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1420,42 +835,11 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
                     ++cnt;
                 }
             std::fprintf(stderr,
-                         "[sweep_ir2] steps %3d+: step %6.2f us | own1 pub %6.2f | own2 pub %6.2f | FP64 done %6.2f | "
+                         "[sweep_ir] steps %3d+: step %6.2f us | own1 pub %6.2f | own2 pub %6.2f | FP64 done %6.2f | "
                          "B done %6.2f | FP32 done %6.2f | hist1 %6.2f | hist2 %6.2f | producer blocked %6.2f\n",
                          lo, acc[7] / cnt * 1e-3, acc[0] / cnt * 1e-3, acc[1] / cnt * 1e-3, acc[2] / cnt * 1e-3,
                          acc[3] / cnt * 1e-3, acc[4] / cnt * 1e-3, acc[5] / cnt * 1e-3, acc[6] / cnt * 1e-3,
                          acc[8] / cnt * 1e-3);
-        }
-    }
-    if (tracing && !v2) {
-        // per step (averaged over CTAs and steps): pdone wait, reduce, x, ring tiles, history, B tiles
-        std::vector<unsigned long long> h(trace.n);
-        FI_CUDA(cudaMemcpyAsync(h.data(), trace.p, trace.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
-        FI_CUDA(cudaStreamSynchronize(ctx->stream));
-        auto ph = [&](int c, int t, int i) { return (double)h[((size_t)c * nst1 + t) * 12 + i]; };
-        for (int lo : {1, nst1 / 2, nst1 - 40}) {
-            double acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-            int cnt = 0;
-            for (int c = 0; c < P->G; ++c)
-                for (int t = lo; t < lo + 32 && t < nst1 - 3; ++t) {
-                    acc[0] += ph(c, t, 1) - ph(c, t, 0);
-                    acc[1] += ph(c, t, 2) - ph(c, t, 1);
-                    acc[2] += ph(c, t, 3) - ph(c, t, 2);
-                    acc[3] += ph(c, t, 4) - ph(c, t, 3);
-                    acc[4] += ph(c, t, 5) - ph(c, t, 3);
-                    acc[5] += ph(c, t, 6) - ph(c, t, 3);
-                    acc[6] += ph(c, t, 7) / NST;
-                    acc[7] += ph(c, t, 8) - ph(c, t, 3);
-                    acc[8] += ph(c, t, 9) - ph(c, t, 3);
-                    acc[9] += ph(c, t, 10) / NST;
-                    ++cnt;
-                }
-            const double step = (ph(0, std::min(lo + 32, nst1 - 3), 0) - ph(0, lo, 0)) / 32;
-            std::fprintf(stderr,
-                         "[sweep_ir] steps %3d+: step %6.2f us | wait %6.2f | reduce %6.2f | x %6.2f | ring %6.2f | "
-                         "hist %6.2f | btiles %6.2f | ring data wait/warp %6.2f | ring x-poll %6.2f | b x-poll %6.2f | ring item loop/warp %6.2f\n",
-                         lo, step * 1e-3, acc[0] / cnt * 1e-3, acc[1] / cnt * 1e-3, acc[2] / cnt * 1e-3,
-                         acc[3] / cnt * 1e-3, acc[4] / cnt * 1e-3, acc[5] / cnt * 1e-3, acc[6] / cnt * 1e-3, acc[7] / cnt * 1e-3, acc[8] / cnt * 1e-3, acc[9] / cnt * 1e-3);
         }
     }
 }
