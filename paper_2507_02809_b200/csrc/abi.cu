@@ -333,7 +333,9 @@ void fi_precond_destroy(fi_precond* P) {
     fi_system_destroy(sys);
 }
 
-long long fi_precond_bytes(const fi_precond* P) { return P ? (long long)(P->H.bytes() + P->Hf.bytes()) : 0; }
+long long fi_precond_bytes(const fi_precond* P) {
+    return P ? (long long)(P->H.bytes() + P->Hf.bytes() + fib::hodlr_bytes(P->hodlr)) : 0;
+}
 
 int fi_precond_set_refine(fi_precond* P, int refine) {
     return guard([&] {

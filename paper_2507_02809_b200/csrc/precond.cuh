@@ -4,6 +4,10 @@
 
 #include "system.cuh"
 
+namespace fib {
+struct HodlrData;
+}
+
 struct fi_precond {
     fi_system* sys = nullptr;
     int nb = 0;        // 64-row blocks per level (Np / 64)
@@ -11,6 +15,7 @@ struct fi_precond {
     int G = 0;         // persistent CTAs of the apply kernel
     int levels = 0;    // S + 1
     int refine = 1;    // one iterative-refinement sweep with the FP32 inverses (parity with LU solves)
+    fib::HodlrData* hodlr = nullptr;  // dense blocks in HODLR form (precond_hodlr.cu), else packed tiles
     fib::DevBuf<double> H;      // [level][tile][64*64]: packed symmetric inverses
     fib::DevBuf<float> Hf;      // FP32 copy for the refinement sweep
     fib::DevBuf<double> rbuf, dbuf;  // refinement residual and correction
@@ -51,6 +56,16 @@ bool iterative_supported(const Layout& L);
 void precond_build_iterative(fi_precond* P, double tol, int maxit);
 void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip);
 void precond_build(fi_precond* P);
+// HODLR form of the dense-block inverses (precond_hodlr.cu)
+bool hodlr_supported(const Layout& L, int levels, int sm_count);
+HodlrData* hodlr_create(const Layout& L, int levels);
+void hodlr_destroy(HodlrData* h);
+size_t hodlr_bytes(const HodlrData* h);
+size_t hodlr_work_doubles(const Layout& L, int nbt);
+void hodlr_compress(fi_ctx* ctx, HodlrData* h, const Layout& L, const double* W, int nbt, int l0, double* work);
+double hodlr_check(fi_ctx* ctx, HodlrData* h, const Layout& L, const double* W, int nbt, int l0, double* work);
+void hodlr_sweep(fi_ctx* ctx, HodlrData* h, const fi_system* sys, const double* d2inv, const double* z, double* y,
+                 int levels, const int* skip);
 // merged sweep: forward substitution + one refinement step in one persistent kernel (K2)
 bool sweep_ir_available(const fi_precond* P);
 void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip);

@@ -583,6 +583,18 @@ void precond_apply(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int l
     }
     const fi_system* sys = P->sys;
     const bool full = levels == sys->L.S + 1;
+    if (P->hodlr) {
+        // HODLR blocks: sweep, residual r = z - P y through K1, correction sweep, y += d
+        hodlr_sweep(ctx, P->hodlr, sys, P->d2inv.p, z, y, levels, skip);
+        if (!P->refine) return;
+        if (!full)
+            FI_CUDA(cudaMemsetAsync(y + (long long)sys->L.S * sys->L.Np, 0, sys->L.Np * sizeof(double), ctx->stream));
+        toeplitz_apply(ctx, sys->view(), y, P->rbuf.p, skip, z, true);
+        hodlr_sweep(ctx, P->hodlr, sys, P->d2inv.p, P->rbuf.p, P->dbuf.p, levels, skip);
+        axpy_kernel<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(y, P->dbuf.p, (long long)levels * sys->L.Np, skip);
+        FI_LAUNCHED(ctx);
+        return;
+    }
     if (P->refine && sweep_ir_available(P)) {
         // sweep + residual + refinement sweep interleaved in one persistent kernel
         launch_sweep_ir(ctx, P, z, y, levels, skip);

@@ -10,6 +10,8 @@
 // is applied to the Gauss-Jordan pivots, the LDL^T diagonal of M.
 #include <cmath>
 
+#include <cstdlib>
+
 #include "precond.cuh"
 
 namespace fib {
@@ -276,8 +278,12 @@ void precond_build(fi_precond* P) {
     P->nb = (int)(Np / TB);
     P->T = (long long)P->nb * (P->nb + 1) / 2;
     P->levels = S + 1;
-    P->H.alloc((size_t)(S + 1) * P->T * TILE);
-    P->Hf.alloc((size_t)(S + 1) * P->T * TILE);
+    // dense blocks in HODLR form when the sweep supports the shape (FI_HODLR=0: packed tiles)
+    static const bool hodlr_env = [] {
+        const char* v = std::getenv("FI_HODLR");
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    bool use_hodlr = hodlr_env && hodlr_supported(L, S + 1, ctx->sm_count);
     P->rbuf.alloc((size_t)L.nI());
     P->dbuf.alloc((size_t)L.nI());
     P->d2inv.alloc((size_t)S * Np);
@@ -303,40 +309,66 @@ void precond_build(fi_precond* P) {
         Dinv((size_t)batch * TILE), piv((size_t)batch * 2);
     std::vector<double> piv_h((size_t)batch * 2);
     const OperatorView op = sys->view();
-    int first_singular = 0;
-    for (long long l0 = 0; l0 < S + 1; l0 += batch) {
-        const int nbt = (int)std::min<long long>(batch, S + 1 - l0);
-        for (int b = 0; b < nbt; ++b) {
-            piv_h[2 * b] = INFINITY;
-            piv_h[2 * b + 1] = 0.0;
+    // One pass over all levels; the HODLR pass checks every batch a posteriori (probe vector,
+    // |H x - H_hodlr x| <= 1e-12 |H x|) and, if the rank does not suffice, the build restarts with
+    // packed tiles.
+    auto build_pass = [&](bool hodlr) -> bool {
+        DevBuf<double> hwork;
+        if (hodlr) {
+            P->hodlr = hodlr_create(L, S + 1);
+            hwork.alloc(std::max(hodlr_work_doubles(L, (int)batch), (size_t)batch * (2 * 64 * 2 * 32 + 2)));
+        } else {
+            P->H.alloc((size_t)(S + 1) * P->T * TILE);
+            P->Hf.alloc((size_t)(S + 1) * P->T * TILE);
         }
-        FI_CUDA(cudaMemcpyAsync(piv.p, piv_h.data(), 2 * nbt * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        FillArgs fa{op, W.p, (int)l0, diag_d.p, bscale_d.p};
-        gj_fill<<<dim3((unsigned)std::min<long long>(4096, (Np * Np + 255) / 256), nbt), 256, 0, ctx->stream>>>(fa);
-        FI_LAUNCHED(ctx);
-        for (int K = 0; K < P->nb; ++K) {
-            const int K0 = K * TB;
-            gj_diag_inv<<<nbt, 256, 0, ctx->stream>>>(W.p, Np, K0, Dinv.p, piv.p);
+        int first_singular = 0;
+        for (long long l0 = 0; l0 < S + 1; l0 += batch) {
+            const int nbt = (int)std::min<long long>(batch, S + 1 - l0);
+            for (int b = 0; b < nbt; ++b) {
+                piv_h[2 * b] = INFINITY;
+                piv_h[2 * b + 1] = 0.0;
+            }
+            FI_CUDA(cudaMemcpyAsync(piv.p, piv_h.data(), 2 * nbt * sizeof(double), cudaMemcpyHostToDevice,
+                                    ctx->stream));
+            FillArgs fa{op, W.p, (int)l0, diag_d.p, bscale_d.p};
+            gj_fill<<<dim3((unsigned)std::min<long long>(4096, (Np * Np + 255) / 256), nbt), 256, 0, ctx->stream>>>(fa);
             FI_LAUNCHED(ctx);
-            gj_panels<<<dim3(P->nb, nbt), 256, 0, ctx->stream>>>(W.p, Np, K0, Dinv.p, Ftmp.p, Rtmp.p);
-            FI_LAUNCHED(ctx);
-            gj_update<<<dim3(P->nb, P->nb, nbt), 256, 0, ctx->stream>>>(W.p, Np, K0, Ftmp.p, Rtmp.p);
-            FI_LAUNCHED(ctx);
+            for (int K = 0; K < P->nb; ++K) {
+                const int K0 = K * TB;
+                gj_diag_inv<<<nbt, 256, 0, ctx->stream>>>(W.p, Np, K0, Dinv.p, piv.p);
+                FI_LAUNCHED(ctx);
+                gj_panels<<<dim3(P->nb, nbt), 256, 0, ctx->stream>>>(W.p, Np, K0, Dinv.p, Ftmp.p, Rtmp.p);
+                FI_LAUNCHED(ctx);
+                gj_update<<<dim3(P->nb, P->nb, nbt), 256, 0, ctx->stream>>>(W.p, Np, K0, Ftmp.p, Rtmp.p);
+                FI_LAUNCHED(ctx);
+            }
+            if (hodlr) {
+                hodlr_compress(ctx, P->hodlr, L, W.p, nbt, (int)l0, hwork.p);
+            } else {
+                pack_tiles<<<dim3((unsigned)std::min<long long>(P->T, 4096), nbt), 256, 0, ctx->stream>>>(
+                    W.p, Np, L.n2, L.ld2, P->T, P->H.p + (size_t)l0 * P->T * TILE, P->Hf.p + (size_t)l0 * P->T * TILE);
+                FI_LAUNCHED(ctx);
+            }
+            FI_CUDA(cudaMemcpyAsync(piv_h.data(), piv.p, 2 * nbt * sizeof(double), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+            FI_CUDA(cudaStreamSynchronize(ctx->stream));
+            for (int b = 0; b < nbt && !first_singular; ++b) {
+                const double pmin = piv_h[2 * b], pmax = piv_h[2 * b + 1];
+                if (!(pmax > 0.0) || !(pmin > 1e-14 * pmax)) first_singular = (int)(l0 + b) + 1;
+            }
+            if (first_singular)
+                throw Error(FI_E_SINGULAR,
+                            "precond_build: singular block at time level " + std::to_string(first_singular),
+                            first_singular);
+            if (hodlr && hodlr_check(ctx, P->hodlr, L, W.p, nbt, (int)l0, hwork.p) > 1e-12) {
+                hodlr_destroy(P->hodlr);
+                P->hodlr = nullptr;
+                return false;
+            }
         }
-        pack_tiles<<<dim3((unsigned)std::min<long long>(P->T, 4096), nbt), 256, 0, ctx->stream>>>(
-            W.p, Np, L.n2, L.ld2, P->T, P->H.p + (size_t)l0 * P->T * TILE, P->Hf.p + (size_t)l0 * P->T * TILE);
-        FI_LAUNCHED(ctx);
-        FI_CUDA(cudaMemcpyAsync(piv_h.data(), piv.p, 2 * nbt * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        FI_CUDA(cudaStreamSynchronize(ctx->stream));
-        for (int b = 0; b < nbt && !first_singular; ++b) {
-            const double pmin = piv_h[2 * b], pmax = piv_h[2 * b + 1];
-            if (!(pmax > 0.0) || !(pmin > 1e-14 * pmax)) first_singular = (int)(l0 + b) + 1;
-        }
-        if (first_singular)
-            throw Error(FI_E_SINGULAR,
-                        "precond_build: singular block at time level " + std::to_string(first_singular),
-                        first_singular);
-    }
+        return true;
+    };
+    if (!(use_hodlr && build_pass(true))) build_pass(false);
 }
 
 }  // namespace fib

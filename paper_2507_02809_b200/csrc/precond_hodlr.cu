@@ -1,0 +1,717 @@
+// K2h — the per-level inverses in hierarchical off-diagonal low-rank (HODLR) form, and the forward
+// substitution over them.
+//
+// H_s = M_s^{-1} is dense, but its off-diagonal blocks are numerically low-rank: on
+// config 1 a 2048 x 2048 block has rank 19 at 1e-12 ||H||, a 128 x 128 block rank 12.  With 64-row
+// leaves and a binary tree over them, each internal node (left child I, right child J) stores
+//   H[J, I] ~ Q V^T   (Q: |J| x 32 orthonormal, V = H[I, J] Q: |I| x 32)
+// so y = H x is   y_leaf += H[leaf, leaf] x_leaf   and, per node,   y_J += Q (V^T x_I),  y_I += V (Q^T x_J).
+// A row therefore needs its 64-entry leaf row and one 32-vector per ancestor node: 256 doubles
+// for 64 leaves (depth 6), 8.4 MB per level instead of 67 MB of packed FP64 tiles.
+//
+// Compression (setup, per batch of levels, from the dense Gauss-Jordan inverses): per depth, a
+// randomized range finder  Y = M Omega, Q = CGS2(Y), V = M^T Q  (M = H[J, I]).  Rank 32 against a
+// numerical rank <= 19 at 1e-12 keeps the truncation near rounding level.
+//
+// Sweep (one persistent cooperative kernel, one CTA per 32 rows): per level, a CTA computes x of
+// its rows, publishes the partial projections V^T x / Q^T x of its rows for every ancestor node
+// (one release counter per node side), waits for the other sides' partials and its leaf sibling's
+// x, and forms y.  One cross-CTA hop per level; the whole y history of the CTA's rows stays in
+// shared memory for the L1 time-convolution sums.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "precond.cuh"
+
+namespace fib {
+namespace {
+
+constexpr int TB = 64;     // leaf rows
+constexpr int RK = 32;     // rank per node
+constexpr int HR = 32;     // rows per sweep CTA
+constexpr int HPART = 8;   // threads per row in the sweep: 2 leaf halves + up to 6 ancestor depths
+constexpr int DMAX = 6;    // tree depth supported (nb <= 64 leaves)
+constexpr int CSTR = kCounterStride;
+constexpr unsigned kSpin = 1u << 25;
+constexpr int PRS = HR * 33 + 1;  // per-depth stride of the projection products (doubles)
+constexpr int TVS = RK + 1;       // per-depth stride of the summed projections
+constexpr int YHS = HR + 1;       // per-level stride of the y history (the 8 threads of a row read 8 levels)
+
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_relaxed(unsigned* p, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void warp_wait(const unsigned* p, unsigned target) {
+    for (unsigned n = 0; !__all_sync(0xffffffffu, ld_relaxed(p) >= target); ++n) {
+        __nanosleep(64);
+        if (n == kSpin) __trap();
+    }
+    (void)ld_acquire(p);
+}
+
+// Tree tables (device): per depth d (1..D) and leaf block b: node id and side (0 = I, 1 = J, -1 none)
+struct Tree {
+    int D, nb, nnodes;
+    const int* rb_node;  // [DMAX + 1][nb]
+    const int* rb_side;  // [DMAX + 1][nb]
+    const int* lo;       // [nnodes] first leaf
+    const int* mid;      // [nnodes] first leaf of J
+    const int* hi;       // [nnodes] one past the last leaf
+};
+
+__device__ __forceinline__ double omega(int d, long long row, int k) {
+    // deterministic pseudo-random test matrix (SplitMix64 finaliser -> uniform in [-1, 1))
+    unsigned long long x = (unsigned long long)row * 0x9E3779B97F4A7C15ull + (unsigned long long)(k + 64 * d) * 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return (double)(x >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+// out rows of the nodes at depth d (side `out_side` of each node, 64-row block blockIdx.x):
+//   buf[out rows][k] = sum over the node's other side's rows c of  H[row][c] * in(c, k)
+// in = Omega (mode 0) or buf of the other side (mode 1).  H is the dense inverse W (pads read as 0).
+__global__ void hodlr_gemm(const double* W, long long Np, int n2, int ld2, Tree tr, int d, int out_side, int mode,
+                           double* buf) {
+    const int b = blockIdx.x, lvb = blockIdx.y;
+    const int node = tr.rb_node[d * tr.nb + b];
+    if (node < 0 || tr.rb_side[d * tr.nb + b] != out_side) return;
+    const double* Wb = W + (long long)lvb * Np * Np;
+    double* bf = buf + ((long long)lvb * (DMAX + 1) + d) * Np * RK;
+    const int in_lo = out_side == 1 ? tr.lo[node] : tr.mid[node];
+    const int in_hi = out_side == 1 ? tr.mid[node] : tr.hi[node];
+    __shared__ double Wt[TB][33];
+    __shared__ double Bt[32][RK + 1];
+    const int tid = threadIdx.x;
+    const int orow = tid >> 2, kq = (tid & 3) * 8;
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long r0 = (long long)b * TB;
+    for (long long c0 = (long long)in_lo * TB; c0 < (long long)in_hi * TB; c0 += 32) {
+        for (int q = tid; q < TB * 32; q += blockDim.x) {
+            const int rr = q >> 5, cc = q & 31;
+            const long long i = r0 + rr, j = c0 + cc;
+            const bool pad = (int)(i % ld2) >= n2 || (int)(j % ld2) >= n2;
+            Wt[rr][cc] = pad ? 0.0 : Wb[i * Np + j];
+        }
+        for (int q = tid; q < 32 * RK; q += blockDim.x) {
+            const int cc = q >> 5, k = q & 31;
+            const long long j = c0 + cc;
+            Bt[cc][k] = mode == 0 ? ((int)(j % ld2) >= n2 ? 0.0 : omega(d, j, k)) : bf[j * RK + k];
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int cc = 0; cc < 32; ++cc) {
+            const double w = Wt[orow][cc];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[u] += w * Bt[cc][kq + u];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bf[(r0 + orow) * RK + kq + u] = acc[u];
+}
+
+// CGS2 orthonormalisation of the J-side columns of every node at depth d (in place in buf)
+__global__ void hodlr_cgs2(Tree tr, int d, long long Np, double* buf, int nnodes_d, const int* nodes_d) {
+    const int node = nodes_d[blockIdx.x];
+    const int lvb = blockIdx.y;
+    double* bf = buf + ((long long)lvb * (DMAX + 1) + d) * Np * RK;
+    const long long j0 = (long long)tr.mid[node] * TB, j1 = (long long)tr.hi[node] * TB;
+    __shared__ double red[8][RK];
+    __shared__ double coef[RK];
+    __shared__ double nrm0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto block_sum_vec = [&](double* v, int n) {  // sums v[0..n) over the block into coef[0..n)
+        for (int i = 0; i < n; ++i) {
+            double s = v[i];
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            if (lane == 0) red[warp][i] = s;
+        }
+        __syncthreads();
+        if (tid < n) {
+            double s = 0.0;
+            for (int w = 0; w < 8; ++w) s += red[w][tid];
+            coef[tid] = s;
+        }
+        __syncthreads();
+    };
+    for (int j = 0; j < RK; ++j) {
+        double part[RK];
+        part[0] = 0.0;
+        for (long long r = j0 + tid; r < j1; r += blockDim.x) part[0] += bf[r * RK + j] * bf[r * RK + j];
+        block_sum_vec(part, 1);
+        if (tid == 0) nrm0 = sqrt(coef[0]);
+        __syncthreads();
+        for (int pass = 0; pass < 2 && j > 0; ++pass) {
+            for (int i = 0; i < j; ++i) part[i] = 0.0;
+            for (long long r = j0 + tid; r < j1; r += blockDim.x) {
+                const double v = bf[r * RK + j];
+                for (int i = 0; i < j; ++i) part[i] += bf[r * RK + i] * v;
+            }
+            block_sum_vec(part, j);
+            for (long long r = j0 + tid; r < j1; r += blockDim.x) {
+                double v = bf[r * RK + j];
+                for (int i = 0; i < j; ++i) v -= coef[i] * bf[r * RK + i];
+                bf[r * RK + j] = v;
+            }
+            __syncthreads();
+        }
+        part[0] = 0.0;
+        for (long long r = j0 + tid; r < j1; r += blockDim.x) part[0] += bf[r * RK + j] * bf[r * RK + j];
+        block_sum_vec(part, 1);
+        const double nv = sqrt(coef[0]);
+        // a direction already spanned (numerical rank < 32) is dropped
+        const double sc = nv > 1e-13 * nrm0 && nv > 0.0 ? 1.0 / nv : 0.0;
+        for (long long r = j0 + tid; r < j1; r += blockDim.x) bf[r * RK + j] *= sc;
+        __syncthreads();
+    }
+}
+
+// Pack the sweep layout: per level and 32-row CTA block, element (row i, part p, k) at double2
+// index (k / 2) * 256 + 8 i + p: p = 0, 1 the leaf row (columns 32 p + k of the row's 64-row leaf),
+// p = 2..7 the basis row of the depth-(p-1) ancestor (Q for J rows, V for I rows), 0 if none.
+__global__ void hodlr_pack(const double* W, long long Np, int n2, int ld2, Tree tr, const double* buf,
+                           double2* out) {
+    const int c = blockIdx.x, lvb = blockIdx.y;
+    const double* Wb = W + (long long)lvb * Np * Np;
+    const double* bf = buf + (long long)lvb * (DMAX + 1) * Np * RK;
+    double2* o = out + ((long long)lvb * (Np / HR) + c) * (RK / 2) * 256;
+    const int t = threadIdx.x;  // 256 threads
+    const int i = t >> 3, p = t & 7;
+    const long long r = (long long)c * HR + i;
+    const int b = (int)(r / TB);
+    const bool prow = (int)(r % ld2) >= n2;
+    double v[RK];
+#pragma unroll
+    for (int k = 0; k < RK; ++k) {
+        double val = 0.0;
+        if (!prow) {
+            if (p < 2) {
+                const long long col = (long long)b * TB + 32 * p + k;
+                val = (int)(col % ld2) >= n2 ? 0.0 : Wb[r * Np + col];
+            } else {
+                const int d = p - 1;
+                if (d <= tr.D && tr.rb_node[d * tr.nb + b] >= 0) val = bf[((long long)d * Np + r) * RK + k];
+            }
+        }
+        v[k] = val;
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < RK / 2; ++k2) o[k2 * 256 + t] = make_double2(v[2 * k2], v[2 * k2 + 1]);
+}
+
+// ------------------------------------------------------------------ sweep
+struct HArgs {
+    const double2* hd;  // [level][cta][16][256]
+    int nlev, S;
+    long long Np;
+    int n2, ld2;
+    Tree tr;
+    const double* z;
+    double* y;
+    const double* D1;
+    const double* d2inv;
+    const double* epad;  // epad[k] = e_k (0 <= k < S), zeros around
+    double* xg;          // [2][Np] x of the level (leaf siblings read it)
+    double* proj;        // [2][nnodes][2 sides][slots <= nb * 2][RK] partial projections
+    unsigned* cnt;       // [nnodes][2] release counters (stride CSTR)
+    unsigned* xrd;       // [nb] leaf x counters (stride CSTR)
+    const int* skip;
+    unsigned long long* trace;  // optional [8]: per-phase time sums of CTA 0 (FI_HODLR_TRACE=1)
+};
+
+
+__global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
+    if (a.skip && *a.skip) return;
+    extern __shared__ __align__(16) double sm[];
+    const int nlev = a.nlev, S = a.S, D = a.tr.D, nb = a.tr.nb;
+    const long long Np = a.Np;
+    const int c = blockIdx.x, t = threadIdx.x, warp = t >> 5;
+    const int i = t >> 3, p = t & 7;
+    const long long r0 = (long long)c * HR, r = r0 + i;
+    const int b = (int)(r0 / TB);  // leaf block of the CTA (two CTAs per leaf)
+    const bool prow = (int)(r % a.ld2) >= a.n2;
+    const int maxslots = 2 * nb;
+    // shared memory: y history of the CTA's rows [nlev][32], projection products, staging
+    // (strides padded so that the 8 threads of a row, which differ in depth, hit different banks)
+    double* yh = sm;                               // nlev x YHS: y of the CTA's rows, every level
+    double* pr = yh + (long long)nlev * YHS;       // DMAX x PRS products (row i, k) at i * 33 + k
+    double* stage = pr + DMAX * PRS;               // partial projections of the other sides
+    double* tvec = stage + 2 * nb * RK;            // DMAX x TVS summed projections
+    double* xs = tvec + DMAX * TVS;                // 64 (+1): x of the leaf block, halves at 0 and 33
+    double* hs = xs + TB + 2;                      // 32: history sums of the next level
+    double* es = hs + HR;                          // nlev + 2: L1 weights e_0.. (history sums)
+    // per-depth node, side, slot, and the other side's CTA count
+    __shared__ int s_node[DMAX + 1], s_side[DMAX + 1], s_slot[DMAX + 1], s_nother[DMAX + 1], s_ooff[DMAX + 2];
+    if (t <= DMAX) {
+        int node = -1, side = -1, slot = 0, nother = 0;
+        if (t >= 1 && t <= D) {
+            node = a.tr.rb_node[t * nb + b];
+            side = a.tr.rb_side[t * nb + b];
+            if (node >= 0) {
+                const int lo = a.tr.lo[node], mid = a.tr.mid[node], hi = a.tr.hi[node];
+                slot = side == 0 ? (int)((r0 - (long long)lo * TB) / HR) : (int)((r0 - (long long)mid * TB) / HR);
+                nother = side == 0 ? (hi - mid) * (TB / HR) : (mid - lo) * (TB / HR);
+            }
+        }
+        s_node[t] = node;
+        s_side[t] = side;
+        s_slot[t] = slot;
+        s_nother[t] = nother;
+    }
+    __syncthreads();
+    if (t == 0) {
+        int off = 0;
+        for (int d = 1; d <= DMAX; ++d) {
+            s_ooff[d] = off;
+            off += s_nother[d] * RK;
+        }
+        s_ooff[DMAX + 1] = off;  // total staged partials
+    }
+    __syncthreads();
+    for (int q = t; q < nlev + 2; q += blockDim.x) es[q] = a.epad[q];
+    __syncthreads();
+    const double e1 = es[1];
+    const long long lvstride = (Np / HR) * (RK / 2) * 256;
+    // this thread's 32 coefficients of the current level (registers), prefetched one level ahead
+    double2 cur[RK / 2], nxt[RK / 2];
+    auto load_level = [&](int lv, double2* dst) {
+        const double2* src = a.hd + (long long)lv * lvstride + (long long)c * (RK / 2) * 256;
+#pragma unroll
+        for (int k2 = 0; k2 < RK / 2; ++k2) dst[k2] = __ldg(src + k2 * 256 + t);
+    };
+    // the other sides' partials this thread stages each level: fixed offsets within a parity block
+    constexpr int MAXE = (2 * 64 * RK + 255) / 256;  // <= 2 nb RK staged values / 256 threads
+    int soff[MAXE];
+    double sv[MAXE];
+#pragma unroll
+    for (int u = 0; u < MAXE; ++u) {
+        const int e = t + u * 256;
+        soff[u] = -1;
+        if (e < s_ooff[DMAX + 1]) {
+            int d = 1;
+            while (d < DMAX && e >= s_ooff[d + 1]) ++d;
+            const int le = e - s_ooff[d];
+            soff[u] = (((s_node[d] * 2 + (1 - s_side[d])) * maxslots) + le / RK) * RK + le % RK;
+        }
+    }
+    load_level(0, cur);
+    double hnext = 0.0;  // (p == 0) history sum of the current level's x numerator
+    // (p == 0) z, D1, 1/D2 of the row for level lv, loaded one level ahead
+    auto load_coef = [&](int lv, double& cz, double& cd1, double& cdi) {
+        cz = cd1 = cdi = 0.0;
+        if (p != 0 || prow || lv >= nlev) return;
+        if (lv < S) {
+            const long long o = (long long)lv * Np + r;
+            cz = a.z[o];
+            cd1 = a.D1[o];
+            cdi = a.d2inv[o];
+        } else {
+            cz = a.z[(long long)S * Np + r];
+            cdi = a.d2inv[(long long)(S - 1) * Np + r];
+        }
+    };
+    double cz, cd1, cdi, nz, nd1, ndi;
+    load_coef(0, cz, cd1, cdi);
+    unsigned long long tl = 0;
+    auto stamp = [&](int ph) {
+        if (a.trace && blockIdx.x == 0 && t == 0) {
+            const unsigned long long now = clock64();
+            if (tl) a.trace[ph] += now - tl;
+            tl = now;
+        }
+    };
+    for (int lv = 0; lv < nlev; ++lv) {
+        stamp(7);
+        const int par = lv & 1;
+        // ---- x of the CTA's rows
+        if (p == 0) {
+            double x = 0.0;
+            if (!prow) {
+                if (lv < S) {
+                    const double hist = (lv >= 2 ? hnext : 0.0) + (lv >= 1 ? e1 * yh[(lv - 1) * YHS + i] : 0.0);
+                    x = (cz - cd1 * hist) * cdi;
+                } else {
+                    x = (cz - yh[(S - 1) * YHS + i]) * cdi;
+                }
+            }
+            xs[(r0 % TB) + i + (r0 % TB ? 1 : 0)] = x;
+            a.xg[(long long)par * Np + r] = x;
+        }
+        __syncthreads();
+        stamp(0);
+        // ---- partial projections of the CTA's rows for every ancestor node
+        if (p >= 2 && p - 1 <= D && s_node[p - 1] >= 0) {
+            const double xv = xs[(r0 % TB) + i + (r0 % TB ? 1 : 0)];
+            double* pd = pr + (p - 2) * PRS + i * 33;
+#pragma unroll
+            for (int k2 = 0; k2 < RK / 2; ++k2) {
+                pd[2 * k2] = cur[k2].x * xv;
+                pd[2 * k2 + 1] = cur[k2].y * xv;
+            }
+        }
+        __syncthreads();
+        if (t < D * RK) {
+            const int d = t / RK + 1, k = t % RK;
+            if (s_node[d] >= 0) {
+                const double* pd = pr + (d - 1) * PRS;
+                double s = 0.0;
+                for (int ii = 0; ii < HR; ++ii) s += pd[ii * 33 + k];
+                const long long slotbase = (((long long)par * a.tr.nnodes + s_node[d]) * 2 + s_side[d]) * maxslots;
+                a.proj[(slotbase + s_slot[d]) * RK + k] = s;
+            }
+        }
+        __syncthreads();
+        if (t == 0) {
+            // one release fence for the CTA's partials and x, then relaxed increments
+            asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+            for (int d = 1; d <= D; ++d)
+                if (s_node[d] >= 0) red_relaxed(a.cnt + (s_node[d] * 2 + s_side[d]) * CSTR, 1u);
+            red_relaxed(a.xrd + b * CSTR, 1u);
+        }
+        stamp(1);
+        // next level's coefficients: issued here, off the publish path, consumed at the level's end
+        if (lv + 1 < nlev) load_level(lv + 1, nxt);
+        load_coef(lv + 1, nz, nd1, ndi);
+        // ---- history of the next level (rows' y up to lv - 1): sum_{m <= lv-1} e_{lv+1-m} y_m
+        {
+            double h4[4] = {0.0, 0.0, 0.0, 0.0};
+            if (lv + 1 < S) {
+                int m = p;
+                for (; m + 3 * HPART <= lv - 1; m += 4 * HPART)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) h4[u] += es[lv + 1 - m - u * HPART] * yh[(m + u * HPART) * YHS + i];
+                for (; m <= lv - 1; m += HPART) h4[0] += es[lv + 1 - m] * yh[m * YHS + i];
+            }
+            double h = (h4[0] + h4[1]) + (h4[2] + h4[3]);
+            h += __shfl_xor_sync(0xffffffffu, h, 1);
+            h += __shfl_xor_sync(0xffffffffu, h, 2);
+            h += __shfl_xor_sync(0xffffffffu, h, 4);
+            if (p == 0) hs[i] = h;
+        }
+        stamp(2);
+        // ---- wait for the other sides' partials and the leaf sibling's x
+        if (warp >= 1 && warp <= D && s_node[warp] >= 0) {
+            const int d = warp;
+            warp_wait(a.cnt + (s_node[d] * 2 + (1 - s_side[d])) * CSTR, (unsigned)(s_nother[d] * (lv + 1)));
+        }
+        if (warp == 0) warp_wait(a.xrd + b * CSTR, (unsigned)((TB / HR) * (lv + 1)));
+        __syncthreads();
+        stamp(3);
+        // ---- stage the other sides' partials (all loads in flight), the sibling half of x
+        {
+            const long long pbase = (long long)par * a.tr.nnodes * 2 * maxslots * RK;
+#pragma unroll
+            for (int u = 0; u < MAXE; ++u) sv[u] = soff[u] >= 0 ? __ldcg(a.proj + pbase + soff[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < MAXE; ++u)
+                if (soff[u] >= 0) stage[t + u * 256] = sv[u];
+        }
+        if (t < TB) {
+            const long long rr = (long long)b * TB + t;
+            if (rr < r0 || rr >= r0 + HR) xs[t + (t >= 32 ? 1 : 0)] = __ldcg(a.xg + (long long)par * Np + rr);
+        }
+        __syncthreads();
+        if (t < D * RK) {
+            const int d = t / RK + 1, k = t % RK;
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};
+            if (s_node[d] >= 0)
+                for (int j = 0; j < s_nother[d]; ++j) s4[j & 3] += stage[s_ooff[d] + j * RK + k];
+            tvec[(d - 1) * TVS + k] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+        }
+        __syncthreads();
+        stamp(4);
+        // ---- y of the CTA's rows: leaf product + low-rank terms, 8 threads per row
+        double part = 0.0;
+        if (p < 2) {
+#pragma unroll
+            for (int k2 = 0; k2 < RK / 2; ++k2)
+                part += cur[k2].x * xs[33 * p + 2 * k2] + cur[k2].y * xs[33 * p + 2 * k2 + 1];
+        } else if (p - 1 <= D && s_node[p - 1] >= 0) {
+            const double* tv = tvec + (p - 2) * TVS;
+#pragma unroll
+            for (int k2 = 0; k2 < RK / 2; ++k2) part += cur[k2].x * tv[2 * k2] + cur[k2].y * tv[2 * k2 + 1];
+        }
+        part += __shfl_xor_sync(0xffffffffu, part, 1);
+        part += __shfl_xor_sync(0xffffffffu, part, 2);
+        part += __shfl_xor_sync(0xffffffffu, part, 4);
+        if (p == 0) {
+            const double yv = prow ? 0.0 : part;
+            yh[lv * YHS + i] = yv;
+            a.y[(long long)lv * Np + r] = yv;
+            hnext = hs[i];
+        }
+        __syncthreads();
+        stamp(5);
+#pragma unroll
+        for (int k2 = 0; k2 < RK / 2; ++k2) cur[k2] = nxt[k2];
+        cz = nz;
+        cd1 = nd1;
+        cdi = ndi;
+    }
+}
+
+// ------------------------------------------------------------------ a-posteriori accuracy check
+// For every level of the batch: y = H x with the dense inverse and with the packed HODLR form for a
+// fixed pseudo-random x; acc[level] += (|y_dense - y_hodlr|^2, |y_dense|^2).  Rank 32 is ample for
+// the 1D BASELINE blocks; where it is not (the build checks every batch), the preconditioner falls
+// back to packed tiles.
+__device__ __forceinline__ double probe(long long r, int n2, int ld2) {
+    return (int)(r % ld2) >= n2 ? 0.0 : omega(7, r, 3);
+}
+__global__ void hodlr_check_proj(const double2* hd, long long Np, int n2, int ld2, Tree tr, double* pj) {
+    const int c = blockIdx.x, lvb = blockIdx.y, t = threadIdx.x;
+    const int i = t >> 3, p = t & 7;
+    const long long r = (long long)c * HR + i;
+    const int b = (int)(r / TB);
+    if (p < 2 || p - 1 > tr.D) return;
+    const int d = p - 1, node = tr.rb_node[d * tr.nb + b];
+    if (node < 0) return;
+    const int side = tr.rb_side[d * tr.nb + b];
+    const double2* o = hd + ((long long)lvb * (Np / HR) + c) * (RK / 2) * 256;
+    const double xv = probe(r, n2, ld2);
+    double* dst = pj + (((long long)lvb * tr.nnodes + node) * 2 + side) * RK;
+    for (int k2 = 0; k2 < RK / 2; ++k2) {
+        const double2 v = o[k2 * 256 + t];
+        atomicAdd(dst + 2 * k2, v.x * xv);
+        atomicAdd(dst + 2 * k2 + 1, v.y * xv);
+    }
+}
+__global__ void hodlr_check_apply(const double* W, const double2* hd, long long Np, int n2, int ld2, Tree tr,
+                                  const double* pj, double* acc) {
+    const int c = blockIdx.x, lvb = blockIdx.y, t = threadIdx.x;
+    const int i = t >> 3, p = t & 7;
+    const long long r = (long long)c * HR + i;
+    const int b = (int)(r / TB);
+    const double* Wb = W + (long long)lvb * Np * Np;
+    const double2* o = hd + ((long long)lvb * (Np / HR) + c) * (RK / 2) * 256;
+    const bool prow = (int)(r % ld2) >= n2;
+    double yh = 0.0, yd = 0.0;
+    if (p < 2) {
+        for (int k2 = 0; k2 < RK / 2; ++k2) {
+            const double2 v = o[k2 * 256 + t];
+            const long long c0 = (long long)b * TB + 32 * p + 2 * k2;
+            yh += v.x * probe(c0, n2, ld2) + v.y * probe(c0 + 1, n2, ld2);
+        }
+    } else if (p - 1 <= tr.D && tr.rb_node[(p - 1) * tr.nb + b] >= 0) {
+        const int d = p - 1, node = tr.rb_node[d * tr.nb + b], side = tr.rb_side[d * tr.nb + b];
+        const double* tv = pj + (((long long)lvb * tr.nnodes + node) * 2 + (1 - side)) * RK;
+        for (int k2 = 0; k2 < RK / 2; ++k2) {
+            const double2 v = o[k2 * 256 + t];
+            yh += v.x * tv[2 * k2] + v.y * tv[2 * k2 + 1];
+        }
+    }
+    if (!prow)
+        for (long long col = p; col < Np; col += HPART)
+            if ((int)(col % ld2) < n2) yd += Wb[r * Np + col] * probe(col, n2, ld2);
+    for (int off = 1; off < HPART; off <<= 1) {
+        yh += __shfl_xor_sync(0xffffffffu, yh, off);
+        yd += __shfl_xor_sync(0xffffffffu, yd, off);
+    }
+    if (p == 0 && !prow) {
+        atomicAdd(acc + 2 * lvb, (yd - yh) * (yd - yh));
+        atomicAdd(acc + 2 * lvb + 1, yd * yd);
+    }
+}
+
+size_t hodlr_sweep_smem(int nlev, int nb) {
+    return ((size_t)nlev * YHS + DMAX * PRS + 2 * (size_t)nb * RK + DMAX * TVS + TB + 2 + HR + nlev + 2) *
+           sizeof(double);
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------------- host side
+struct HodlrData {
+    int D = 0, nb = 0, nnodes = 0;
+    DevBuf<int> rb_node, rb_side, lo, mid, hi, nodes_by_depth;
+    std::vector<int> depth_off, depth_cnt;  // nodes of each depth in nodes_by_depth
+    DevBuf<double2> hd;                     // [levels][Np/32][16][256]
+    DevBuf<double> proj, xg;
+    DevBuf<unsigned> cnt;
+    Tree tree() const {
+        return Tree{D, nb, nnodes, rb_node.p, rb_side.p, lo.p, mid.p, hi.p};
+    }
+};
+
+bool hodlr_supported(const Layout& L, int levels, int sm_count) {
+    const long long nb = L.Np / TB;
+    if (nb < 2 || nb > 64) return false;
+    if (L.Np / HR > sm_count) return false;
+    return hodlr_sweep_smem(levels, (int)nb) <= 227 * 1024;
+}
+
+HodlrData* hodlr_create(const Layout& L, int levels) {
+    auto* h = new HodlrData();
+    const int nb = (int)(L.Np / TB);
+    h->nb = nb;
+    std::vector<int> lo, mid, hi, dep;
+    std::vector<int> rbn((size_t)(DMAX + 1) * nb, -1), rbs((size_t)(DMAX + 1) * nb, -1);
+    // recursive bisection of [0, nb): node (lo, mid, hi) at depth d covers leaves lo..hi-1
+    std::vector<std::array<int, 3>> stack{{0, nb, 1}};
+    int D = 0;
+    while (!stack.empty()) {
+        auto [l, hh, d] = stack.back();
+        stack.pop_back();
+        if (hh - l < 2) continue;
+        const int m = (l + hh) / 2;
+        const int id = (int)lo.size();
+        lo.push_back(l);
+        mid.push_back(m);
+        hi.push_back(hh);
+        dep.push_back(d);
+        D = std::max(D, d);
+        for (int bb = l; bb < hh; ++bb) {
+            rbn[(size_t)d * nb + bb] = id;
+            rbs[(size_t)d * nb + bb] = bb < m ? 0 : 1;
+        }
+        stack.push_back({l, m, d + 1});
+        stack.push_back({m, hh, d + 1});
+    }
+    if (D > DMAX) throw Error(FI_E_RESOURCE, "hodlr: tree too deep");
+    h->D = D;
+    h->nnodes = (int)lo.size();
+    std::vector<int> byd;
+    h->depth_off.assign(DMAX + 2, 0);
+    h->depth_cnt.assign(DMAX + 2, 0);
+    for (int d = 1; d <= D; ++d) {
+        h->depth_off[d] = (int)byd.size();
+        for (int n = 0; n < h->nnodes; ++n)
+            if (dep[n] == d) byd.push_back(n);
+        h->depth_cnt[d] = (int)byd.size() - h->depth_off[d];
+    }
+    auto up = [](DevBuf<int>& dst, const std::vector<int>& v) {
+        dst.alloc(std::max<size_t>(v.size(), 1));
+        FI_CUDA(cudaMemcpy(dst.p, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+    };
+    up(h->rb_node, rbn);
+    up(h->rb_side, rbs);
+    up(h->lo, lo);
+    up(h->mid, mid);
+    up(h->hi, hi);
+    up(h->nodes_by_depth, byd);
+    h->hd.alloc((size_t)levels * (L.Np / HR) * (RK / 2) * 256);
+    h->proj.alloc((size_t)2 * h->nnodes * 2 * (2 * nb) * RK);
+    h->xg.alloc((size_t)2 * L.Np);
+    h->cnt.alloc((size_t)(2 * h->nnodes + nb) * CSTR);
+    return h;
+}
+
+void hodlr_destroy(HodlrData* h) { delete h; }
+
+size_t hodlr_bytes(const HodlrData* h) { return h ? h->hd.bytes() : 0; }
+
+// Compress the dense inverses W[0..nbt) of levels l0.. into the sweep layout.
+void hodlr_compress(fi_ctx* ctx, HodlrData* h, const Layout& L, const double* W, int nbt, int l0, double* work) {
+    const long long Np = L.Np;
+    const Tree tr = h->tree();
+    // work: nbt x (DMAX + 1) x Np x RK doubles
+    for (int d = 1; d <= h->D; ++d) {
+        const dim3 g((unsigned)h->nb, (unsigned)nbt);
+        // (no power iteration: without re-orthonormalisation it would wash the small singular
+        // directions out of Y; rank 32 against a numerical rank <= 19 needs none)
+        hodlr_gemm<<<g, 256, 0, ctx->stream>>>(W, Np, L.n2, L.ld2, tr, d, 1, 0, work);  // Y_J = M Omega
+        FI_LAUNCHED(ctx);
+        hodlr_cgs2<<<dim3((unsigned)h->depth_cnt[d], (unsigned)nbt), 256, 0, ctx->stream>>>(
+            tr, d, Np, work, h->depth_cnt[d], h->nodes_by_depth.p + h->depth_off[d]);  // Q_J
+        FI_LAUNCHED(ctx);
+        hodlr_gemm<<<g, 256, 0, ctx->stream>>>(W, Np, L.n2, L.ld2, tr, d, 0, 1, work);  // V_I = M^T Q_J
+        FI_LAUNCHED(ctx);
+    }
+    hodlr_pack<<<dim3((unsigned)(Np / HR), (unsigned)nbt), 256, 0, ctx->stream>>>(
+        W, Np, L.n2, L.ld2, tr, work, h->hd.p + (size_t)l0 * (Np / HR) * (RK / 2) * 256);
+    FI_LAUNCHED(ctx);
+}
+
+size_t hodlr_work_doubles(const Layout& L, int nbt) { return (size_t)nbt * (DMAX + 1) * L.Np * RK; }
+
+// Largest relative error |H x - H_hodlr x| / |H x| over the batch's levels (probe vector x).
+double hodlr_check(fi_ctx* ctx, HodlrData* h, const Layout& L, const double* W, int nbt, int l0, double* work) {
+    const long long Np = L.Np;
+    const Tree tr = h->tree();
+    const double2* hd = h->hd.p + (size_t)l0 * (Np / HR) * (RK / 2) * 256;
+    double* pj = work;                                          // nbt x nnodes x 2 x RK
+    double* acc = work + (size_t)nbt * h->nnodes * 2 * RK;      // nbt x 2
+    FI_CUDA(cudaMemsetAsync(work, 0, ((size_t)nbt * h->nnodes * 2 * RK + 2 * nbt) * sizeof(double), ctx->stream));
+    hodlr_check_proj<<<dim3((unsigned)(Np / HR), (unsigned)nbt), 256, 0, ctx->stream>>>(hd, Np, L.n2, L.ld2, tr, pj);
+    FI_LAUNCHED(ctx);
+    hodlr_check_apply<<<dim3((unsigned)(Np / HR), (unsigned)nbt), 256, 0, ctx->stream>>>(W, hd, Np, L.n2, L.ld2, tr,
+                                                                                        pj, acc);
+    FI_LAUNCHED(ctx);
+    std::vector<double> hacc((size_t)2 * nbt);
+    FI_CUDA(cudaMemcpyAsync(hacc.data(), acc, hacc.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    FI_CUDA(cudaStreamSynchronize(ctx->stream));
+    double worst = 0.0;
+    for (int q = 0; q < nbt; ++q)
+        worst = std::max(worst, hacc[(size_t)2 * q + 1] > 0 ? std::sqrt(hacc[(size_t)2 * q] / hacc[(size_t)2 * q + 1]) : 0.0);
+    return worst;
+}
+
+void hodlr_sweep(fi_ctx* ctx, HodlrData* h, const fi_system* sys, const double* d2inv, const double* z, double* y,
+                 int levels, const int* skip) {
+    const Layout& L = sys->L;
+    const size_t smem = hodlr_sweep_smem(levels, h->nb);
+    static size_t configured = 0;
+    if (smem > configured) {
+        FI_CUDA(cudaFuncSetAttribute(hodlr_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    HArgs a;
+    a.hd = h->hd.p;
+    a.nlev = levels;
+    a.S = L.S;
+    a.Np = L.Np;
+    a.n2 = L.n2;
+    a.ld2 = L.ld2;
+    a.tr = h->tree();
+    a.z = z;
+    a.y = y;
+    a.D1 = sys->D1.p;
+    a.d2inv = d2inv;
+    a.epad = sys->epad.p + kEOFF;
+    a.xg = h->xg.p;
+    a.proj = h->proj.p;
+    a.cnt = h->cnt.p;
+    a.xrd = h->cnt.p + (size_t)2 * h->nnodes * CSTR;
+    a.skip = skip;
+    static const bool tracing = std::getenv("FI_HODLR_TRACE") != nullptr;
+    DevBuf<unsigned long long> trace;
+    a.trace = nullptr;
+    if (tracing) {
+        trace.alloc(8);
+        FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
+        a.trace = trace.p;
+    }
+    FI_CUDA(cudaMemsetAsync(h->cnt.p, 0, h->cnt.bytes(), ctx->stream));
+    void* args[] = {&a};
+    FI_CUDA(cudaLaunchCooperativeKernel((const void*)hodlr_sweep_kernel, dim3((unsigned)(L.Np / HR)), dim3(256), args,
+                                        smem, ctx->stream));
+    FI_LAUNCHED(ctx);
+    if (tracing) {
+        unsigned long long hv[8];
+        FI_CUDA(cudaMemcpyAsync(hv, trace.p, sizeof(hv), cudaMemcpyDeviceToHost, ctx->stream));
+        FI_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::fprintf(stderr,
+                     "[hodlr_sweep] kcycles/level: x %.2f | proj+release %.2f | history %.2f | wait %.2f | stage+sum %.2f | "
+                     "y %.2f | loop %.2f\n",
+                     hv[0] * 1e-3 / levels, hv[1] * 1e-3 / levels, hv[2] * 1e-3 / levels, hv[3] * 1e-3 / levels,
+                     hv[4] * 1e-3 / levels, hv[5] * 1e-3 / levels, hv[7] * 1e-3 / levels);
+    }
+}
+
+}  // namespace fib

@@ -779,4 +779,4 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
 
 }  // namespace fib
 
-fi_precond::~fi_precond() = default;
+fi_precond::~fi_precond() { fib::hodlr_destroy(hodlr); }
