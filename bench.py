@@ -290,10 +290,18 @@ def run_ours(args):
     y = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, n)).to(b_dev.device)
     out = torch.empty_like(y)
     ms = ctypes.c_double()
-    # P^{-1} (forward substitution + its refinement) is one persistent kernel: sweep_ir_kernel
+    form = P.form
+    if form == "hodlr":
+        # P^{-1} = HODLR sweep, K1 residual, HODLR correction sweep, axpy: the dominant kernel is the
+        # sweep, timed alone (refinement off = one hodlr_sweep_kernel launch)
+        P.set_refine(False)
+        assert lib.fi_precond_apply_timed(P.handle, y.data_ptr(), out.data_ptr(), reps, ctypes.byref(ms)) == 0
+        ms_sweep = ms.value
+        P.set_refine(True)
     assert lib.fi_precond_apply_timed(P.handle, y.data_ptr(), out.data_ptr(), reps, ctypes.byref(ms)) == 0
     ms_papply = ms.value
-    ms_sweep = ms_papply
+    if form != "hodlr":
+        ms_sweep = ms_papply  # packed tiles: sweep + refinement are one persistent kernel (sweep_ir_kernel)
     assert lib.fi_system_apply_timed(A.handle, y.data_ptr(), out.data_ptr(), reps, ctypes.byref(ms)) == 0
     ms_op = ms.value
 
@@ -301,11 +309,18 @@ def run_ours(args):
     Np = ((N + 63) // 64) * 64 if spec.sgrid.d == 1 else spec.sgrid.n[0] * ((spec.sgrid.n[1] + 63) // 64) * 64
     nb = Np // 64
     T = nb * (nb + 1) // 2
-    tile_bytes = 64 * 64 * (8 + 4)
-    # algorithmic bytes of one P^{-1} apply: the packed lower-triangular FP64
-    # and FP32 tiles of all S+1 levels once each, plus per level row z, D1, D2^-1 read twice, D2 once,
-    # y1 written and re-read once, y written, the FP32 correction written (10 doubles-equivalent)
-    sweep_bytes = (S + 1) * T * tile_bytes + 10 * 8 * Np * (S + 1)
+    if form == "hodlr":
+        # algorithmic bytes of one sweep: every level's HODLR rows once
+        # (fi_precond_bytes: 64 leaf + 32 per ancestor doubles per row) + z, D1, 1/D2 read, y written
+        sweep_bytes = int(P.device_bytes()) + 4 * 8 * Np * (S + 1)
+        sweep_kernel = "hodlr_sweep_kernel (K2: substitution over HODLR inverses; chain of S+1 dependent levels)"
+    else:
+        tile_bytes = 64 * 64 * (8 + 4)
+        # the packed lower-triangular FP64 and FP32 tiles of all S+1 levels once each, plus per level
+        # row z, D1, D2^-1 read twice, D2 once, y1 written and re-read once, y written, the FP32
+        # correction written (10 doubles-equivalent)
+        sweep_bytes = (S + 1) * T * tile_bytes + 10 * 8 * Np * (S + 1)
+        sweep_kernel = "sweep_ir_kernel (K2: FP64 substitution + FP32 refinement sweep)"
     hbm_peak, peak_src = load_peaks()
     achieved = sweep_bytes / (ms_sweep * 1e-3) / 1e9
     op_flops = 2.0 * N * N * (S + 1)
@@ -341,7 +356,8 @@ def run_ours(args):
                 "workload": NAMES[cfg],
                 "M": N, "N_t": S, "dim": n, "restart": RESTART, "tol": TOL[cfg], "precond": "block-triangular",
                 "noise": f"{NOISE[cfg] * 100:g}% gaussian rel-L2 seed {SEED_BASE + cfg}",
-                "l2": "inputs larger than L2 (each iteration streams ~52 GB of preconditioner tiles)",
+                "l2": ("each P apply streams the HODLR inverses twice (2 x %.1f GB, above L2)" % (P.device_bytes() / 1e9)
+                       if form == "hodlr" else "inputs larger than L2 (each iteration streams ~52 GB of tiles)"),
                 "parallelism": f"replicas x{ws}",
                 "recon_error_vs_fstar": recon_err,
                 "final_true_residual": rep.final_true_residual,
@@ -351,10 +367,11 @@ def run_ours(args):
             "e2e": {"value": round(e2e_value, 3), "unit": "iters/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "kernel": "sweep_ir_kernel (K2: FP64 substitution + FP32 refinement sweep)",
+            "roofline": {"bound": "hbm", "kernel": sweep_kernel,
                          "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": None,
                          "bytes_per_launch": sweep_bytes, "ms_per_launch": round(ms_sweep, 4),
+                         "us_per_level": round(ms_sweep * 1e3 / (S + 1), 3), "precond_form": form,
                          "peak_source": peak_src},
             "roofline_operator": {"bound": "tensor", "kernel": "toeplitz_apply_kernel (K1, FP64 DMMA)",
                                   "achieved": round(op_tflops, 3), "peak": FP64_DMMA_PEAK_TFLOPS,

@@ -120,6 +120,9 @@ int fi_precond_create(fi_system* sys, long long block_cap, fi_precond** out);
 int fi_precond_create_ex(fi_system* sys, long long block_cap, int inner, double tol, int maxit, fi_precond** out);
 /* 0 = dense inverses, 1 = tau-PCG per block. */
 int fi_precond_inner(const fi_precond* P);
+/* Storage of the dense inverses: 0 = packed 64x64 tiles (FP64 + FP32 copy), 1 = tau-PCG (no
+ * inverses), 2 = HODLR (64-row leaves, rank-32 off-diagonal blocks). */
+int fi_precond_form(const fi_precond* P);
 void fi_precond_destroy(fi_precond* P);
 /* y = P^{-1} z (forward block substitution), device vectors, async. */
 int fi_precond_apply(fi_precond* P, const double* z_dev, double* y_dev);

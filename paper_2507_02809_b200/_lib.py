@@ -87,6 +87,7 @@ _SIGS = {
     "fi_precond_create_ex": (ctypes.c_int, [c_void_p, ctypes.c_longlong, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                              ctypes.POINTER(c_void_p)]),
     "fi_precond_inner": (ctypes.c_int, [c_void_p]),
+    "fi_precond_form": (ctypes.c_int, [c_void_p]),
     "fi_build_rhs": (ctypes.c_int, [c_void_p, c_double_p, c_double_p, c_double_p]),
     "fi_forward_solve": (ctypes.c_int, [c_void_p, c_void_p, c_double_p, c_double_p, c_double_p, c_double_p]),
     "fi_gmres": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, ctypes.POINTER(GmresOpts),

@@ -324,6 +324,7 @@ int fi_precond_create_ex(fi_system* sys, long long block_cap, int inner, double 
 }
 
 int fi_precond_inner(const fi_precond* P) { return P ? P->mode : -1; }
+int fi_precond_form(const fi_precond* P) { return P ? (P->mode == 1 ? 1 : (P->hodlr ? 2 : 0)) : -1; }
 
 void fi_precond_destroy(fi_precond* P) {
     if (!P) return;

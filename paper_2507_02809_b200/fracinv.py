@@ -449,6 +449,11 @@ class BlockTriangularPreconditioner:
     def inner(self) -> str:
         return "pcg" if lib.fi_precond_inner(self.handle) == 1 else "lu"
 
+    @property
+    def form(self) -> str:
+        """Storage of the block inverses: "tiles" (packed FP64/FP32), "hodlr" or "pcg" (none)."""
+        return {0: "tiles", 1: "pcg", 2: "hodlr"}[lib.fi_precond_form(self.handle)]
+
     def dim(self) -> int:
         return self.A.dim()
 
