@@ -15,8 +15,8 @@
 //
 // Sweep (one persistent cooperative kernel, one CTA per 32 rows): per level, a CTA computes x of
 // its rows, publishes the partial projections V^T x / Q^T x of its rows for every ancestor node
-// (one release counter per node side), waits for the other sides' partials and its leaf sibling's
-// x, and forms y.  One cross-CTA hop per level; the whole y history of the CTA's rows stays in
+// (each value carries a level tag in its last mantissa bit, so readers poll the data itself), reads
+// the other sides' partials and its leaf sibling's x, and forms y.  One cross-CTA hop per level; the whole y history of the CTA's rows stays in
 // shared memory for the L1 time-convolution sums.
 #include <algorithm>
 #include <array>
@@ -35,31 +35,22 @@ constexpr int RK = 32;     // rank per node
 constexpr int HR = 32;     // rows per sweep CTA
 constexpr int HPART = 8;   // threads per row in the sweep: 2 leaf halves + up to 6 ancestor depths
 constexpr int DMAX = 6;    // tree depth supported (nb <= 64 leaves)
-constexpr int CSTR = kCounterStride;
 constexpr unsigned kSpin = 1u << 25;
 constexpr int PRS = HR * 33 + 1;  // per-depth stride of the projection products (doubles)
 constexpr int TVS = RK + 1;       // per-depth stride of the summed projections
 constexpr int YHS = HR + 1;       // per-level stride of the y history (the 8 threads of a row read 8 levels)
 
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+// Values exchanged between CTAs carry their own arrival signal: the least significant mantissa bit
+// holds the level tag ((level >> 1) & 1; buffers alternate by level parity), so a reader polls the
+// value itself — no counters, no release fences.  (Costs one ulp, 2.2e-16 relative.)
+__device__ __forceinline__ void st_tagged(double* p, double v, unsigned tag) {
+    const unsigned long long bits = ((unsigned long long)__double_as_longlong(v) & ~1ull) | tag;
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(bits) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_bits(const double* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
     return v;
-}
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void red_relaxed(unsigned* p, unsigned v) {
-    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void warp_wait(const unsigned* p, unsigned target) {
-    for (unsigned n = 0; !__all_sync(0xffffffffu, ld_relaxed(p) >= target); ++n) {
-        __nanosleep(64);
-        if (n == kSpin) __trap();
-    }
-    (void)ld_acquire(p);
 }
 
 // Tree tables (device): per depth d (1..D) and leaf block b: node id and side (0 = I, 1 = J, -1 none)
@@ -227,10 +218,8 @@ struct HArgs {
     const double* D1;
     const double* d2inv;
     const double* epad;  // epad[k] = e_k (0 <= k < S), zeros around
-    double* xg;          // [2][Np] x of the level (leaf siblings read it)
-    double* proj;        // [2][nnodes][2 sides][slots <= nb * 2][RK] partial projections
-    unsigned* cnt;       // [nnodes][2] release counters (stride CSTR)
-    unsigned* xrd;       // [nb] leaf x counters (stride CSTR)
+    double* xg;          // [2][Np] x of the level (leaf siblings read it), level-tagged
+    double* proj;        // [2][nnodes][2 sides][slots <= nb * 2][RK] partial projections, level-tagged
     const int* skip;
     unsigned long long* trace;  // optional [8]: per-phase time sums of CTA 0 (FI_HODLR_TRACE=1)
 };
@@ -241,7 +230,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int nlev = a.nlev, S = a.S, D = a.tr.D, nb = a.tr.nb;
     const long long Np = a.Np;
-    const int c = blockIdx.x, t = threadIdx.x, warp = t >> 5;
+    const int c = blockIdx.x, t = threadIdx.x;
     const int i = t >> 3, p = t & 7;
     const long long r0 = (long long)c * HR, r = r0 + i;
     const int b = (int)(r0 / TB);  // leaf block of the CTA (two CTAs per leaf)
@@ -298,7 +287,6 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     // the other sides' partials this thread stages each level: fixed offsets within a parity block
     constexpr int MAXE = (2 * 64 * RK + 255) / 256;  // <= 2 nb RK staged values / 256 threads
     int soff[MAXE];
-    double sv[MAXE];
 #pragma unroll
     for (int u = 0; u < MAXE; ++u) {
         const int e = t + u * 256;
@@ -339,6 +327,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     for (int lv = 0; lv < nlev; ++lv) {
         stamp(7);
         const int par = lv & 1;
+        const unsigned tag = (unsigned)(lv >> 1) & 1u;
         // ---- x of the CTA's rows
         if (p == 0) {
             double x = 0.0;
@@ -351,7 +340,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
                 }
             }
             xs[(r0 % TB) + i + (r0 % TB ? 1 : 0)] = x;
-            a.xg[(long long)par * Np + r] = x;
+            st_tagged(a.xg + (long long)par * Np + r, x, tag);
         }
         __syncthreads();
         stamp(0);
@@ -373,16 +362,8 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
                 double s = 0.0;
                 for (int ii = 0; ii < HR; ++ii) s += pd[ii * 33 + k];
                 const long long slotbase = (((long long)par * a.tr.nnodes + s_node[d]) * 2 + s_side[d]) * maxslots;
-                a.proj[(slotbase + s_slot[d]) * RK + k] = s;
+                st_tagged(a.proj + (slotbase + s_slot[d]) * RK + k, s, tag);
             }
-        }
-        __syncthreads();
-        if (t == 0) {
-            // one release fence for the CTA's partials and x, then relaxed increments
-            asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-            for (int d = 1; d <= D; ++d)
-                if (s_node[d] >= 0) red_relaxed(a.cnt + (s_node[d] * 2 + s_side[d]) * CSTR, 1u);
-            red_relaxed(a.xrd + b * CSTR, 1u);
         }
         stamp(1);
         // next level's coefficients: issued here, off the publish path, consumed at the level's end
@@ -405,26 +386,34 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
             if (p == 0) hs[i] = h;
         }
         stamp(2);
-        // ---- wait for the other sides' partials and the leaf sibling's x
-        if (warp >= 1 && warp <= D && s_node[warp] >= 0) {
-            const int d = warp;
-            warp_wait(a.cnt + (s_node[d] * 2 + (1 - s_side[d])) * CSTR, (unsigned)(s_nother[d] * (lv + 1)));
-        }
-        if (warp == 0) warp_wait(a.xrd + b * CSTR, (unsigned)((TB / HR) * (lv + 1)));
-        __syncthreads();
         stamp(3);
-        // ---- stage the other sides' partials (all loads in flight), the sibling half of x
+        // ---- the other sides' partials and the leaf sibling's x: load all, re-poll the ones whose
+        // level tag is not current yet
         {
             const long long pbase = (long long)par * a.tr.nnodes * 2 * maxslots * RK;
+            unsigned long long bv[MAXE];
+            unsigned long long xb = 0;
+            const long long rr = (long long)b * TB + t;
+            const bool xsib = t < TB && (rr < r0 || rr >= r0 + HR);
 #pragma unroll
-            for (int u = 0; u < MAXE; ++u) sv[u] = soff[u] >= 0 ? __ldcg(a.proj + pbase + soff[u]) : 0.0;
+            for (int u = 0; u < MAXE; ++u) bv[u] = soff[u] >= 0 ? ld_bits(a.proj + pbase + soff[u]) : tag;
+            if (xsib) xb = ld_bits(a.xg + (long long)par * Np + rr);
+            for (unsigned n = 0;; ++n) {
+                bool ok = !xsib || (unsigned)(xb & 1ull) == tag;
+#pragma unroll
+                for (int u = 0; u < MAXE; ++u) ok = ok && (unsigned)(bv[u] & 1ull) == tag;
+                if (ok) break;
+                __nanosleep(32);
+                if (n == kSpin) __trap();
+#pragma unroll
+                for (int u = 0; u < MAXE; ++u)
+                    if (soff[u] >= 0 && (unsigned)(bv[u] & 1ull) != tag) bv[u] = ld_bits(a.proj + pbase + soff[u]);
+                if (xsib && (unsigned)(xb & 1ull) != tag) xb = ld_bits(a.xg + (long long)par * Np + rr);
+            }
 #pragma unroll
             for (int u = 0; u < MAXE; ++u)
-                if (soff[u] >= 0) stage[t + u * 256] = sv[u];
-        }
-        if (t < TB) {
-            const long long rr = (long long)b * TB + t;
-            if (rr < r0 || rr >= r0 + HR) xs[t + (t >= 32 ? 1 : 0)] = __ldcg(a.xg + (long long)par * Np + rr);
+                if (soff[u] >= 0) stage[t + u * 256] = __longlong_as_double((long long)bv[u]);
+            if (xsib) xs[t + (t >= 32 ? 1 : 0)] = __longlong_as_double((long long)xb);
         }
         __syncthreads();
         if (t < D * RK) {
@@ -543,7 +532,6 @@ struct HodlrData {
     std::vector<int> depth_off, depth_cnt;  // nodes of each depth in nodes_by_depth
     DevBuf<double2> hd;                     // [levels][Np/32][16][256]
     DevBuf<double> proj, xg;
-    DevBuf<unsigned> cnt;
     Tree tree() const {
         return Tree{D, nb, nnodes, rb_node.p, rb_side.p, lo.p, mid.p, hi.p};
     }
@@ -608,7 +596,6 @@ HodlrData* hodlr_create(const Layout& L, int levels) {
     h->hd.alloc((size_t)levels * (L.Np / HR) * (RK / 2) * 256);
     h->proj.alloc((size_t)2 * h->nnodes * 2 * (2 * nb) * RK);
     h->xg.alloc((size_t)2 * L.Np);
-    h->cnt.alloc((size_t)(2 * h->nnodes + nb) * CSTR);
     return h;
 }
 
@@ -686,8 +673,6 @@ void hodlr_sweep(fi_ctx* ctx, HodlrData* h, const fi_system* sys, const double* 
     a.epad = sys->epad.p + kEOFF;
     a.xg = h->xg.p;
     a.proj = h->proj.p;
-    a.cnt = h->cnt.p;
-    a.xrd = h->cnt.p + (size_t)2 * h->nnodes * CSTR;
     a.skip = skip;
     static const bool tracing = std::getenv("FI_HODLR_TRACE") != nullptr;
     DevBuf<unsigned long long> trace;
@@ -697,7 +682,8 @@ void hodlr_sweep(fi_ctx* ctx, HodlrData* h, const fi_system* sys, const double* 
         FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
         a.trace = trace.p;
     }
-    FI_CUDA(cudaMemsetAsync(h->cnt.p, 0, h->cnt.bytes(), ctx->stream));
+    FI_CUDA(cudaMemsetAsync(h->proj.p, 0xff, h->proj.bytes(), ctx->stream));
+    FI_CUDA(cudaMemsetAsync(h->xg.p, 0xff, h->xg.bytes(), ctx->stream));
     void* args[] = {&a};
     FI_CUDA(cudaLaunchCooperativeKernel((const void*)hodlr_sweep_kernel, dim3((unsigned)(L.Np / HR)), dim3(256), args,
                                         smem, ctx->stream));
