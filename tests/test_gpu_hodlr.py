@@ -1,0 +1,63 @@
+"""GPU tests of the HODLR form of the dense-block inverses (precond_hodlr.cu): which shapes use it,
+and parity of P^{-1} against the packed-tile form (FI_HODLR=0, a separate process) and the oracle."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import fracinv_oracle as O
+from paper_2507_02809_b200.configs import baseline_problem
+
+pytestmark = pytest.mark.gpu
+F = pytest.importorskip("paper_2507_02809_b200.fracinv")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_CHILD = r"""
+import os, sys, numpy as np
+sys.path.insert(0, os.environ["ROOT"])
+from paper_2507_02809_b200 import fracinv as F
+from paper_2507_02809_b200.configs import baseline_problem
+A = F.SystemOperator(baseline_problem(F, int(os.environ["CFG"])))
+P = F.BlockTriangularPreconditioner(A)
+z = np.random.default_rng(3).uniform(-1, 1, A.dim())
+P.set_refine(False)
+y0 = P.apply(z)
+P.set_refine(True)
+y1 = P.apply(z)
+np.savez(os.environ["OUT"], y0=y0, y1=y1, z=z, form=P.form)
+"""
+
+
+def _run(cfg, hodlr, tmp_path):
+    out = str(tmp_path / f"p{cfg}_{hodlr}.npz")
+    env = dict(os.environ, FI_HODLR=str(hodlr), CFG=str(cfg), OUT=out, ROOT=ROOT)
+    subprocess.run([sys.executable, "-c", _CHILD], env=env, check=True, timeout=600)
+    return np.load(out)
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_hodlr_matches_tiles_and_oracle(cfg, tmp_path):
+    h, t = _run(cfg, 1, tmp_path), _run(cfg, 0, tmp_path)
+    assert str(h["form"]) == "hodlr" and str(t["form"]) == "tiles"
+    rel = float(np.linalg.norm(h["y1"] - t["y1"]) / np.linalg.norm(t["y1"]))
+    Ao = O.SystemOperator(baseline_problem(O, cfg))
+    z = h["z"]
+    bwd = float(np.linalg.norm(Ao.apply_precond_matrix(h["y1"]) - z) / np.linalg.norm(z))
+    print(f"config{cfg}: HODLR vs tiles {rel:.3e}, backward error {bwd:.3e}")
+    assert rel <= 1e-11 and bwd <= 1e-12
+
+
+def test_hodlr_form_selection():
+    # 1D with >= 2 leaves -> HODLR; one leaf -> tiles; 2D dense blocks fail the rank-32 probe -> tiles
+    A1 = F.SystemOperator(baseline_problem(F, 0))
+    assert F.BlockTriangularPreconditioner(A1).form == "hodlr"
+    small = F.make_problem("paper1d", 0.5, 1.5, [32], 8, 5e-3, 0.01)
+    assert F.BlockTriangularPreconditioner(F.SystemOperator(small)).form == "tiles"
+    grid = F.SpaceGrid([15, 15], [0.0, 0.0], [1.0, 1.0])
+    X = grid.nodes()
+    spec2 = F.make_custom_problem(F.FractionalOrders(0.3, 1.2), grid, 8, 1.0, lambda X, t: 1 + X[:, 0] * X[:, 1],
+                                  lambda X, t: 1 + X[:, 0] * (1 + t), lambda t: 1 + t * t, np.zeros(X.shape[0]),
+                                  np.sin(np.pi * X[:, 0]) * np.sin(np.pi * X[:, 1]), 1e-3, 0.01)
+    assert F.BlockTriangularPreconditioner(F.SystemOperator(spec2), inner="lu").form == "tiles"
