@@ -359,14 +359,23 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
             const int d = t / RK + 1, k = t % RK;
             if (s_node[d] >= 0) {
                 const double* pd = pr + (d - 1) * PRS;
-                double s = 0.0;
-                for (int ii = 0; ii < HR; ++ii) s += pd[ii * 33 + k];
+                double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int ii = 0; ii < HR; ++ii) s4[ii & 3] += pd[ii * 33 + k];
+                const double s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
                 const long long slotbase = (((long long)par * a.tr.nnodes + s_node[d]) * 2 + s_side[d]) * maxslots;
                 st_tagged(a.proj + (slotbase + s_slot[d]) * RK + k, s, tag);
             }
         }
         stamp(1);
-        // next level's coefficients: issued here, off the publish path, consumed at the level's end
+        // next level's coefficients: issued here, off the publish path, consumed at the level's end;
+        // the level after that is pulled into L2 now, so these register loads hit L2
+        if (lv + 2 < nlev) {
+            const char* pf = reinterpret_cast<const char*>(a.hd + (long long)(lv + 2) * lvstride +
+                                                           (long long)c * (RK / 2) * 256);
+            for (int q = t; q < (RK / 2) * 256 * 16 / 128; q += blockDim.x)
+                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pf + (long long)q * 128));
+        }
         if (lv + 1 < nlev) load_level(lv + 1, nxt);
         load_coef(lv + 1, nz, nd1, ndi);
         // ---- history of the next level (rows' y up to lv - 1): sum_{m <= lv-1} e_{lv+1-m} y_m
@@ -419,8 +428,16 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         if (t < D * RK) {
             const int d = t / RK + 1, k = t % RK;
             double s4[4] = {0.0, 0.0, 0.0, 0.0};
-            if (s_node[d] >= 0)
-                for (int j = 0; j < s_nother[d]; ++j) s4[j & 3] += stage[s_ooff[d] + j * RK + k];
+            if (s_node[d] >= 0) {
+                const double* st = stage + s_ooff[d] + k;
+                const int no = s_nother[d];
+                int j = 0;
+                for (; j + 4 <= no; j += 4) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) s4[u] += st[(j + u) * RK];
+                }
+                for (; j < no; ++j) s4[j & 3] += st[j * RK];
+            }
             tvec[(d - 1) * TVS + k] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
         }
         __syncthreads();
