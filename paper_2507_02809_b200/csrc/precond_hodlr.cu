@@ -284,6 +284,14 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
 #pragma unroll
         for (int k2 = 0; k2 < RK / 2; ++k2) dst[k2] = __ldg(src + k2 * 256 + t);
     };
+    // the next level's coefficients in four groups at different points of the level, so that the
+    // loads (L2 hits after the prefetch) never throttle a warp's issue
+    auto load_quarter = [&](int lv, int q) {
+        if (lv >= nlev) return;
+        const double2* src = a.hd + (long long)lv * lvstride + (long long)c * (RK / 2) * 256;
+#pragma unroll
+        for (int k2 = 4 * q; k2 < 4 * q + 4; ++k2) nxt[k2] = __ldg(src + k2 * 256 + t);
+    };
     // the other sides' partials this thread stages each level: fixed offsets within a parity block
     constexpr int MAXE = (2 * 64 * RK + 255) / 256;  // <= 2 nb RK staged values / 256 threads
     int soff[MAXE];
@@ -344,6 +352,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         }
         __syncthreads();
         stamp(0);
+        load_quarter(lv + 1, 0);
         // ---- partial projections of the CTA's rows for every ancestor node
         if (p >= 2 && p - 1 <= D && s_node[p - 1] >= 0) {
             const double xv = xs[(r0 % TB) + i + (r0 % TB ? 1 : 0)];
@@ -376,7 +385,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
             for (int q = t; q < (RK / 2) * 256 * 16 / 128; q += blockDim.x)
                 asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pf + (long long)q * 128));
         }
-        if (lv + 1 < nlev) load_level(lv + 1, nxt);
+        load_quarter(lv + 1, 1);
         load_coef(lv + 1, nz, nd1, ndi);
         // ---- history of the next level (rows' y up to lv - 1): sum_{m <= lv-1} e_{lv+1-m} y_m
         {
@@ -396,6 +405,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         }
         stamp(2);
         stamp(3);
+        load_quarter(lv + 1, 2);
         // ---- the other sides' partials and the leaf sibling's x: load all, re-poll the ones whose
         // level tag is not current yet
         {
@@ -442,6 +452,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         }
         __syncthreads();
         stamp(4);
+        load_quarter(lv + 1, 3);
         // ---- y of the CTA's rows: leaf product + low-rank terms, 8 threads per row
         double part = 0.0;
         if (p < 2) {
