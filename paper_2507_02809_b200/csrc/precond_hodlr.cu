@@ -242,9 +242,8 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     double* pr = yh + (long long)nlev * YHS;       // DMAX x PRS products (row i, k) at i * 33 + k
     double* stage = pr + DMAX * PRS;               // partial projections of the other sides
     double* tvec = stage + 2 * nb * RK;            // DMAX x TVS summed projections
-    double* xs = tvec + DMAX * TVS;                // 64 (+1): x of the leaf block, halves at 0 and 33
-    double* hs = xs + TB + 2;                      // 32: history sums of the next level
-    double* es = hs + HR;                          // nlev + 2: L1 weights e_0.. (history sums)
+    double* xsb = tvec + DMAX * TVS;               // 2 x 66: x of the leaf block, halves at 0 and 33, by level parity
+    double* es = xsb + 2 * (TB + 2);               // nlev + 2: L1 weights e_0.. (history sums)
     // per-depth node, side, slot, and the other side's CTA count
     __shared__ int s_node[DMAX + 1], s_side[DMAX + 1], s_slot[DMAX + 1], s_nother[DMAX + 1], s_ooff[DMAX + 2];
     if (t <= DMAX) {
@@ -308,6 +307,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     }
     load_level(0, cur);
     double hnext = 0.0;  // (p == 0) history sum of the current level's x numerator
+    double hsum = 0.0, xrow = 0.0;
     // (p == 0) z, D1, 1/D2 of the row for level lv, loaded one level ahead
     auto load_coef = [&](int lv, double& cz, double& cd1, double& cdi) {
         cz = cd1 = cdi = 0.0;
@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         stamp(7);
         const int par = lv & 1;
         const unsigned tag = (unsigned)(lv >> 1) & 1u;
+        double* xs = xsb + par * (TB + 2);
         // ---- x of the CTA's rows
         if (p == 0) {
             double x = 0.0;
@@ -349,13 +350,15 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
             }
             xs[(r0 % TB) + i + (r0 % TB ? 1 : 0)] = x;
             st_tagged(a.xg + (long long)par * Np + r, x, tag);
+            xrow = x;
         }
-        __syncthreads();
+        // x of the row to its 8 threads (no block barrier: the row's threads share a warp)
+        xrow = __shfl_sync(0xffffffffu, xrow, (t & 31) & ~7);
         stamp(0);
         load_quarter(lv + 1, 0);
         // ---- partial projections of the CTA's rows for every ancestor node
         if (p >= 2 && p - 1 <= D && s_node[p - 1] >= 0) {
-            const double xv = xs[(r0 % TB) + i + (r0 % TB ? 1 : 0)];
+            const double xv = xrow;
             double* pd = pr + (p - 2) * PRS + i * 33;
 #pragma unroll
             for (int k2 = 0; k2 < RK / 2; ++k2) {
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
             h += __shfl_xor_sync(0xffffffffu, h, 1);
             h += __shfl_xor_sync(0xffffffffu, h, 2);
             h += __shfl_xor_sync(0xffffffffu, h, 4);
-            if (p == 0) hs[i] = h;
+            hsum = h;  // (all 8 threads of the row hold the sum)
         }
         stamp(2);
         stamp(3);
@@ -471,9 +474,8 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
             const double yv = prow ? 0.0 : part;
             yh[lv * YHS + i] = yv;
             a.y[(long long)lv * Np + r] = yv;
-            hnext = hs[i];
+            hnext = hsum;
         }
-        __syncthreads();
         stamp(5);
 #pragma unroll
         for (int k2 = 0; k2 < RK / 2; ++k2) cur[k2] = nxt[k2];
@@ -547,7 +549,7 @@ __global__ void hodlr_check_apply(const double* W, const double2* hd, long long 
 }
 
 size_t hodlr_sweep_smem(int nlev, int nb) {
-    return ((size_t)nlev * YHS + DMAX * PRS + 2 * (size_t)nb * RK + DMAX * TVS + TB + 2 + HR + nlev + 2) *
+    return ((size_t)nlev * YHS + DMAX * PRS + 2 * (size_t)nb * RK + DMAX * TVS + 2 * (TB + 2) + nlev + 2) *
            sizeof(double);
 }
 
