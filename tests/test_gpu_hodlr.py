@@ -49,6 +49,37 @@ def test_hodlr_matches_tiles_and_oracle(cfg, tmp_path):
     assert rel <= 1e-11 and bwd <= 1e-12
 
 
+_CHILD_PAPER = r"""
+import os, sys, numpy as np
+sys.path.insert(0, os.environ["ROOT"])
+from paper_2507_02809_b200 import fracinv as F
+beta, omega = float(os.environ["BETA"]), float(os.environ["OMEGA"])
+A = F.SystemOperator(F.make_problem("paper1d", beta, omega, [1023], 48, 5e-3, 0.01))
+P = F.BlockTriangularPreconditioner(A)
+z = np.random.default_rng(4).uniform(-1, 1, A.dim())
+np.savez(os.environ["OUT"], y=P.apply(z), z=z, form=P.form)
+"""
+
+
+@pytest.mark.parametrize("beta,omega", [(0.1, 1.9), (0.5, 1.5), (0.9, 1.1)])
+def test_hodlr_paper_orders(beta, omega, tmp_path):
+    """The reference's three (beta, omega) pairs at n = 1023 (16 leaves): the rank-32 probe passes
+    and P^{-1} keeps its parity with the packed tiles and the oracle."""
+    res = {}
+    for flag in (1, 0):
+        out = str(tmp_path / f"o{flag}.npz")
+        env = dict(os.environ, FI_HODLR=str(flag), BETA=str(beta), OMEGA=str(omega), OUT=out, ROOT=ROOT)
+        subprocess.run([sys.executable, "-c", _CHILD_PAPER], env=env, check=True, timeout=600)
+        res[flag] = np.load(out)
+    assert str(res[1]["form"]) == "hodlr"
+    rel = float(np.linalg.norm(res[1]["y"] - res[0]["y"]) / np.linalg.norm(res[0]["y"]))
+    Ao = O.SystemOperator(O.make_problem("paper1d", beta, omega, [1023], 48, 5e-3, 0.01))
+    z = res[1]["z"]
+    bwd = float(np.linalg.norm(Ao.apply_precond_matrix(res[1]["y"]) - z) / np.linalg.norm(z))
+    print(f"(beta, omega) = ({beta}, {omega}): HODLR vs tiles {rel:.3e}, backward error {bwd:.3e}")
+    assert rel <= 1e-11 and bwd <= 1e-12
+
+
 def test_hodlr_form_selection():
     # 1D with >= 2 leaves -> HODLR; one leaf -> tiles; 2D dense blocks fail the rank-32 probe -> tiles
     A1 = F.SystemOperator(baseline_problem(F, 0))
