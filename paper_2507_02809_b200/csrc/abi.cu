@@ -133,6 +133,9 @@ int fi_ctx_create(int device, fi_ctx** out) {
         FI_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         FI_CUDA(cudaEventCreate(&c->ev0));
         FI_CUDA(cudaEventCreate(&c->ev1));
+        FI_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        FI_CUDA(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+        FI_CUDA(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
         *out = c;
     });
 }
@@ -142,6 +145,9 @@ void fi_ctx_destroy(fi_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
+    cudaEventDestroy(ctx->fork);
+    cudaEventDestroy(ctx->join);
+    cudaStreamDestroy(ctx->side);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

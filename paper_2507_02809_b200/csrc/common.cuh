@@ -106,6 +106,9 @@ struct fi_ctx {
     cudaStream_t stream = nullptr;
     long long launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // side stream for independent work that overlaps a main-stream kernel (fork/join events)
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 // --------------------------------------------------------------------------- kernels (launchers)

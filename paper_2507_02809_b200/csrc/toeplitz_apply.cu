@@ -83,7 +83,7 @@ __device__ __forceinline__ void load_stage(const OperatorView& op, const double*
         for (int c = tid; c < BN * BK / 2; c += NTHREADS) {
             const int sl = c / (BK / 2), jp = c % (BK / 2);
             const int s = tc.s0 + sl;
-            const bool valid = s <= op.S;
+            const bool valid = s < op.S;
             const double* src = valid ? U + (long long)s * op.Np + j0 + 2 * jp : U;
             cp_async16(stage + sl * LDJ + 2 * jp, src, valid);
         }
@@ -117,8 +117,9 @@ toeplitz_apply_kernel(OperatorView op, const double* __restrict__ U, double* __r
     const int g = lane >> 2, t = lane & 3;
     const int wm0 = (warp & 1) * 32;
     const int wn0 = (warp >> 1) * 16;
-    // warps whose 16 columns are all virtual (beyond the f column) skip the math
-    const bool active = tc.s0 + wn0 <= op.S;
+    // warps whose 16 columns are all virtual (beyond the last time level) skip the math; the f
+    // column is done by fcol_kernel (a 64-wide tile for that one column would cost a full tile)
+    const bool active = tc.s0 + wn0 < op.S;
 
     double acc1[4][2][2], acc2[4][2][2];
 #pragma unroll
@@ -197,7 +198,7 @@ toeplitz_apply_kernel(OperatorView op, const double* __restrict__ U, double* __r
     for (int idx = threadIdx.x; idx < BM * BN; idx += NTHREADS) {
         const int sl = idx / BM, il = idx % BM;
         const int s = tc.s0 + sl;
-        if (s > op.S) break;  // idx increases with s
+        if (s >= op.S) break;  // idx increases with s
         const long long i = tc.i0 + il;
         const long long o = (long long)s * Np + i;
         double out;
@@ -215,6 +216,56 @@ toeplitz_apply_kernel(OperatorView op, const double* __restrict__ U, double* __r
     }
 }
 
+// f column: Z[:, S] = y^(S) + cr D2_S o (K f)   (minus_from: Z = minus_from - that).  K f is one
+// matrix-vector product (N^2 FMAs): CUDA cores, one CTA per 64 output rows, the generating-vector
+// segment and a chunk of f staged in shared memory; 4 threads per row split each chunk.
+constexpr int FC = 256;  // f chunk per stage
+__global__ void __launch_bounds__(256) fcol_kernel(OperatorView op, const double* __restrict__ U,
+                                                   double* __restrict__ Z, const int* skip,
+                                                   const double* __restrict__ minus_from) {
+    if (skip && *skip) return;
+    __shared__ double fseg[FC];
+    __shared__ double gseg[FC + BM];
+    __shared__ double red[4][BM];
+    const long long Np = op.Np;
+    const long long i0 = (long long)blockIdx.x * BM;
+    const int i1 = (int)(i0 / op.ld2), i2_0 = (int)(i0 % op.ld2);
+    const int r = threadIdx.x & (BM - 1), part = threadIdx.x >> 6;
+    const double* f = U + (long long)op.S * Np;
+    double acc = 0.0;
+    for (int j1 = 0; j1 < op.n1; ++j1) {
+        const double* grow = op.gen + (long long)(i1 - j1 + op.n1 - 1) * op.gen_stride + op.ld2;
+        for (int j0 = 0; j0 < op.n2; j0 += FC) {
+            const int nc = min(FC, op.n2 - j0);
+            __syncthreads();
+            for (int q = threadIdx.x; q < FC; q += blockDim.x) fseg[q] = q < nc ? f[(long long)j1 * op.ld2 + j0 + q] : 0.0;
+            // gseg[x] = a[i2_0 - j0 - (FC - 1) + x]: row r, column c -> gseg[r - c + FC - 1]
+            for (int q = threadIdx.x; q < FC + BM; q += blockDim.x) {
+                const int l2 = i2_0 - j0 - (FC - 1) + q;
+                gseg[q] = (l2 > -op.n2 && l2 < op.n2) ? grow[l2] : 0.0;
+            }
+            __syncthreads();
+            double a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+            for (int cc = part; cc < FC; cc += 4) a4[cc & 3] += gseg[r - cc + FC - 1] * fseg[cc];
+            acc += (a4[0] + a4[1]) + (a4[2] + a4[3]);
+        }
+    }
+    red[part][r] = acc;
+    __syncthreads();
+    if (threadIdx.x < BM) {
+        const double kf = (red[0][r] + red[1][r]) + (red[2][r] + red[3][r]);
+        const long long i = i0 + r;
+        const long long o = (long long)op.S * Np + i;
+        double out = 0.0;
+        if (i2_0 + r < op.n2) {
+            const long long dl = (long long)(op.S - 1) * Np + i;
+            out = U[dl] + op.cr * op.D2[dl] * kf;
+        }
+        Z[o] = minus_from ? minus_from[o] - out : out;
+    }
+}
+
 }  // namespace
 
 void toeplitz_apply(fi_ctx* ctx, const OperatorView& op, const double* U, double* Z, const int* skip,
@@ -224,10 +275,17 @@ void toeplitz_apply(fi_ctx* ctx, const OperatorView& op, const double* U, double
         FI_CUDA(cudaFuncSetAttribute(toeplitz_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         configured = true;
     }
-    dim3 grid((unsigned)(op.Np / BM), (unsigned)((op.S + 1 + BN - 1) / BN));
+    // the f column (fcol_kernel) on the side stream, overlapping the time-level GEMM
+    FI_CUDA(cudaEventRecord(ctx->fork, ctx->stream));
+    FI_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));
+    fcol_kernel<<<(unsigned)(op.Np / BM), 256, 0, ctx->side>>>(op, U, Z, skip, minus_from);
+    FI_LAUNCHED(ctx);
+    FI_CUDA(cudaEventRecord(ctx->join, ctx->side));
+    dim3 grid((unsigned)(op.Np / BM), (unsigned)((op.S + BN - 1) / BN));
     toeplitz_apply_kernel<<<grid, NTHREADS, SMEM_BYTES, ctx->stream>>>(op, U, Z, skip, minus_from,
                                                                          precond_matrix ? 1 : 0);
     FI_LAUNCHED(ctx);
+    FI_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join, 0));
 }
 
 }  // namespace fib
