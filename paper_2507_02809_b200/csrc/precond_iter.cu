@@ -205,6 +205,7 @@ struct FusedCtl {
     int rpc;    // rows per CTA in the row passes (G * rpc >= n1)
     int cbf;    // columns per CTA in the column passes (power of two, cbf * L1 <= 8 * 256)
     int lgcbf;
+    int cbt, lgcbt;  // the same for the tau column pass (n2 columns instead of L2)
 };
 __device__ __forceinline__ unsigned long long gtime_ns() {
     unsigned long long t;
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
     const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
     const long long Np = a.Np;
-    const int rpc = ctl.rpc, cbf = ctl.cbf, lgc = ctl.lgcbf;
+    const int rpc = ctl.rpc, cbf = ctl.cbf, lgc = ctl.lgcbf, cbt = ctl.cbt, lgt = ctl.lgcbt;
     unsigned target = 0;
     int rk = 0;
     unsigned long long tlast = 0;
@@ -331,17 +332,17 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
     // column pass of the tau solve: DST along columns, divide by the tau eigenvalues, DST back
     auto tau_cols_phase = [&](int lv) {
         const double c = level_c(a, lv), dmean = level_dmean(a, lv);
-        const int ngroups = (a.n2 + cbf - 1) / cbf;
+        const int ngroups = (a.n2 + cbt - 1) / cbt;
         for (int g = cta; g < ngroups; g += G) {
-            const int k0 = g * cbf, nc = min(cbf, a.n2 - k0);
+            const int k0 = g * cbt, nc = min(cbt, a.n2 - k0);
             // the tau eigenvalues of the element each thread divides later are loaded with the data
             double ilam[8];
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 const int q = tid + t * nthr;
-                const int cc = q & (cbf - 1), j = q >> lgc;  // column fastest: adjacent loads
+                const int cc = q & (cbt - 1), j = q >> lgt;  // column fastest: adjacent loads
                 ilam[t] = 0.0;
-                if (q < cbf * a.L1) {
+                if (q < cbt * a.L1) {
                     double val = 0.0;
                     if (cc < nc) {
                         int k = -1;
@@ -358,13 +359,13 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                 }
             }
             __syncthreads();
-            double2* U = fft4_smem(u, v, cbf, a.L1, a.lg1, tws1, false, tid, nthr);
+            double2* U = fft4_smem(u, v, cbt, a.L1, a.lg1, tws1, false, tid, nthr);
             double2* W = U == u ? v : u;
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 const int q = tid + t * nthr;
-                if (q < cbf * a.L1) {
-                    const int cc = q & (cbf - 1), j = q >> lgc;
+                if (q < cbt * a.L1) {
+                    const int cc = q & (cbt - 1), j = q >> lgt;
                     double val = 0.0;
                     if (cc < nc) {
                         int k = -1;
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
             }
             __syncthreads();
             double2* V = W == u ? v : u;
-            const double2* R = fft4_smem(W, V, cbf, a.L1, a.lg1, tws1, false, tid, nthr);
+            const double2* R = fft4_smem(W, V, cbt, a.L1, a.lg1, tws1, false, tid, nthr);
             for (int q = tid; q < nc * a.n1; q += nthr) {
                 const int cc = q % nc, k = q / nc;
                 a.Rr[(long long)k * a.n2 + k0 + cc] = sc1 * R[cc * a.L1 + k + 1].y;
@@ -758,7 +759,12 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
         }
         int lgc = 0;
         while ((1 << lgc) < cbf) ++lgc;
-        FusedCtl ctl{P->it_fbar.p, P->it_fparts.p, tracing ? trace.p : nullptr, rpc, cbf, lgc};
+        int cbt = 1, lgt = 0;  // tau column pass: n2 columns over the grid
+        while (cbt * G < a.n2 && cbt < cbf) {
+            cbt *= 2;
+            ++lgt;
+        }
+        FusedCtl ctl{P->it_fbar.p, P->it_fparts.p, tracing ? trace.p : nullptr, rpc, cbf, lgc, cbt, lgt};
         FI_CUDA(cudaMemsetAsync(P->it_fbar.p, 0, sizeof(unsigned), ctx->stream));
         void* args[] = {&a, &ctl};
         FI_CUDA(cudaLaunchCooperativeKernel((const void*)tau_pcg_fused, dim3(P->it_fgrid), dim3(256), args, smem,
