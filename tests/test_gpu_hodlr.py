@@ -92,3 +92,12 @@ def test_hodlr_form_selection():
                                   lambda X, t: 1 + X[:, 0] * (1 + t), lambda t: 1 + t * t, np.zeros(X.shape[0]),
                                   np.sin(np.pi * X[:, 0]) * np.sin(np.pi * X[:, 1]), 1e-3, 0.01)
     assert F.BlockTriangularPreconditioner(F.SystemOperator(spec2), inner="lu").form == "tiles"
+
+
+def test_hodlr_apply_is_bit_reproducible():
+    # fixed-order reductions and level-tagged exchange: two applies give identical bits
+    A = F.SystemOperator(baseline_problem(F, 0))
+    P = F.BlockTriangularPreconditioner(A)
+    z = np.random.default_rng(8).uniform(-1, 1, A.dim())
+    y1, y2 = P.apply(z), P.apply(z)
+    assert P.form == "hodlr" and np.array_equal(y1, y2)
