@@ -36,9 +36,13 @@ constexpr int HR = 32;     // rows per sweep CTA
 constexpr int HPART = 8;   // threads per row in the sweep: 2 leaf halves + up to 6 ancestor depths
 constexpr int DMAX = 6;    // tree depth supported (nb <= 64 leaves)
 constexpr unsigned kSpin = 1u << 25;
-constexpr int PRS = HR * 33 + 1;  // per-depth stride of the projection products (doubles)
+constexpr int PRS = HR * 33 + 2;  // per-depth stride of the projection products (doubles; = 2 mod 16:
+                                  // the 12 writers of a half-warp, 6 depths x 2 rows, hit distinct banks)
 constexpr int TVS = RK + 1;       // per-depth stride of the summed projections
-constexpr int YHS = HR + 1;       // per-level stride of the y history (the 8 threads of a row read 8 levels)
+constexpr int YHS = HR;           // per-level stride of the y history
+// y history slot of (level m, row i): rows XOR-swizzled by level so that a half-warp (2 rows x 8
+// consecutive levels) of the history sum hits 16 distinct 8-byte bank pairs
+__device__ __forceinline__ int yhs(int m, int i) { return m * YHS + (i ^ ((m & 7) << 1)); }
 
 // Values exchanged between CTAs carry their own arrival signal: the least significant mantissa bit
 // holds the level tag ((level >> 1) & 1; buffers alternate by level parity), so a reader polls the
@@ -324,6 +328,8 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     };
     double cz, cd1, cdi, nz, nd1, ndi;
     load_coef(0, cz, cd1, cdi);
+    // (each stamp is a global read-modify-write of one thread: the phase after it carries its latency;
+    // register accumulators would cost the kernel spills)
     unsigned long long tl = 0;
     auto stamp = [&](int ph) {
         if (a.trace && blockIdx.x == 0 && t == 0) {
@@ -342,10 +348,10 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
             double x = 0.0;
             if (!prow) {
                 if (lv < S) {
-                    const double hist = (lv >= 2 ? hnext : 0.0) + (lv >= 1 ? e1 * yh[(lv - 1) * YHS + i] : 0.0);
+                    const double hist = (lv >= 2 ? hnext : 0.0) + (lv >= 1 ? e1 * yh[yhs(lv - 1, i)] : 0.0);
                     x = (cz - cd1 * hist) * cdi;
                 } else {
-                    x = (cz - yh[(S - 1) * YHS + i]) * cdi;
+                    x = (cz - yh[yhs(S - 1, i)]) * cdi;
                 }
             }
             xs[(r0 % TB) + i + (r0 % TB ? 1 : 0)] = x;
@@ -397,8 +403,8 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
                 int m = p;
                 for (; m + 3 * HPART <= lv - 1; m += 4 * HPART)
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) h4[u] += es[lv + 1 - m - u * HPART] * yh[(m + u * HPART) * YHS + i];
-                for (; m <= lv - 1; m += HPART) h4[0] += es[lv + 1 - m] * yh[m * YHS + i];
+                    for (int u = 0; u < 4; ++u) h4[u] += es[lv + 1 - m - u * HPART] * yh[yhs(m + u * HPART, i)];
+                for (; m <= lv - 1; m += HPART) h4[0] += es[lv + 1 - m] * yh[yhs(m, i)];
             }
             double h = (h4[0] + h4[1]) + (h4[2] + h4[3]);
             h += __shfl_xor_sync(0xffffffffu, h, 1);
@@ -457,22 +463,25 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         stamp(4);
         load_quarter(lv + 1, 3);
         // ---- y of the CTA's rows: leaf product + low-rank terms, 8 threads per row
-        double part = 0.0;
-        if (p < 2) {
+        // (one branch-free loop for both kinds of part, four independent FMA chains)
+        double part;
+        {
+            const bool act = p < 2 || (p - 1 <= D && s_node[p - 1] >= 0);
+            const double* src = p < 2 ? xs + 33 * p : tvec + (p - 2) * TVS;
+            double q4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int k2 = 0; k2 < RK / 2; ++k2)
-                part += cur[k2].x * xs[33 * p + 2 * k2] + cur[k2].y * xs[33 * p + 2 * k2 + 1];
-        } else if (p - 1 <= D && s_node[p - 1] >= 0) {
-            const double* tv = tvec + (p - 2) * TVS;
-#pragma unroll
-            for (int k2 = 0; k2 < RK / 2; ++k2) part += cur[k2].x * tv[2 * k2] + cur[k2].y * tv[2 * k2 + 1];
+            for (int k2 = 0; k2 < RK / 2; ++k2) {
+                q4[(2 * k2) & 3] = fma(cur[k2].x, src[2 * k2], q4[(2 * k2) & 3]);
+                q4[(2 * k2 + 1) & 3] = fma(cur[k2].y, src[2 * k2 + 1], q4[(2 * k2 + 1) & 3]);
+            }
+            part = act ? (q4[0] + q4[1]) + (q4[2] + q4[3]) : 0.0;
         }
         part += __shfl_xor_sync(0xffffffffu, part, 1);
         part += __shfl_xor_sync(0xffffffffu, part, 2);
         part += __shfl_xor_sync(0xffffffffu, part, 4);
         if (p == 0) {
             const double yv = prow ? 0.0 : part;
-            yh[lv * YHS + i] = yv;
+            yh[yhs(lv, i)] = yv;
             a.y[(long long)lv * Np + r] = yv;
             hnext = hsum;
         }
