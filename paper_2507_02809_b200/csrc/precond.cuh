@@ -27,7 +27,7 @@ struct fi_precond {
     // merged refinement sweep (precond_sweep_ir.cu), allocated on first use
     fib::DevBuf<double> ir_xb;        // 3 kinds x 2 parities x Np
     fib::DevBuf<double> ir_pb;        // 3 kinds x 2 parities x nb x nb x 64
-    fib::DevBuf<unsigned> ir_counters;  // xready[nb], pdone[3][nb]
+    fib::DevBuf<unsigned> ir_counters;  // xready[nb], pdone[3][nb], xready2[nb], pdone1b[nb]
 
     // ---- mode 1: substituted per-block solve (tau-preconditioned CG, precond_iter.cu)
     int mode = 0;  // 0 = dense packed inverses, 1 = tau-PCG per level

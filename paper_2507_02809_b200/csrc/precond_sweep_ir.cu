@@ -137,7 +137,10 @@ struct IrArgs {
     double* pb;   // [3 kinds][2 parities][nb][nb][TB]
     unsigned* xready;  // [nb] (stride CSTR); version 2: chain-1 counters
     unsigned* xready2;  // version 2: chain-2 counters [nb]
-    unsigned* pdone;   // [3][nb] (stride CSTR)
+    unsigned* pdone;   // [3][nb] (stride CSTR); kind 1 (B tiles) counts the even steps only
+    unsigned* pdone1b;  // [nb]: B tiles of the odd steps.  The B tiles run up to one step ahead of
+                        // their consumer (owner2), so one cumulative counter could reach step t-1's
+                        // target with step-t bumps; split by step parity, a counter cannot run ahead
     const int* skip;
     int evict_first;
     unsigned long long* trace;  // optional [G][nsteps+1][8] phase timestamps (FI_SWEEP_TRACE=1)
@@ -503,11 +506,12 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                 }
                 if (lane == 0 && nbt > 0) {
                     asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+                    unsigned* pc = (t & 1) ? a.pdone1b : a.pdone + nbb * CSTR;
                     for (int c = 0; c < nbt; ++c) {
                         int bi, bj;
                         coords_of(c, bi, bj);
-                        red_relaxed(a.pdone + (1 * nbb + bi) * CSTR, 1u);
-                        if (bi != bj) red_relaxed(a.pdone + (1 * nbb + bj) * CSTR, 1u);
+                        red_relaxed(pc + bi * CSTR, 1u);
+                        if (bi != bj) red_relaxed(pc + bj * CSTR, 1u);
                     }
                 }
                 if (tr && lane == 0) atomicMax(tr + 3, gtime());
@@ -525,6 +529,12 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
     // polls of the partial-product counters of this CTA's row blocks, spread over the spare warps
     auto poll_pdone = [&](int kind, unsigned target) {
         for (int q = sw; q < nrb; q += NSO) warp_spin_until(a.pdone + (kind * nbb + rb0 + q) * CSTR, target);
+    };
+    // B tiles of step s (1 <= s) done for the CTA's row blocks: the parity counter of s has seen all
+    // (s + 1) / 2 of its steps up to s
+    auto poll_bstep = [&](int s) {
+        const unsigned* pc = (s & 1) ? a.pdone1b : a.pdone + nbb * CSTR;
+        for (int q = sw; q < nrb; q += NSO) warp_spin_until(pc + (rb0 + q) * CSTR, (unsigned)(nbb * ((s + 1) / 2)));
     };
     // fixed-order sum of the nb partials of `kind` (parity par) for the owned rows -> red[slot]
     auto load_partials = [&](int kind, int par, int slot) {
@@ -570,7 +580,7 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
             if (t >= 1) {
                 poll_pdone(0, (unsigned)(nbb * min(t, nlev)));
                 // xb1[t & 1] is rewritten below: the B tiles of step t-2 that read it are done
-                if (t >= 3) poll_pdone(1, (unsigned)(nbb * clampi(t - 2, 0, nlev)));
+                if (t >= 3) poll_bstep(t - 2);
                 spare_bar();
                 if (sw == 0) c_h = h1p[lane];
                 load_partials(0, (t - 1) & 1, 0);
@@ -650,7 +660,7 @@ __global__ void __maxnreg__(168) sweep_ir_kernel(IrArgs a) {
                 c_d2 = a.D2[o];
                 c_di = a.d2inv[o];
             }
-            if (k1) poll_pdone(1, (unsigned)(nbb * clampi(t - 1, 0, nlev)));
+            if (k1) poll_bstep(t - 1);
             if (k2) poll_pdone(2, (unsigned)(nbb * clampi(t - 2, 0, nlev)));
             spare_bar();
             if (sw == 0) c_h2 = h2p[lane];
@@ -766,7 +776,7 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
     if (!P->ir_xb.p) {
         P->ir_xb.alloc((size_t)6 * L.Np);
         P->ir_pb.alloc((size_t)6 * P->nb * P->nb * TB);
-        P->ir_counters.alloc((size_t)5 * P->nb * CSTR);
+        P->ir_counters.alloc((size_t)6 * P->nb * CSTR);
     }
     IrArgs a;
     a.H64 = P->H.p;
@@ -797,6 +807,7 @@ void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int
     a.xready = P->ir_counters.p;
     a.pdone = P->ir_counters.p + (size_t)P->nb * CSTR;
     a.xready2 = P->ir_counters.p + (size_t)4 * P->nb * CSTR;
+    a.pdone1b = P->ir_counters.p + (size_t)5 * P->nb * CSTR;
     a.skip = skip;
     static const int evict = [] {
         const char* v = std::getenv("FI_IR_EVICT");

@@ -101,3 +101,27 @@ def test_hodlr_apply_is_bit_reproducible():
     z = np.random.default_rng(8).uniform(-1, 1, A.dim())
     y1, y2 = P.apply(z), P.apply(z)
     assert P.form == "hodlr" and np.array_equal(y1, y2)
+
+
+_CHILD_REPEAT = r"""
+import os, sys, numpy as np
+sys.path.insert(0, os.environ["ROOT"])
+from paper_2507_02809_b200 import fracinv as F
+from paper_2507_02809_b200.configs import baseline_problem
+A = F.SystemOperator(baseline_problem(F, 1))
+P = F.BlockTriangularPreconditioner(A)
+z = np.random.default_rng(5).uniform(-1, 1, A.dim())
+y0 = P.apply(z)
+bad = sum(not np.array_equal(P.apply(z), y0) for _ in range(int(os.environ["REPS"])))
+print(P.form, bad)
+"""
+
+
+@pytest.mark.parametrize("hodlr", [1, 0])
+def test_persistent_sweeps_repeat_bit_exactly(hodlr):
+    """Race check of both persistent P^{-1} kernels (hodlr_sweep_kernel; sweep_ir_kernel, whose
+    B-tile steps run ahead of their consumer): repeated applies on BASELINE config 1 are identical."""
+    env = dict(os.environ, FI_HODLR=str(hodlr), REPS="40", ROOT=ROOT)
+    out = subprocess.run([sys.executable, "-c", _CHILD_REPEAT], env=env, check=True, timeout=900,
+                         capture_output=True, text=True).stdout.split()
+    assert out[-2] == ("hodlr" if hodlr else "tiles") and out[-1] == "0", out
