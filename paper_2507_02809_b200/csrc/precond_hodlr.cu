@@ -39,10 +39,9 @@ constexpr unsigned kSpin = 1u << 25;
 constexpr int PRS = HR * 33 + 2;  // per-depth stride of the projection products (doubles; = 2 mod 16:
                                   // the 12 writers of a half-warp, 6 depths x 2 rows, hit distinct banks)
 constexpr int TVS = RK + 1;       // per-depth stride of the summed projections
-constexpr int YHS = HR;           // per-level stride of the y history
-// y history slot of (level m, row i): rows XOR-swizzled by level so that a half-warp (2 rows x 8
-// consecutive levels) of the history sum hits 16 distinct 8-byte bank pairs
-__device__ __forceinline__ int yhs(int m, int i) { return m * YHS + (i ^ ((m & 7) << 1)); }
+// y history: row-major [row][level], row stride = nlev rounded up to 2 mod 16 (even: level pairs load
+// as double2; 2 mod 16: the rows of a warp write different banks)
+__host__ __device__ inline int yh_stride(int nlev) { return (nlev + 13) / 16 * 16 + 2; }
 
 // Values exchanged between CTAs carry their own arrival signal: the least significant mantissa bit
 // holds the level tag ((level >> 1) & 1; buffers alternate by level parity), so a reader polls the
@@ -242,12 +241,14 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     const int maxslots = 2 * nb;
     // shared memory: y history of the CTA's rows [nlev][32], projection products, staging
     // (strides padded so that the 8 threads of a row, which differ in depth, hit different banks)
-    double* yh = sm;                               // nlev x YHS: y of the CTA's rows, every level
-    double* pr = yh + (long long)nlev * YHS;       // DMAX x PRS products (row i, k) at i * 33 + k
+    const int LS = yh_stride(nlev);
+    double* yh = sm;                               // HR x LS: y of the CTA's rows, every level
+    double* pr = yh + (long long)HR * LS;          // DMAX x PRS products (row i, k) at i * 33 + k
     double* stage = pr + DMAX * PRS;               // partial projections of the other sides
     double* tvec = stage + 2 * nb * RK;            // DMAX x TVS summed projections
     double* xsb = tvec + DMAX * TVS;               // 2 x 66: x of the leaf block, halves at 0 and 33, by level parity
     double* es = xsb + 2 * (TB + 2);               // nlev + 2: L1 weights e_0.. (history sums)
+    double* es1 = es + ((nlev + 3) & ~1);          // nlev + 2: the same shifted by one, es1[k] = e_{k+1}
     // per-depth node, side, slot, and the other side's CTA count
     __shared__ int s_node[DMAX + 1], s_side[DMAX + 1], s_slot[DMAX + 1], s_nother[DMAX + 1], s_ooff[DMAX + 2];
     if (t <= DMAX) {
@@ -276,7 +277,10 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         s_ooff[DMAX + 1] = off;  // total staged partials
     }
     __syncthreads();
-    for (int q = t; q < nlev + 2; q += blockDim.x) es[q] = a.epad[q];
+    for (int q = t; q < nlev + 2; q += blockDim.x) {
+        es[q] = a.epad[q];
+        es1[q] = a.epad[q + 1];
+    }
     __syncthreads();
     const double e1 = es[1];
     const long long lvstride = (Np / HR) * (RK / 2) * 256;
@@ -348,10 +352,10 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
             double x = 0.0;
             if (!prow) {
                 if (lv < S) {
-                    const double hist = (lv >= 2 ? hnext : 0.0) + (lv >= 1 ? e1 * yh[yhs(lv - 1, i)] : 0.0);
+                    const double hist = (lv >= 2 ? hnext : 0.0) + (lv >= 1 ? e1 * yh[i * LS + lv - 1] : 0.0);
                     x = (cz - cd1 * hist) * cdi;
                 } else {
-                    x = (cz - yh[yhs(S - 1, i)]) * cdi;
+                    x = (cz - yh[i * LS + S - 1]) * cdi;
                 }
             }
             xs[(r0 % TB) + i + (r0 % TB ? 1 : 0)] = x;
@@ -398,13 +402,26 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         load_coef(lv + 1, nz, nd1, ndi);
         // ---- history of the next level (rows' y up to lv - 1): sum_{m <= lv-1} e_{lv+1-m} y_m
         {
+            // level pairs (m, m + 1), m even, thread p takes m = 2p + 16j; weights (e_{lv+1-m}, e_{lv-m})
+            // as one double2 from es (lv even) or es1 (lv odd); a lone last level m = lv - 1 separately
             double h4[4] = {0.0, 0.0, 0.0, 0.0};
             if (lv + 1 < S) {
-                int m = p;
-                for (; m + 3 * HPART <= lv - 1; m += 4 * HPART)
+                const double* yr = yh + i * LS;
+                const double* eb = (lv & 1) ? es1 - 1 : es;  // eb + (lv - m) is 16-byte aligned
+                int m = 2 * p;
+                for (; m + 48 + 1 <= lv - 1; m += 64)
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) h4[u] += es[lv + 1 - m - u * HPART] * yh[yhs(m + u * HPART, i)];
-                for (; m <= lv - 1; m += HPART) h4[0] += es[lv + 1 - m] * yh[yhs(m, i)];
+                    for (int u = 0; u < 4; ++u) {
+                        const double2 yv = *reinterpret_cast<const double2*>(yr + m + 16 * u);
+                        const double2 ev = *reinterpret_cast<const double2*>(eb + lv - m - 16 * u);
+                        h4[u] = fma(yv.x, ev.y, fma(yv.y, ev.x, h4[u]));
+                    }
+                for (; m + 1 <= lv - 1; m += 16) {
+                    const double2 yv = *reinterpret_cast<const double2*>(yr + m);
+                    const double2 ev = *reinterpret_cast<const double2*>(eb + lv - m);
+                    h4[0] = fma(yv.x, ev.y, fma(yv.y, ev.x, h4[0]));
+                }
+                if (((lv - 1) & 1) == 0 && lv >= 1 && 2 * p == ((lv - 1) & 15)) h4[1] += es[2] * yr[lv - 1];
             }
             double h = (h4[0] + h4[1]) + (h4[2] + h4[3]);
             h += __shfl_xor_sync(0xffffffffu, h, 1);
@@ -481,7 +498,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         part += __shfl_xor_sync(0xffffffffu, part, 4);
         if (p == 0) {
             const double yv = prow ? 0.0 : part;
-            yh[yhs(lv, i)] = yv;
+            yh[i * LS + lv] = yv;
             a.y[(long long)lv * Np + r] = yv;
             hnext = hsum;
         }
@@ -558,7 +575,8 @@ __global__ void hodlr_check_apply(const double* W, const double2* hd, long long 
 }
 
 size_t hodlr_sweep_smem(int nlev, int nb) {
-    return ((size_t)nlev * YHS + DMAX * PRS + 2 * (size_t)nb * RK + DMAX * TVS + 2 * (TB + 2) + nlev + 2) *
+    return ((size_t)HR * yh_stride(nlev) + DMAX * PRS + 2 * (size_t)nb * RK + DMAX * TVS + 2 * (TB + 2) +
+            2 * (size_t)((nlev + 3) & ~1)) *
            sizeof(double);
 }
 
