@@ -129,9 +129,10 @@ int fi_precond_apply(fi_precond* P, const double* z_dev, double* y_dev);
 int fi_precond_apply_host(fi_precond* P, const double* z_host, double* y_host);
 /* Device memory held by the preconditioner's per-level inverses (bytes). */
 long long fi_precond_bytes(const fi_precond* P);
-/* refine != 0 (default): each apply adds one iterative-refinement sweep (FP32 inverses, FP64
- * residual through the operator kernel) so P^{-1} z matches LU-based solves to ~1e-13;
- * refine == 0: single FP64 sweep (forward error ~ kappa(block) * eps). */
+/* refine == 0 (default for dense blocks): one FP64 sweep over the polished inverses (built to the
+ * accuracy of the reference's LU solves: forward parity ~1e-13);
+ * refine != 0: each apply adds one iterative-refinement sweep (residual through the operator
+ * kernel), which also brings the residual |P y - z| to LU grade.  No effect in tau-PCG mode. */
 int fi_precond_set_refine(fi_precond* P, int refine);
 
 /* ------------------------------------------------------------------ problem assembly helpers

