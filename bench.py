@@ -278,16 +278,23 @@ def run_ours(args):
         rc = lib.fi_gmres_host(A.handle, P.handle, dp(b_host), None, dp(x_host), ctypes.byref(o), ctypes.byref(r),
                                hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 4096)
         assert rc == 0, last_error()
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        rc = lib.fi_gmres_host(A.handle, P.handle, dp(b_host), None, dp(x_host), ctypes.byref(o), ctypes.byref(r),
-                               hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 4096)
-        assert rc == 0, last_error()
-        e_iters += r.iterations
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    ms_e2e = ev0.elapsed_time(ev1)
+    # three timed passes of K solves each; the median pass is reported (a host-side hiccup in one
+    # pass, e.g. the thread descheduled while it waits on the look-ahead event, would otherwise
+    # decide the number)
+    passes = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        e_iters = 0
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rc = lib.fi_gmres_host(A.handle, P.handle, dp(b_host), None, dp(x_host), ctypes.byref(o), ctypes.byref(r),
+                                   hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 4096)
+            assert rc == 0, last_error()
+            e_iters += r.iterations
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        passes.append((ev0.elapsed_time(ev1), e_iters))
+    ms_e2e, e_iters = sorted(passes)[1]
 
     # ---- roofline: K2 preconditioner sweep (dominant) and K1 operator, live CUDA events
     reps = 5
@@ -367,7 +374,7 @@ def run_ours(args):
                             "forward_solve": round(t_fwd, 3)},
             },
             "e2e": {"value": round(e2e_value, 3), "unit": "iters/s", "h2d_bytes_per_step": 8 * n,
-                    "d2h_bytes_per_step": 8 * n},
+                    "d2h_bytes_per_step": 8 * n, "timing": "median of 3 timed passes of K solves"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": sweep_kernel,
                          "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",

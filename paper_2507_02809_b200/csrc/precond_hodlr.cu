@@ -13,11 +13,13 @@
 // randomized range finder  Y = M Omega, Q = CGS2(Y), V = M^T Q  (M = H[J, I]).  Rank 32 against a
 // numerical rank <= 19 at 1e-12 keeps the truncation near rounding level.
 //
-// Sweep (one persistent cooperative kernel, one CTA per 32 rows): per level, a CTA computes x of
-// its rows, publishes the partial projections V^T x / Q^T x of its rows for every ancestor node
-// (each value carries a level tag in its last mantissa bit, so readers poll the data itself), reads
-// the other sides' partials and its leaf sibling's x, and forms y.  One cross-CTA hop per level; the whole y history of the CTA's rows stays in
-// shared memory for the L1 time-convolution sums.
+// Sweep (one persistent cooperative kernel, one CTA per 32 rows, warp w = coefficient part): per
+// level every warp computes x of the CTA's rows, the low-rank warps publish their node's partial
+// projection V^T x / Q^T x (each value carries a level tag in its last mantissa bit, so readers poll
+// the data itself), all warps poll and pre-sum their share of the other sides' partials, and each
+// warp adds its part's contribution to y (leaf product or low-rank term).  One cross-CTA hop and two
+// block barriers per level; the y history of the CTA's rows stays in shared memory, and the L1
+// time-convolution sums over it run as one DMMA product per 8-level block, off the critical path.
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -36,12 +38,7 @@ constexpr int HR = 32;     // rows per sweep CTA
 constexpr int HPART = 8;   // threads per row in the sweep: 2 leaf halves + up to 6 ancestor depths
 constexpr int DMAX = 6;    // tree depth supported (nb <= 64 leaves)
 constexpr unsigned kSpin = 1u << 25;
-constexpr int PRS = HR * 33 + 2;  // per-depth stride of the projection products (doubles; = 2 mod 16:
-                                  // the 12 writers of a half-warp, 6 depths x 2 rows, hit distinct banks)
-constexpr int TVS = RK + 1;       // per-depth stride of the summed projections
-// y history: row-major [row][level], row stride = nlev rounded up to 2 mod 16 (even: level pairs load
-// as double2; 2 mod 16: the rows of a warp write different banks)
-__host__ __device__ inline int yh_stride(int nlev) { return (nlev + 13) / 16 * 16 + 2; }
+constexpr int MAXQ = 16;  // partial-projection vectors polled per warp and level (<= ceil(126 / 8))
 
 // Values exchanged between CTAs carry their own arrival signal: the least significant mantissa bit
 // holds the level tag ((level >> 1) & 1; buffers alternate by level parity), so a reader polls the
@@ -65,6 +62,18 @@ struct Tree {
     const int* mid;      // [nnodes] first leaf of J
     const int* hi;       // [nnodes] one past the last leaf
 };
+
+// Register layout of a sweep thread (warp w = part, lane = (g, kq) = (lane >> 3, lane & 7)): the
+// 32 coefficients C_w[row][k] for rows 8g + i (i < 8) and columns k = 4kq + c (c < 4), as 16 double2
+// (i, h) = (C[8g+i][4kq+2h], C[8g+i][4kq+2h+1]) at double2 index (2i + h) * 256 + 32w + lane of the
+// CTA's level block.  Part w = 0, 1: columns 32w.. of the row's 64-row leaf block; w = 2..7: the
+// basis row of the depth-(w-1) ancestor (Q on the J side, V on the I side).  A projection V^T x
+// (a sum over rows) then needs a 4-way cross-lane reduction, and a row's y (a sum over columns) an
+// 8-way one: 10 shuffles of doubles per warp instead of a 32-row transpose through shared memory.
+__host__ __device__ inline long long hd_index(int row, int part, int k2) {
+    // element pair (C[row][2 k2], C[row][2 k2 + 1]) of part `part` within a CTA's level block
+    return (long long)((row & 7) * 2 + (k2 & 1)) * 256 + 32 * part + (row >> 3) * 8 + (k2 >> 1);
+}
 
 __device__ __forceinline__ double omega(int d, long long row, int k) {
     // deterministic pseudo-random test matrix (SplitMix64 finaliser -> uniform in [-1, 1))
@@ -176,9 +185,9 @@ __global__ void hodlr_cgs2(Tree tr, int d, long long Np, double* buf, int nnodes
     }
 }
 
-// Pack the sweep layout: per level and 32-row CTA block, element (row i, part p, k) at double2
-// index (k / 2) * 256 + 8 i + p: p = 0, 1 the leaf row (columns 32 p + k of the row's 64-row leaf),
-// p = 2..7 the basis row of the depth-(p-1) ancestor (Q for J rows, V for I rows), 0 if none.
+// Pack the sweep layout (hd_index): per level and 32-row CTA block, part p = 0, 1 the leaf row
+// (columns 32 p + k of the row's 64-row leaf), p = 2..7 the basis row of the depth-(p-1) ancestor
+// (Q for J rows, V for I rows), 0 if none.
 __global__ void hodlr_pack(const double* W, long long Np, int n2, int ld2, Tree tr, const double* buf,
                            double2* out) {
     const int c = blockIdx.x, lvb = blockIdx.y;
@@ -206,7 +215,7 @@ __global__ void hodlr_pack(const double* W, long long Np, int n2, int ld2, Tree 
         v[k] = val;
     }
 #pragma unroll
-    for (int k2 = 0; k2 < RK / 2; ++k2) o[k2 * 256 + t] = make_double2(v[2 * k2], v[2 * k2 + 1]);
+    for (int k2 = 0; k2 < RK / 2; ++k2) o[hd_index(i, p, k2)] = make_double2(v[2 * k2], v[2 * k2 + 1]);
 }
 
 // ------------------------------------------------------------------ sweep
@@ -225,8 +234,23 @@ struct HArgs {
     double* proj;        // [2][nnodes][2 sides][slots <= nb * 2][RK] partial projections, level-tagged
     const int* skip;
     unsigned long long* trace;  // optional [8]: per-phase time sums of CTA 0 (FI_HODLR_TRACE=1)
+    int dbg;                    // FI_HODLR_DBG experiment bits (0 in production)
 };
 
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Shared-memory plan of the sweep (doubles): y history [nlev][YS], history partials of the old
+// part [8 warps][8 targets][32], per-warp history and y contributions [8][32] each, per-warp x
+// [8][32], the leaf sibling's x [32], segment sums [16][SGS], L1 weights [nlev + 24]
+// (history partials twice, by level parity).
+constexpr int YS = 36;   // y history row stride (DMMA A-fragment loads: 2 wavefronts)
+constexpr int SGS = 36;  // segment-sum stride (16-byte aligned rows)
+__host__ __device__ inline int es_len(int nlev) { return (nlev + 24 + 1) & ~1; }
 
 __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     if (a.skip && *a.skip) return;
@@ -234,23 +258,21 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     const int nlev = a.nlev, S = a.S, D = a.tr.D, nb = a.tr.nb;
     const long long Np = a.Np;
     const int c = blockIdx.x, t = threadIdx.x;
-    const int i = t >> 3, p = t & 7;
-    const long long r0 = (long long)c * HR, r = r0 + i;
+    const int w = t >> 5, lane = t & 31, g = lane >> 3, kq = lane & 7;
+    const long long r0 = (long long)c * HR;
     const int b = (int)(r0 / TB);  // leaf block of the CTA (two CTAs per leaf)
-    const bool prow = (int)(r % a.ld2) >= a.n2;
+    const int own_half = (int)((r0 % TB) / HR);
     const int maxslots = 2 * nb;
-    // shared memory: y history of the CTA's rows [nlev][32], projection products, staging
-    // (strides padded so that the 8 threads of a row, which differ in depth, hit different banks)
-    const int LS = yh_stride(nlev);
-    double* yh = sm;                               // HR x LS: y of the CTA's rows, every level
-    double* pr = yh + (long long)HR * LS;          // DMAX x PRS products (row i, k) at i * 33 + k
-    double* stage = pr + DMAX * PRS;               // partial projections of the other sides
-    double* tvec = stage + 2 * nb * RK;            // DMAX x TVS summed projections
-    double* xsb = tvec + DMAX * TVS;               // 2 x 66: x of the leaf block, halves at 0 and 33, by level parity
-    double* es = xsb + 2 * (TB + 2);               // nlev + 2: L1 weights e_0.. (history sums)
-    double* es1 = es + ((nlev + 3) & ~1);          // nlev + 2: the same shifted by one, es1[k] = e_{k+1}
-    // per-depth node, side, slot, and the other side's CTA count
-    __shared__ int s_node[DMAX + 1], s_side[DMAX + 1], s_slot[DMAX + 1], s_nother[DMAX + 1], s_ooff[DMAX + 2];
+    double* yh = sm;                                  // [nlev][YS]
+    double* hpart = yh + (long long)nlev * YS;        // [8][8][32]
+    double* hps = hpart + 8 * 8 * 32;                 // [2][8][32] (by level parity: a fast warp's next
+                                                      //  write must not meet a slow warp's read)
+    double* ycon = hps + 2 * 8 * 32;                  // [8][32]
+    double* xw = ycon + 8 * 32;                       // [8][32]
+    double* xr = xw + 8 * 32;                         // [32]
+    double* segout = xr + 32;                         // [16][SGS]
+    double* es = segout + 16 * SGS;                   // [es_len]
+    __shared__ int s_node[DMAX + 1], s_side[DMAX + 1], s_slot[DMAX + 1], s_nother[DMAX + 1];
     if (t <= DMAX) {
         int node = -1, side = -1, slot = 0, nother = 0;
         if (t >= 1 && t <= D) {
@@ -268,247 +290,269 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         s_nother[t] = nother;
     }
     __syncthreads();
+    // The other sides' partial projections of every ancestor node: a warp takes up to MAXQ whole
+    // 32-vectors (lane = k), polls them and sums them in registers per depth ("segment": one depth's
+    // run of slots within the warp's share, fixed order); a depth warp then adds its depth's segment
+    // sums in fixed order.  Partition (thread 0, once): depths in order, slots in order,
+    // ceil(total / 8) slots per warp.
+    __shared__ int w_nq[8], w_nseg[8], w_slot[8][MAXQ], w_segend[8][DMAX + 1], w_segg[8][DMAX + 1], s_gfirst[DMAX + 2];
     if (t == 0) {
-        int off = 0;
+        int tot = 0;
+        for (int d = 1; d <= D; ++d)
+            if (s_node[d] >= 0) tot += s_nother[d];
+        const int quota = (tot + 7) / 8;
+        for (int q = 0; q < 8; ++q) w_nq[q] = w_nseg[q] = 0;
+        int ww = 0, gg = 0;
         for (int d = 1; d <= DMAX; ++d) {
-            s_ooff[d] = off;
-            off += s_nother[d] * RK;
+            s_gfirst[d] = gg;
+            if (d > D || s_node[d] < 0) continue;
+            bool open = false;
+            for (int sl = 0; sl < s_nother[d]; ++sl) {
+                if (w_nq[ww] == quota) {
+                    ++ww;
+                    open = false;
+                }
+                if (!open) {
+                    w_segg[ww][w_nseg[ww]++] = gg++;
+                    open = true;
+                }
+                w_slot[ww][w_nq[ww]++] = ((s_node[d] * 2 + (1 - s_side[d])) * maxslots + sl) * RK;
+                w_segend[ww][w_nseg[ww] - 1] = w_nq[ww];
+            }
         }
-        s_ooff[DMAX + 1] = off;  // total staged partials
+        s_gfirst[DMAX + 1] = gg;
     }
+    for (int q = t; q < es_len(nlev); q += blockDim.x) es[q] = a.epad[q];
+    for (int q = t; q < 8 * 8 * 32; q += blockDim.x) hpart[q] = 0.0;
+    __shared__ unsigned long long s_trace[8];
+    if (t < 8) s_trace[t] = 0;
     __syncthreads();
-    for (int q = t; q < nlev + 2; q += blockDim.x) {
-        es[q] = a.epad[q];
-        es1[q] = a.epad[q + 1];
-    }
-    __syncthreads();
+    const int wq = w_nq[w];
+    // the warp's slot offsets (shared), the mask of its segments' last slots, its first segment
+    const int* soff = w_slot[w];
+    unsigned segend_mask = 0;
+    for (int sg = 0; sg < w_nseg[w]; ++sg) segend_mask |= 1u << (w_segend[w][sg] - 1);
+    const int gfirst_w = w_nseg[w] > 0 ? w_segg[w][0] : 0;
+    const int dep = w - 1;  // depth of a low-rank warp (w >= 2)
+    const bool lowrank = w >= 2 && dep <= D && s_node[dep] >= 0;
+    const bool leaf_remote = w < 2 && w != own_half;
+    const long long sib_r = (long long)b * TB + (own_half ? 0 : HR) + lane;
+    const long long my_slot = lowrank ? ((long long)(s_node[dep] * 2 + s_side[dep]) * maxslots + s_slot[dep]) * RK : 0;
+    const long long row = r0 + lane;  // the row this lane owns in x / y / history (lane = row)
+    const bool prow = (int)(row % a.ld2) >= a.n2;
     const double e1 = es[1];
     const long long lvstride = (Np / HR) * (RK / 2) * 256;
-    // this thread's 32 coefficients of the current level (registers), prefetched one level ahead
     double2 cur[RK / 2], nxt[RK / 2];
     auto load_level = [&](int lv, double2* dst) {
         const double2* src = a.hd + (long long)lv * lvstride + (long long)c * (RK / 2) * 256;
 #pragma unroll
         for (int k2 = 0; k2 < RK / 2; ++k2) dst[k2] = __ldg(src + k2 * 256 + t);
     };
-    // the next level's coefficients in four groups at different points of the level, so that the
-    // loads (L2 hits after the prefetch) never throttle a warp's issue
     auto load_quarter = [&](int lv, int q) {
-        if (lv >= nlev) return;
+        if (lv >= nlev || (a.dbg & 2)) return;
         const double2* src = a.hd + (long long)lv * lvstride + (long long)c * (RK / 2) * 256;
 #pragma unroll
         for (int k2 = 4 * q; k2 < 4 * q + 4; ++k2) nxt[k2] = __ldg(src + k2 * 256 + t);
     };
-    // the other sides' partials this thread stages each level: fixed offsets within a parity block
-    constexpr int MAXE = (2 * 64 * RK + 255) / 256;  // <= 2 nb RK staged values / 256 threads
-    int soff[MAXE];
-#pragma unroll
-    for (int u = 0; u < MAXE; ++u) {
-        const int e = t + u * 256;
-        soff[u] = -1;
-        if (e < s_ooff[DMAX + 1]) {
-            int d = 1;
-            while (d < DMAX && e >= s_ooff[d + 1]) ++d;
-            const int le = e - s_ooff[d];
-            soff[u] = (((s_node[d] * 2 + (1 - s_side[d])) * maxslots) + le / RK) * RK + le % RK;
-        }
-    }
-    load_level(0, cur);
-    double hnext = 0.0;  // (p == 0) history sum of the current level's x numerator
-    double hsum = 0.0, xrow = 0.0;
-    // (p == 0) z, D1, 1/D2 of the row for level lv, loaded one level ahead
+    // z, D1, 1/D2 of the lane's row for level lv (every warp: x is computed redundantly per warp)
+    // (pad rows read the zero pads of z, D1, 1/D2; levels past the last read level S's rows)
     auto load_coef = [&](int lv, double& cz, double& cd1, double& cdi) {
-        cz = cd1 = cdi = 0.0;
-        if (p != 0 || prow || lv >= nlev) return;
-        if (lv < S) {
-            const long long o = (long long)lv * Np + r;
-            cz = a.z[o];
-            cd1 = a.D1[o];
-            cdi = a.d2inv[o];
-        } else {
-            cz = a.z[(long long)S * Np + r];
-            cdi = a.d2inv[(long long)(S - 1) * Np + r];
-        }
+        const int lz = min(lv, S), ld = min(lv, S - 1);
+        cz = __ldg(a.z + (long long)lz * Np + row);
+        cd1 = __ldg(a.D1 + (long long)ld * Np + row);
+        cdi = __ldg(a.d2inv + (long long)ld * Np + row);
     };
-    double cz, cd1, cdi, nz, nd1, ndi;
-    load_coef(0, cz, cd1, cdi);
-    // (each stamp is a global read-modify-write of one thread: the phase after it carries its latency;
-    // register accumulators would cost the kernel spills)
+    // sum over the lane's 8 rows and 4 columns with u[4 kq + c]: an 8-way reduce-scatter over kq
+    // leaves row 8g + kq = lane in the lane
+    auto row_sums = [&](const double* u) -> double {
+        const double4 uv = *reinterpret_cast<const double4*>(u + 4 * kq);
+        double Y[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            Y[i] = fma(cur[2 * i + 1].y, uv.w, fma(cur[2 * i + 1].x, uv.z, fma(cur[2 * i].y, uv.y, cur[2 * i].x * uv.x)));
+        const bool b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+        double Z[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) Z[i] = (b2 ? Y[i + 4] : Y[i]) + __shfl_xor_sync(0xffffffffu, b2 ? Y[i] : Y[i + 4], 4);
+        double Z2[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) Z2[i] = (b1 ? Z[i + 2] : Z[i]) + __shfl_xor_sync(0xffffffffu, b1 ? Z[i] : Z[i + 2], 2);
+        return (b0 ? Z2[1] : Z2[0]) + __shfl_xor_sync(0xffffffffu, b0 ? Z2[0] : Z2[1], 1);
+    };
     unsigned long long tl = 0;
     auto stamp = [&](int ph) {
         if (a.trace && blockIdx.x == 0 && t == 0) {
             const unsigned long long now = clock64();
-            if (tl) a.trace[ph] += now - tl;
+            if (tl) s_trace[ph] += now - tl;
             tl = now;
         }
     };
+    load_level(0, cur);
+    double cz, cd1, cdi, nz, nd1, ndi;
+    load_coef(0, cz, cd1, cdi);
+    double yprev = 0.0, hrest = 0.0;  // y of the previous level and sum_{m <= lv-2} e_{lv-m} y_m (lane's row)
+    double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // old-part history (DMMA C)
     for (int lv = 0; lv < nlev; ++lv) {
         stamp(7);
         const int par = lv & 1;
         const unsigned tag = (unsigned)(lv >> 1) & 1u;
-        double* xs = xsb + par * (TB + 2);
-        // ---- x of the CTA's rows
-        if (p == 0) {
-            double x = 0.0;
-            if (!prow) {
-                if (lv < S) {
-                    const double hist = (lv >= 2 ? hnext : 0.0) + (lv >= 1 ? e1 * yh[i * LS + lv - 1] : 0.0);
-                    x = (cz - cd1 * hist) * cdi;
-                } else {
-                    x = (cz - yh[i * LS + S - 1]) * cdi;
-                }
+        // ---- x of the CTA's rows (lane = row), identical in every warp
+        double x = 0.0;
+        if (!prow) x = lv < S ? (cz - cd1 * fma(e1, yprev, hrest)) * cdi : (cz - yprev) * cdi;
+        if (w == 0) st_tagged(a.xg + (long long)par * Np + row, x, tag);
+        xw[w * 32 + lane] = x;
+        load_coef(lv + 1, nz, nd1, ndi);
+        __syncwarp();
+        // ---- partial projection V^T x / Q^T x of the CTA's rows (low-rank warps), published
+        if (lowrank) {
+            const double* xv = xw + w * 32 + 8 * g;
+            double P[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const double xi = xv[i];
+                P[0] = fma(cur[2 * i].x, xi, P[0]);
+                P[1] = fma(cur[2 * i].y, xi, P[1]);
+                P[2] = fma(cur[2 * i + 1].x, xi, P[2]);
+                P[3] = fma(cur[2 * i + 1].y, xi, P[3]);
             }
-            xs[(r0 % TB) + i + (r0 % TB ? 1 : 0)] = x;
-            st_tagged(a.xg + (long long)par * Np + r, x, tag);
-            xrow = x;
+            const bool hi = lane & 16, lo = lane & 8;
+            const double q0 = (hi ? P[2] : P[0]) + __shfl_xor_sync(0xffffffffu, hi ? P[0] : P[2], 16);
+            const double q1 = (hi ? P[3] : P[1]) + __shfl_xor_sync(0xffffffffu, hi ? P[1] : P[3], 16);
+            const double s = (lo ? q1 : q0) + __shfl_xor_sync(0xffffffffu, lo ? q0 : q1, 8);
+            // lane (g, kq) holds k = 4 kq + g
+            const long long pb = (long long)par * a.tr.nnodes * 2 * maxslots * RK;
+            st_tagged(a.proj + pb + my_slot + 4 * kq + g, s, tag);
         }
-        // x of the row to its 8 threads (no block barrier: the row's threads share a warp)
-        xrow = __shfl_sync(0xffffffffu, xrow, (t & 31) & ~7);
         stamp(0);
         load_quarter(lv + 1, 0);
-        // ---- partial projections of the CTA's rows for every ancestor node
-        if (p >= 2 && p - 1 <= D && s_node[p - 1] >= 0) {
-            const double xv = xrow;
-            double* pd = pr + (p - 2) * PRS + i * 33;
-#pragma unroll
-            for (int k2 = 0; k2 < RK / 2; ++k2) {
-                pd[2 * k2] = cur[k2].x * xv;
-                pd[2 * k2 + 1] = cur[k2].y * xv;
-            }
-        }
-        __syncthreads();
-        if (t < D * RK) {
-            const int d = t / RK + 1, k = t % RK;
-            if (s_node[d] >= 0) {
-                const double* pd = pr + (d - 1) * PRS;
-                double s4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                for (int ii = 0; ii < HR; ++ii) s4[ii & 3] += pd[ii * 33 + k];
-                const double s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-                const long long slotbase = (((long long)par * a.tr.nnodes + s_node[d]) * 2 + s_side[d]) * maxslots;
-                st_tagged(a.proj + (slotbase + s_slot[d]) * RK + k, s, tag);
-            }
-        }
-        stamp(1);
-        // next level's coefficients: issued here, off the publish path, consumed at the level's end;
-        // the level after that is pulled into L2 now, so these register loads hit L2
-        if (lv + 2 < nlev) {
+        // next-next level's coefficients pulled into L2 now, so the register loads hit L2
+        if (lv + 2 < nlev && !(a.dbg & 1)) {
             const char* pf = reinterpret_cast<const char*>(a.hd + (long long)(lv + 2) * lvstride +
                                                            (long long)c * (RK / 2) * 256);
             for (int q = t; q < (RK / 2) * 256 * 16 / 128; q += blockDim.x)
                 asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pf + (long long)q * 128));
         }
-        load_quarter(lv + 1, 1);
-        load_coef(lv + 1, nz, nd1, ndi);
-        // ---- history of the next level (rows' y up to lv - 1): sum_{m <= lv-1} e_{lv+1-m} y_m
+        // ---- the own leaf half (its x is the CTA's own): no remote input
+        double ypart = 0.0;
+        if (w == own_half) ypart = row_sums(xw + w * 32);
+        // ---- history (off the critical path).  hist_L = e1 y_{L-1} + sum_{m <= L-2} e_{L-m} y_m,
+        // the sum split into an old part (m < 8 kb - 8, kb = L >> 3: one DMMA product per 8-level
+        // block, accumulated during the block before and spread over its levels and warps) and a
+        // recent part (<= 14 terms, m = w mod 8 per warp); the 8 warp partials meet in hps.
         {
-            // level pairs (m, m + 1), m even, thread p takes m = 2p + 16j; weights (e_{lv+1-m}, e_{lv-m})
-            // as one double2 from es (lv even) or es1 (lv odd); a lone last level m = lv - 1 separately
-            double h4[4] = {0.0, 0.0, 0.0, 0.0};
-            if (lv + 1 < S) {
-                const double* yr = yh + i * LS;
-                const double* eb = (lv & 1) ? es1 - 1 : es;  // eb + (lv - m) is 16-byte aligned
-                int m = 2 * p;
-                for (; m + 48 + 1 <= lv - 1; m += 64)
+            const int kb = lv >> 3, j = lv & 7;
+            const int T0 = 8 * kb + 8;  // targets of the next block
+            for (int s = 8 * j + w; s < 2 * kb; s += 64) {
+                const int m0 = 4 * s;
+                const double bf = es[T0 + (lane >> 2) - (m0 + (lane & 3))];
+                const double* ya = yh + (long long)(m0 + (lane & 3)) * YS + (lane >> 2);
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const double2 yv = *reinterpret_cast<const double2*>(yr + m + 16 * u);
-                        const double2 ev = *reinterpret_cast<const double2*>(eb + lv - m - 16 * u);
-                        h4[u] = fma(yv.x, ev.y, fma(yv.y, ev.x, h4[u]));
-                    }
-                for (; m + 1 <= lv - 1; m += 16) {
-                    const double2 yv = *reinterpret_cast<const double2*>(yr + m);
-                    const double2 ev = *reinterpret_cast<const double2*>(eb + lv - m);
-                    h4[0] = fma(yv.x, ev.y, fma(yv.y, ev.x, h4[0]));
-                }
-                if (((lv - 1) & 1) == 0 && lv >= 1 && 2 * p == ((lv - 1) & 15)) h4[1] += es[2] * yr[lv - 1];
+                for (int rt = 0; rt < 4; ++rt) dmma884(acc[rt][0], acc[rt][1], ya[8 * rt], bf);
             }
-            double h = (h4[0] + h4[1]) + (h4[2] + h4[3]);
-            h += __shfl_xor_sync(0xffffffffu, h, 1);
-            h += __shfl_xor_sync(0xffffffffu, h, 2);
-            h += __shfl_xor_sync(0xffffffffu, h, 4);
-            hsum = h;  // (all 8 threads of the row hold the sum)
+            if (j == 7) {
+                double* hp = hpart + w * 256;
+#pragma unroll
+                for (int rt = 0; rt < 4; ++rt) {
+                    const int rr = 8 * rt + (lane >> 2), n0 = 2 * (lane & 3);
+                    hp[n0 * 32 + rr] = acc[rt][0];
+                    hp[(n0 + 1) * 32 + rr] = acc[rt][1];
+                    acc[rt][0] = acc[rt][1] = 0.0;
+                }
+                __syncwarp();
+            }
+            const int tgt = lv + 1, kbt = tgt >> 3;
+            double h = hpart[w * 256 + (tgt & 7) * 32 + lane];
+            const int m1 = max(0, 8 * kbt - 8);
+            for (int m = m1 + ((w - m1) & 7); m <= tgt - 2; m += 8) h = fma(es[tgt - m], yh[(long long)m * YS + lane], h);
+            hps[par * 256 + w * 32 + lane] = h;
         }
-        stamp(2);
-        stamp(3);
-        load_quarter(lv + 1, 2);
-        // ---- the other sides' partials and the leaf sibling's x: load all, re-poll the ones whose
-        // level tag is not current yet
+        stamp(1);
+        load_quarter(lv + 1, 1);
+        // ---- the other sides' partials (and the leaf sibling's x): poll, sum per segment
         {
             const long long pbase = (long long)par * a.tr.nnodes * 2 * maxslots * RK;
-            unsigned long long bv[MAXE];
+            const double* pp = a.proj + pbase + lane;
+            unsigned long long bv[MAXQ];
             unsigned long long xb = 0;
-            const long long rr = (long long)b * TB + t;
-            const bool xsib = t < TB && (rr < r0 || rr >= r0 + HR);
 #pragma unroll
-            for (int u = 0; u < MAXE; ++u) bv[u] = soff[u] >= 0 ? ld_bits(a.proj + pbase + soff[u]) : tag;
-            if (xsib) xb = ld_bits(a.xg + (long long)par * Np + rr);
+            for (int u = 0; u < MAXQ; ++u) bv[u] = u < wq ? ld_bits(pp + soff[u]) : tag;
+            if (leaf_remote) xb = ld_bits(a.xg + (long long)par * Np + sib_r);
             for (unsigned n = 0;; ++n) {
-                bool ok = !xsib || (unsigned)(xb & 1ull) == tag;
+                bool ok = !leaf_remote || (unsigned)(xb & 1ull) == tag;
 #pragma unroll
-                for (int u = 0; u < MAXE; ++u) ok = ok && (unsigned)(bv[u] & 1ull) == tag;
+                for (int u = 0; u < MAXQ; ++u) ok = ok && (unsigned)(bv[u] & 1ull) == tag;
                 if (ok) break;
-                __nanosleep(32);
+                if (a.dbg & 4) __nanosleep(32);  // (spinning is faster: a sleeping poller wakes late)
                 if (n == kSpin) __trap();
 #pragma unroll
-                for (int u = 0; u < MAXE; ++u)
-                    if (soff[u] >= 0 && (unsigned)(bv[u] & 1ull) != tag) bv[u] = ld_bits(a.proj + pbase + soff[u]);
-                if (xsib && (unsigned)(xb & 1ull) != tag) xb = ld_bits(a.xg + (long long)par * Np + rr);
+                for (int u = 0; u < MAXQ; ++u)
+                    if (u < wq && (unsigned)(bv[u] & 1ull) != tag) bv[u] = ld_bits(pp + soff[u]);
+                if (leaf_remote && (unsigned)(xb & 1ull) != tag) xb = ld_bits(a.xg + (long long)par * Np + sib_r);
             }
+            stamp(2);
+            // one pass: a segment's sum is stored at its last slot (segend bit), the next starts at 0
+            double sacc = 0.0;
+            double* so = segout + gfirst_w * SGS + lane;
 #pragma unroll
-            for (int u = 0; u < MAXE; ++u)
-                if (soff[u] >= 0) stage[t + u * 256] = __longlong_as_double((long long)bv[u]);
-            if (xsib) xs[t + (t >= 32 ? 1 : 0)] = __longlong_as_double((long long)xb);
-        }
-        __syncthreads();
-        if (t < D * RK) {
-            const int d = t / RK + 1, k = t % RK;
-            double s4[4] = {0.0, 0.0, 0.0, 0.0};
-            if (s_node[d] >= 0) {
-                const double* st = stage + s_ooff[d] + k;
-                const int no = s_nother[d];
-                int j = 0;
-                for (; j + 4 <= no; j += 4) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) s4[u] += st[(j + u) * RK];
+            for (int u = 0; u < MAXQ; ++u) {
+                if (u < wq) sacc += __longlong_as_double((long long)bv[u]);
+                if ((segend_mask >> u) & 1u) {
+                    *so = sacc;
+                    so += SGS;
+                    sacc = 0.0;
                 }
-                for (; j < no; ++j) s4[j & 3] += st[j * RK];
             }
-            tvec[(d - 1) * TVS + k] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+            if (leaf_remote) {
+                xr[lane] = __longlong_as_double((long long)xb);
+                __syncwarp();
+                ypart = row_sums(xr);
+            }
         }
+        load_quarter(lv + 1, 2);
+        load_quarter(lv + 1, 3);
+        __syncthreads();
+        stamp(3);
+        // ---- low-rank terms: the depth's summed partials t (lane: t[4 kq .. 4 kq + 3]), y += C t
+        if (lowrank) {
+            double4 tv = make_double4(0.0, 0.0, 0.0, 0.0);
+            for (int gg = s_gfirst[dep]; gg < s_gfirst[dep + 1]; ++gg) {
+                const double4 sv = *reinterpret_cast<const double4*>(segout + gg * SGS + 4 * kq);
+                tv.x += sv.x;
+                tv.y += sv.y;
+                tv.z += sv.z;
+                tv.w += sv.w;
+            }
+            double* tb = xw + w * 32;  // the warp's x slice is free again: stage t there
+            *reinterpret_cast<double4*>(tb + 4 * kq) = tv;  // (every g writes the same values)
+            __syncwarp();
+            ypart = row_sums(tb);
+        }
+        ycon[w * 32 + lane] = ypart;
         __syncthreads();
         stamp(4);
-        load_quarter(lv + 1, 3);
-        // ---- y of the CTA's rows: leaf product + low-rank terms, 8 threads per row
-        // (one branch-free loop for both kinds of part, four independent FMA chains)
-        double part;
-        {
-            const bool act = p < 2 || (p - 1 <= D && s_node[p - 1] >= 0);
-            const double* src = p < 2 ? xs + 33 * p : tvec + (p - 2) * TVS;
-            double q4[4] = {0.0, 0.0, 0.0, 0.0};
+        // ---- y of the CTA's rows (lane = row): the eight warps' contributions in fixed order
+        double y = 0.0, hr = 0.0;
 #pragma unroll
-            for (int k2 = 0; k2 < RK / 2; ++k2) {
-                q4[(2 * k2) & 3] = fma(cur[k2].x, src[2 * k2], q4[(2 * k2) & 3]);
-                q4[(2 * k2 + 1) & 3] = fma(cur[k2].y, src[2 * k2 + 1], q4[(2 * k2 + 1) & 3]);
-            }
-            part = act ? (q4[0] + q4[1]) + (q4[2] + q4[3]) : 0.0;
+        for (int q = 0; q < 8; ++q) {
+            y += ycon[q * 32 + lane];
+            hr += hps[par * 256 + q * 32 + lane];
         }
-        part += __shfl_xor_sync(0xffffffffu, part, 1);
-        part += __shfl_xor_sync(0xffffffffu, part, 2);
-        part += __shfl_xor_sync(0xffffffffu, part, 4);
-        if (p == 0) {
-            const double yv = prow ? 0.0 : part;
-            yh[i * LS + lv] = yv;
-            a.y[(long long)lv * Np + r] = yv;
-            hnext = hsum;
-        }
+        if (prow) y = 0.0;
+        yh[(long long)lv * YS + lane] = y;  // (every warp writes the same value)
+        if (w == 0) a.y[(long long)lv * Np + row] = y;
+        yprev = y;
+        hrest = hr;
         stamp(5);
+        if (!(a.dbg & 2)) {
 #pragma unroll
-        for (int k2 = 0; k2 < RK / 2; ++k2) cur[k2] = nxt[k2];
+            for (int k2 = 0; k2 < RK / 2; ++k2) cur[k2] = nxt[k2];
+        }
         cz = nz;
         cd1 = nd1;
         cdi = ndi;
     }
+    if (a.trace && blockIdx.x == 0 && t == 0)
+        for (int q = 0; q < 8; ++q) a.trace[q] = s_trace[q];
 }
 
 // ------------------------------------------------------------------ a-posteriori accuracy check
@@ -532,7 +576,7 @@ __global__ void hodlr_check_proj(const double2* hd, long long Np, int n2, int ld
     const double xv = probe(r, n2, ld2);
     double* dst = pj + (((long long)lvb * tr.nnodes + node) * 2 + side) * RK;
     for (int k2 = 0; k2 < RK / 2; ++k2) {
-        const double2 v = o[k2 * 256 + t];
+        const double2 v = o[hd_index(i, p, k2)];
         atomicAdd(dst + 2 * k2, v.x * xv);
         atomicAdd(dst + 2 * k2 + 1, v.y * xv);
     }
@@ -549,7 +593,7 @@ __global__ void hodlr_check_apply(const double* W, const double2* hd, long long 
     double yh = 0.0, yd = 0.0;
     if (p < 2) {
         for (int k2 = 0; k2 < RK / 2; ++k2) {
-            const double2 v = o[k2 * 256 + t];
+            const double2 v = o[hd_index(i, p, k2)];
             const long long c0 = (long long)b * TB + 32 * p + 2 * k2;
             yh += v.x * probe(c0, n2, ld2) + v.y * probe(c0 + 1, n2, ld2);
         }
@@ -557,7 +601,7 @@ __global__ void hodlr_check_apply(const double* W, const double2* hd, long long 
         const int d = p - 1, node = tr.rb_node[d * tr.nb + b], side = tr.rb_side[d * tr.nb + b];
         const double* tv = pj + (((long long)lvb * tr.nnodes + node) * 2 + (1 - side)) * RK;
         for (int k2 = 0; k2 < RK / 2; ++k2) {
-            const double2 v = o[k2 * 256 + t];
+            const double2 v = o[hd_index(i, p, k2)];
             yh += v.x * tv[2 * k2] + v.y * tv[2 * k2 + 1];
         }
     }
@@ -575,9 +619,8 @@ __global__ void hodlr_check_apply(const double* W, const double2* hd, long long 
 }
 
 size_t hodlr_sweep_smem(int nlev, int nb) {
-    return ((size_t)HR * yh_stride(nlev) + DMAX * PRS + 2 * (size_t)nb * RK + DMAX * TVS + 2 * (TB + 2) +
-            2 * (size_t)((nlev + 3) & ~1)) *
-           sizeof(double);
+    (void)nb;
+    return ((size_t)nlev * YS + 8 * 8 * 32 + 2 * 8 * 32 + 8 * 32 + 8 * 32 + 32 + 16 * SGS + es_len(nlev)) * sizeof(double);
 }
 
 }  // namespace
@@ -731,6 +774,8 @@ void hodlr_sweep(fi_ctx* ctx, HodlrData* h, const fi_system* sys, const double* 
     a.xg = h->xg.p;
     a.proj = h->proj.p;
     a.skip = skip;
+    static const int dbg = std::getenv("FI_HODLR_DBG") ? std::atoi(std::getenv("FI_HODLR_DBG")) : 0;
+    a.dbg = dbg;
     static const bool tracing = std::getenv("FI_HODLR_TRACE") != nullptr;
     DevBuf<unsigned long long> trace;
     a.trace = nullptr;
@@ -750,8 +795,8 @@ void hodlr_sweep(fi_ctx* ctx, HodlrData* h, const fi_system* sys, const double* 
         FI_CUDA(cudaMemcpyAsync(hv, trace.p, sizeof(hv), cudaMemcpyDeviceToHost, ctx->stream));
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
         std::fprintf(stderr,
-                     "[hodlr_sweep] kcycles/level: x %.2f | proj+release %.2f | history %.2f | wait %.2f | stage+sum %.2f | "
-                     "y %.2f | loop %.2f\n",
+                     "[hodlr_sweep] kcycles/level: x+publish %.2f | own leaf+history %.2f | poll %.2f | segments+barrier %.2f | "
+                     "low-rank y+barrier %.2f | y %.2f | loop %.2f\n",
                      hv[0] * 1e-3 / levels, hv[1] * 1e-3 / levels, hv[2] * 1e-3 / levels, hv[3] * 1e-3 / levels,
                      hv[4] * 1e-3 / levels, hv[5] * 1e-3 / levels, hv[7] * 1e-3 / levels);
     }
