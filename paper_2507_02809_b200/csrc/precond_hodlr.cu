@@ -505,14 +505,15 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
             if (leaf_remote) {
                 xr[lane] = __longlong_as_double((long long)xb);
                 __syncwarp();
-                ypart = row_sums(xr);
             }
         }
         load_quarter(lv + 1, 2);
         load_quarter(lv + 1, 3);
         __syncthreads();
         stamp(3);
-        // ---- low-rank terms: the depth's summed partials t (lane: t[4 kq .. 4 kq + 3]), y += C t
+        // ---- the remote leaf half (its x just polled) and the low-rank terms: the depth's summed
+        // partials t (lane: t[4 kq .. 4 kq + 3]), y += C t
+        if (leaf_remote) ypart = row_sums(xr);
         if (lowrank) {
             double4 tv = make_double4(0.0, 0.0, 0.0, 0.0);
             for (int gg = s_gfirst[dep]; gg < s_gfirst[dep + 1]; ++gg) {
