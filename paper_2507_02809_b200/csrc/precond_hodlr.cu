@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     unsigned segend_mask = 0;
     for (int sg = 0; sg < w_nseg[w]; ++sg) segend_mask |= 1u << (w_segend[w][sg] - 1);
     const int gfirst_w = w_nseg[w] > 0 ? w_segg[w][0] : 0;
+    const int w_nseg_w = w_nseg[w];
     const int dep = w - 1;  // depth of a low-rank warp (w >= 2)
     const bool lowrank = w >= 2 && dep <= D && s_node[dep] >= 0;
     const bool leaf_remote = w < 2 && w != own_half;
@@ -406,15 +407,33 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         // ---- partial projection V^T x / Q^T x of the CTA's rows (low-rank warps), published
         if (lowrank) {
             const double* xv = xw + w * 32 + 8 * g;
-            double P[4] = {0.0, 0.0, 0.0, 0.0};
+            // two independent chains per column (rows 0-3 and 4-7): half the dependent-FMA depth
+            double P[4], P2[4];
+            {
+                const double x0 = xv[0], x4 = xv[4];
+                P[0] = cur[0].x * x0;
+                P[1] = cur[0].y * x0;
+                P[2] = cur[1].x * x0;
+                P[3] = cur[1].y * x0;
+                P2[0] = cur[8].x * x4;
+                P2[1] = cur[8].y * x4;
+                P2[2] = cur[9].x * x4;
+                P2[3] = cur[9].y * x4;
+            }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const double xi = xv[i];
+            for (int i = 1; i < 4; ++i) {
+                const double xi = xv[i], xj = xv[i + 4];
                 P[0] = fma(cur[2 * i].x, xi, P[0]);
                 P[1] = fma(cur[2 * i].y, xi, P[1]);
                 P[2] = fma(cur[2 * i + 1].x, xi, P[2]);
                 P[3] = fma(cur[2 * i + 1].y, xi, P[3]);
+                P2[0] = fma(cur[2 * i + 8].x, xj, P2[0]);
+                P2[1] = fma(cur[2 * i + 8].y, xj, P2[1]);
+                P2[2] = fma(cur[2 * i + 9].x, xj, P2[2]);
+                P2[3] = fma(cur[2 * i + 9].y, xj, P2[3]);
             }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) P[q] += P2[q];
             const bool hi = lane & 16, lo = lane & 8;
             const double q0 = (hi ? P[2] : P[0]) + __shfl_xor_sync(0xffffffffu, hi ? P[0] : P[2], 16);
             const double q1 = (hi ? P[3] : P[1]) + __shfl_xor_sync(0xffffffffu, hi ? P[1] : P[3], 16);
@@ -490,16 +509,28 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
                 if (leaf_remote && (unsigned)(xb & 1ull) != tag) xb = ld_bits(a.xg + (long long)par * Np + sib_r);
             }
             stamp(2);
-            // one pass: a segment's sum is stored at its last slot (segend bit), the next starts at 0
-            double sacc = 0.0;
-            double* so = segout + gfirst_w * SGS + lane;
+            if (w_nseg_w == 1) {
+                // one segment (the usual case): a fixed pairwise tree, 4 dependent adds instead of 16
+                double v[MAXQ];
 #pragma unroll
-            for (int u = 0; u < MAXQ; ++u) {
-                if (u < wq) sacc += __longlong_as_double((long long)bv[u]);
-                if ((segend_mask >> u) & 1u) {
-                    *so = sacc;
-                    so += SGS;
-                    sacc = 0.0;
+                for (int u = 0; u < MAXQ; ++u) v[u] = u < wq ? __longlong_as_double((long long)bv[u]) : 0.0;
+#pragma unroll
+                for (int h = MAXQ / 2; h >= 1; h >>= 1)
+#pragma unroll
+                    for (int u = 0; u < h; ++u) v[u] += v[u + h];
+                segout[gfirst_w * SGS + lane] = v[0];
+            } else {
+                // one pass: a segment's sum is stored at its last slot (segend bit), the next starts at 0
+                double sacc = 0.0;
+                double* so = segout + gfirst_w * SGS + lane;
+#pragma unroll
+                for (int u = 0; u < MAXQ; ++u) {
+                    if (u < wq) sacc += __longlong_as_double((long long)bv[u]);
+                    if ((segend_mask >> u) & 1u) {
+                        *so = sacc;
+                        so += SGS;
+                        sacc = 0.0;
+                    }
                 }
             }
             if (leaf_remote) {
@@ -532,12 +563,15 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         __syncthreads();
         stamp(4);
         // ---- y of the CTA's rows (lane = row): the eight warps' contributions in fixed order
-        double y = 0.0, hr = 0.0;
+        double yv[8], hv[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            y += ycon[q * 32 + lane];
-            hr += hps[par * 256 + q * 32 + lane];
+            yv[q] = ycon[q * 32 + lane];
+            hv[q] = hps[par * 256 + q * 32 + lane];
         }
+        // fixed pairwise order (identical in every warp)
+        double y = ((yv[0] + yv[1]) + (yv[2] + yv[3])) + ((yv[4] + yv[5]) + (yv[6] + yv[7]));
+        const double hr = ((hv[0] + hv[1]) + (hv[2] + hv[3])) + ((hv[4] + hv[5]) + (hv[6] + hv[7]));
         if (prow) y = 0.0;
         yh[(long long)lv * YS + lane] = y;  // (every warp writes the same value)
         if (w == 0) a.y[(long long)lv * Np + row] = y;
