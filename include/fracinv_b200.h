@@ -70,6 +70,10 @@ int fi_time_grid(double beta, int S, double T, double* dt, double* eta);/* numer
 int fi_symbol_coeffs_1d(double omega, int n, double* coeffs);
 /* coeffs: prod(2n_i-1) entries, lexicographic (symbol.cpp:112-191). d in {1,2}. */
 int fi_symbol_coeffs_md(double omega, int d, const int* n, long long sample_cap, double* coeffs);
+/* The same on the device of ctx (d = 2: the two cosine-sum stages as CUDA kernels, sums in the host's
+ * order without FMA contraction: bit-for-bit fi_symbol_coeffs_md; d = 1 falls back to the host).
+ * SURVEY 8(f) row 2; coeffs is a host array. */
+int fi_symbol_coeffs_md_dev(fi_ctx* ctx, double omega, int d, const int* n, long long sample_cap, double* coeffs);
 /* Gaussian relative-L2 noise (EXTENSION for BASELINE.json; SplitMix64-at-index + Box-Muller)
  * and the reference's additive uniform noise (system.cpp:240-251). out may alias mu. */
 int fi_add_gaussian_noise(const double* mu, long long n, double rel_eps, unsigned long long seed, double* out);

@@ -15,6 +15,7 @@ void l1_weights(double beta, int S, double* b, double* e);
 void time_grid(double beta, int S, double T, double* dt, double* eta);
 void symbol_coeffs_1d(double omega, int n, double* coeffs);
 void symbol_coeffs_md(double omega, int d, const int* n, long long sample_cap, double* coeffs);
+void symbol_coeffs_2d_dev(fi_ctx* ctx, double omega, int n1, int n2, long long sample_cap, double* coeffs);
 void add_noise(const double* mu, long long n, double eps, uint64_t seed, double* out);
 void add_gaussian_noise(const double* mu, long long n, double rel_eps, uint64_t seed, double* out);
 }  // namespace fib
@@ -177,6 +178,14 @@ int fi_symbol_coeffs_1d(double omega, int n, double* coeffs) {
 }
 int fi_symbol_coeffs_md(double omega, int d, const int* n, long long sample_cap, double* coeffs) {
     return guard([&] { fib::symbol_coeffs_md(omega, d, n, sample_cap <= 0 ? (1LL << 26) : sample_cap, coeffs); });
+}
+int fi_symbol_coeffs_md_dev(fi_ctx* ctx, double omega, int d, const int* n, long long sample_cap, double* coeffs) {
+    return guard([&] {
+        require(ctx && n && coeffs, FI_E_DOMAIN, "fi_symbol_coeffs_md_dev: NULL argument");
+        const long long cap = sample_cap <= 0 ? (1LL << 26) : sample_cap;
+        if (d == 2) fib::symbol_coeffs_2d_dev(ctx, omega, n[0], n[1], cap, coeffs);
+        else fib::symbol_coeffs_md(omega, d, n, cap, coeffs);  // d = 1: the host sum (1D uses the recursion)
+    });
 }
 int fi_add_gaussian_noise(const double* mu, long long n, double rel_eps, unsigned long long seed, double* out) {
     return guard([&] { fib::add_gaussian_noise(mu, n, rel_eps, seed, out); });

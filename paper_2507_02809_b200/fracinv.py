@@ -249,14 +249,19 @@ def symbol_coeffs_1d(omega: float, n: int) -> SymbolCoefficients:
     return SymbolCoefficients(omega, [n], out)
 
 
-def symbol_coeffs_md(omega: float, n: Sequence[int], sample_cap: int = 1 << 26) -> SymbolCoefficients:
-    """symbol.hpp:58-64."""
+def symbol_coeffs_md(omega: float, n: Sequence[int], sample_cap: int = 1 << 26,
+                     ctx: Optional["Context"] = None) -> SymbolCoefficients:
+    """symbol.hpp:58-64.  ctx given (2D): the cosine sums run on that context's device, bit-for-bit
+    the host result (fi_symbol_coeffs_md_dev)."""
     n = [int(v) for v in n]
     if any(v < 1 for v in n):
         raise ValueError("symbol_coeffs_md requires n_i >= 1")
     out = np.empty(int(np.prod([2 * v - 1 for v in n])))
     narr = (ctypes.c_int * len(n))(*n)
-    _check(lib.fi_symbol_coeffs_md(float(omega), len(n), narr, int(sample_cap), _dp(out)))
+    if ctx is not None:
+        _check(lib.fi_symbol_coeffs_md_dev(ctx.handle, float(omega), len(n), narr, int(sample_cap), _dp(out)))
+    else:
+        _check(lib.fi_symbol_coeffs_md(float(omega), len(n), narr, int(sample_cap), _dp(out)))
     return SymbolCoefficients(omega, n, out)
 
 
@@ -362,7 +367,7 @@ class SystemOperator:
         self.weights = l1_weights(spec.orders.beta, self.S)
         if symbol is None:
             symbol = (symbol_coeffs_1d(spec.orders.omega, spec.sgrid.n[0]) if spec.sgrid.d == 1
-                      else symbol_coeffs_md(spec.orders.omega, spec.sgrid.n))
+                      else symbol_coeffs_md(spec.orders.omega, spec.sgrid.n, ctx=self.ctx))
         self.symbol = symbol
         self.q = np.array([float(spec.q(s * spec.tgrid.dt)) for s in range(1, self.S + 1)])
         if spec.rho.size != self.N or spec.f_true.size != self.N:
