@@ -12,6 +12,8 @@
 // Every kernel of an enqueued iteration checks a device `done` flag, so a whole restart
 // cycle is enqueued without host synchronisation; the host reads the state once per cycle.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 
@@ -297,6 +299,12 @@ double GmresEngine::norm2(const double* v, int slot) {
 void GmresEngine::solve(const Op& A, const Op* M, const double* b, const double* x0, double* x, double tol, int maxit,
                         int restart, fi_gmres_report* rep, std::vector<double>& history) {
     const auto t_start = std::chrono::steady_clock::now();
+    static const bool htrace = std::getenv("FI_GMRES_HOSTTRACE") != nullptr;
+    auto hstamp = [&](const char* what) {
+        if (htrace)
+            std::fprintf(stderr, "[gmres host] %-14s %8.3f ms\n", what,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+    };
     if (!(tol > 0.0)) throw Error(FI_E_DOMAIN, "gmres requires tol > 0");
     const long long n = n_;
     if (maxit <= 0) maxit = (int)std::min<long long>(n, 0x7fffffff);
@@ -305,13 +313,17 @@ void GmresEngine::solve(const Op& A, const Op* M, const double* b, const double*
     const int blocks = ctx_->sm_count * 4;
 
     // basis V (cycle + 1 vectors) + work vectors
-    const size_t need = ((size_t)cycle + 1 + 3) * (size_t)n * sizeof(double);
-    size_t free_b = 0, total_b = 0;
-    FI_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    if (need > free_b)
-        throw Error(FI_E_RESOURCE, "gmres: Krylov basis of " + std::to_string(cycle + 1) + " vectors (" +
-                                       std::to_string(need) + " bytes) exceeds free device memory; use restart");
     const long long ldv = (n + 1) & ~1LL;
+    if (V_.n < (size_t)(cycle + 1) * ldv) {
+        // (only when the workspace must grow: cudaMemGetInfo costs milliseconds of host time, which
+        // would idle the GPU at the start of every solve)
+        const size_t need = ((size_t)cycle + 1 + 3) * (size_t)n * sizeof(double);
+        size_t free_b = 0, total_b = 0;
+        FI_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        if (need > free_b + V_.bytes() + w_.bytes() + t1_.bytes() + t2_.bytes())
+            throw Error(FI_E_RESOURCE, "gmres: Krylov basis of " + std::to_string(cycle + 1) + " vectors (" +
+                                           std::to_string(need) + " bytes) exceeds free device memory; use restart");
+    }
     // workspaces persist across solves (no cudaMalloc/cudaFree inside a timed solve)
     DevBuf<double>&V = V_, &w = w_, &t1 = t1_, &t2 = t2_, &hist_d = hist_, &arr = arr_, &ycoef = ycoef_;
     DevBuf<GmresState>& st_d = st_buf_;
@@ -342,7 +354,9 @@ void GmresEngine::solve(const Op& A, const Op* M, const double* b, const double*
         FI_CUDA(cudaMemcpyAsync(&hs, st_d.p, sizeof(GmresState), cudaMemcpyDeviceToHost, s));
         FI_CUDA(cudaStreamSynchronize(s));
     };
+    hstamp("workspaces");
     upload_state();
+    hstamp("upload_state");
 
     auto precondition = [&](const double* in, double* out) {
         if (M) (*M)(in, out, nullptr);
@@ -353,7 +367,9 @@ void GmresEngine::solve(const Op& A, const Op* M, const double* b, const double*
     // pb = M^{-1} b ; bnorm
     double* pb = V.p;  // V_0 receives r0 / beta below
     precondition(b, pb);
+    hstamp("precondition");
     const double bnorm = std::sqrt(norm2(pb, 0));
+    hstamp("bnorm");
     const double bnorm_true = std::sqrt(norm2(b, 1));
     if (bnorm == 0.0) {
         FI_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
