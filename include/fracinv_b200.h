@@ -175,6 +175,12 @@ typedef struct {
 int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x0_dev, double* x_dev,
              const fi_gmres_opts* opts, fi_gmres_report* report, double* history_host, int history_cap);
 /* Host-buffer variant: H2D of b (and x0), solve, D2H of x — the reference-facing call. */
+/* Arnoldi step of fi_gmres / fi_gmres_host with a system preconditioner: on = 1 (default) computes
+ * P^{-1} A v as v + P^{-1}((A - P) v) — A and P differ only in the f column of the time rows,
+ * -eta q_s I (spectra.cpp:34-36), so one preconditioner sweep and no operator apply per step (an exact
+ * identity, cf. Eisenstat's trick); on = 0: A v by K1, then P^{-1} (the reference's order of
+ * operations, krylov.cpp:123-126).  Environment FI_SPLIT_APPLY=0 forces 0. */
+int fi_system_set_split_apply(fi_system* sys, int on);
 int fi_gmres_host(fi_system* sys, fi_precond* P, const double* b_host, const double* x0_host, double* x_host,
                   const fi_gmres_opts* opts, fi_gmres_report* report, double* history_host, int history_cap);
 

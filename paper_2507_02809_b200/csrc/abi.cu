@@ -491,12 +491,33 @@ int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x
         // maxit = 0 selects the matrix dimension (krylov.hpp:56), i.e. the reference's n
         const int maxit = opts->maxit > 0 ? opts->maxit : (int)std::min<long long>(L.nRef(), 0x7fffffff);
         if (!sys->engine) sys->engine = new fib::GmresEngine(ctx, n);
+        // optional split apply: P^{-1} A v = v + P^{-1}((A - P) v), one sweep per Arnoldi step
+        static const bool split_env = !(std::getenv("FI_SPLIT_APPLY") && std::atoi(std::getenv("FI_SPLIT_APPLY")) == 0);
+        const bool split = split_env && sys->split_apply;
+        fib::Op Fz = [ctx, P, sys](const double* in, double* out, const int* skip) {
+            fib::precond_times_operator(ctx, P, in, out, sys->sp_u.p, sys->sp_t.p, skip);
+        };
+        if (split && P) {
+            if (sys->sp_u.n < (size_t)n) {
+                sys->sp_u.alloc((size_t)n);
+                sys->sp_t.alloc((size_t)n);
+            }
+        }
+        sys->engine->set_fused(split && P ? &Fz : nullptr);
         std::vector<double> hist;
         sys->engine->solve(A, P ? &M : nullptr, b.p, x0_dev ? x0.p : nullptr, x.p, opts->tol, maxit, opts->restart,
                            report, hist);
+        sys->engine->set_fused(nullptr);
         fib::unpack_vector(ctx, L, x.p, x_dev);
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
         copy_history(hist, history_host, history_cap);
+    });
+}
+
+int fi_system_set_split_apply(fi_system* sys, int on) {
+    return guard([&] {
+        require(sys, FI_E_DOMAIN, "fi_system_set_split_apply: NULL system");
+        sys->split_apply = on ? 1 : 0;
     });
 }
 

@@ -446,7 +446,9 @@ void GmresEngine::solve(const Op& A, const Op* M, const double* b, const double*
                 if (*(volatile int*)done_host_) break;
             }
             const double* vk = V.p + (long long)k * ldv;
-            if (M) {
+            if (M && fused_) {
+                (*fused_)(vk, w.p, done);
+            } else if (M) {
                 A(vk, t1.p, done);
                 (*M)(t1.p, w.p, done);
             } else {

@@ -45,6 +45,8 @@ public:
     GmresEngine& operator=(const GmresEngine&) = delete;
     long long n() const { return n_; }
     // Reference semantics of gmres() (krylov.cpp:72-209) + restart extension.
+    // optional: w = M^{-1} A v in one operation (used for the Arnoldi step instead of A then M)
+    void set_fused(const Op* f) { fused_ = f; }
     void solve(const Op& A, const Op* M, const double* b, const double* x0, double* x, double tol, int maxit,
                int restart, fi_gmres_report* rep, std::vector<double>& history);
 
@@ -67,6 +69,7 @@ private:
     DevBuf<double> V_, w_, t1_, t2_, hist_, arr_, ycoef_;
     DevBuf<GmresState> st_buf_;
     static constexpr int kLook = 2;  // Arnoldi steps kept queued ahead of the host's convergence check
+    const Op* fused_ = nullptr;
     int* done_host_ = nullptr;       // pinned, host-mapped copy of the device `done` flag
     int* done_hmap_ = nullptr;       // its device alias
     cudaEvent_t iter_ev_[kLook] = {};

@@ -51,6 +51,9 @@ constexpr int kCounterStride = 32;
 // y = P^{-1} z on padded vectors (K2).  levels = S+1 (full P) or S (time levels only:
 // the forward solve, system.cpp:192-224).  skip: optional device flag.
 void precond_apply(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip);
+// w = P^{-1} A v = v + P^{-1}((A - P) v) (one sweep, no operator apply); u, t: padded scratch vectors
+void precond_times_operator(fi_ctx* ctx, fi_precond* P, const double* v, double* w, double* u, double* t,
+                            const int* skip);
 // mode 1 (2D blocks above the dense cap): build / apply of the tau-PCG per-level solve
 bool iterative_supported(const Layout& L);
 void precond_build_iterative(fi_precond* P, double tol, int maxit);

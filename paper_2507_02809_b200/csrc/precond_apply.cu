@@ -474,6 +474,25 @@ __global__ void axpy_kernel(double* y, const double* d, long long n, const int* 
         y[i] += d[i];
 }
 
+// (A - P) v: the only block where the operator and its block lower-triangular preconditioner differ
+// is the f column of the time rows, -eta q_s I (spectra.cpp:34-36); u_s = -eta q_s f_v, u_f = 0.
+__global__ void coupling_kernel(const double* __restrict__ v, double* __restrict__ u, const double* __restrict__ q,
+                                double eta, int S, long long Np, const int* skip) {
+    if (skip && *skip) return;
+    const long long n = (long long)(S + 1) * Np;
+    const double* f = v + (long long)S * Np;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long s = i / Np, j = i - s * Np;
+        u[i] = s < S ? -eta * q[s] * f[j] : 0.0;
+    }
+}
+__global__ void add_kernel(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out,
+                           long long n, const int* skip) {
+    if (skip && *skip) return;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = a[i] + b[i];
+}
+
 template <typename T>
 void launch_sweep(fi_ctx* ctx, fi_precond* P, const T* H, const double* z, double* y, int levels, int refine_f,
                   const int* skip) {
@@ -574,6 +593,19 @@ int precond_apply_grid(fi_ctx* ctx, long long T, long long Np) {
         throw Error(FI_E_RESOURCE, "precond sweep: block of " + std::to_string(Np) + " rows needs " +
                                        std::to_string(G) + " resident CTAs");
     return (int)G;
+}
+
+// w = P^{-1} A v computed as v + P^{-1} ((A - P) v): one sweep and no operator apply (the identity is
+// exact; the rounding differs from P^{-1}(A v) at the level of the sweep's own accuracy).  u, t: scratch.
+void precond_times_operator(fi_ctx* ctx, fi_precond* P, const double* v, double* w, double* u, double* t,
+                            const int* skip) {
+    const fi_system* sys = P->sys;
+    const long long n = sys->L.nI();
+    coupling_kernel<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(v, u, sys->q.p, sys->eta, sys->L.S, sys->L.Np, skip);
+    FI_LAUNCHED(ctx);
+    precond_apply(ctx, P, u, t, sys->L.S + 1, skip);
+    add_kernel<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(v, t, w, n, skip);
+    FI_LAUNCHED(ctx);
 }
 
 void precond_apply(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip) {

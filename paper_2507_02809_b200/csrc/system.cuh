@@ -34,6 +34,8 @@ struct fi_system {
     fib::DevBuf<double> gen, epad, D1, D2, q, e, bw;
     fib::DevBuf<double> ubuf, zbuf;  // padded scratch for reference-layout applies
     fib::DevBuf<double> gb, gx, gx0, gio;  // fi_gmres padded b / x / x0 and host-call staging
+    fib::DevBuf<double> sp_u, sp_t;        // scratch of the split preconditioned apply
+    int split_apply = 1;                   // fi_gmres: P^{-1} A v as v + P^{-1}((A - P) v) (fi_system_set_split_apply)
     fib::GmresEngine* engine = nullptr;  // cached Krylov workspace (owned; freed in fi_system_destroy)
     fib::OperatorView view() const {
         fib::OperatorView v;

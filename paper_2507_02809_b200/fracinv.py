@@ -393,6 +393,11 @@ class SystemOperator:
         self.handle = h
         self._keep = None
 
+    def set_split_apply(self, on: bool):
+        """Arnoldi steps of gmres(self, P, ...) compute P^{-1} A v as v + P^{-1}((A - P) v) (default, one
+        sweep per step) or as K1 then P^{-1} (the reference's order) — fi_system_set_split_apply."""
+        _check(lib.fi_system_set_split_apply(self.handle, 1 if on else 0))
+
     # reference accessors
     def space_dim(self) -> int:
         return self.N

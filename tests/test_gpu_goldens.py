@@ -38,3 +38,21 @@ def test_solve_matches_oracle_golden(cfg):
     h, ho = np.asarray(rep.residual_history), np.asarray(g["history"])
     k = min(len(h), len(ho))
     assert np.allclose(h[:k], ho[:k], rtol=1e-4, atol=1e-14)
+
+
+@pytest.mark.parametrize("cfg", [0, 2])
+def test_split_apply_matches_operator_then_precond(cfg):
+    """The default Arnoldi step P^-1 A v = v + P^-1((A - P) v) against the reference's order (K1, then
+    P^-1): same iteration count, residual histories to 1e-6, solutions to 1e-10."""
+    g = np.load(os.path.join(GOLDEN, f"oracle_config{cfg}.npz"))
+    A = F.SystemOperator(baseline_problem(F, cfg))
+    P = F.BlockTriangularPreconditioner(A)
+    z = F.build_rhs(A, g["mu_eps"]).z
+    opts = F.GmresOptions(TOL[cfg], 0, RESTART)
+    x1, r1 = F.gmres(A, P, z, opts)
+    A.set_split_apply(False)
+    x2, r2 = F.gmres(A, P, z, opts)
+    A.set_split_apply(True)
+    assert r1.iterations == r2.iterations
+    assert np.allclose(r1.residual_history, r2.residual_history, rtol=1e-6, atol=1e-15)
+    assert _rel(x1, x2) <= 1e-10
