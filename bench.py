@@ -401,7 +401,11 @@ def run_ours(args):
                          "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": None,
                          "bytes_per_launch": sweep_bytes, "ms_per_launch": round(ms_sweep, 4),
-                         "us_per_level": round(ms_sweep * 1e3 / (S + 1), 3), "precond_form": form,
+                         "us_per_level": round(ms_sweep * 1e3 / (S + 1), 3),
+                         # the level chain's floor: one all-to-all exchange round among the sweep's 128
+                         # CTAs, 1785 cycles = 0.91 us at 1965 MHz (tools/xchg_latency.cu,
+                         # profiles/xchg_latency_r01.txt)
+                         "exchange_floor_us_per_level": 0.908, "precond_form": form,
                          "peak_source": peak_src},
             "roofline_operator": {"bound": "tensor", "kernel": "toeplitz_apply_kernel (K1, FP64 DMMA)",
                                   "achieved": round(op_tflops, 3), "peak": FP64_DMMA_PEAK_TFLOPS,
