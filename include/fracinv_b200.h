@@ -175,6 +175,10 @@ typedef struct {
 int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x0_dev, double* x_dev,
              const fi_gmres_opts* opts, fi_gmres_report* report, double* history_host, int history_cap);
 /* Host-buffer variant: H2D of b (and x0), solve, D2H of x — the reference-facing call. */
+/* Dense realisation (spectra.cpp:14-45, verification only): kind 0 = SystemA, 1 = PreconditionerP,
+ * 2 = ForwardAhat; row-major dim x dim into device memory M_dev (dim = (S+1)N, or S N for Ahat);
+ * FI_E_RESOURCE above cap (<= 0: 4096).  Bit-for-bit the reference's entries. */
+int fi_assemble_dense(fi_system* sys, int kind, long long cap, double* M_dev);
 /* Arnoldi step of fi_gmres / fi_gmres_host with a system preconditioner: on = 1 (default) computes
  * P^{-1} A v as v + P^{-1}((A - P) v) — A and P differ only in the f column of the time rows,
  * -eta q_s I (spectra.cpp:34-36), so one preconditioner sweep and no operator apply per step (an exact

@@ -16,6 +16,7 @@ void time_grid(double beta, int S, double T, double* dt, double* eta);
 void symbol_coeffs_1d(double omega, int n, double* coeffs);
 void symbol_coeffs_md(double omega, int d, const int* n, long long sample_cap, double* coeffs);
 void symbol_coeffs_2d_dev(fi_ctx* ctx, double omega, int n1, int n2, long long sample_cap, double* coeffs);
+void assemble_dense(fi_ctx* ctx, const fi_system* sys, int kind, long long cap, double* M);
 void add_noise(const double* mu, long long n, double eps, uint64_t seed, double* out);
 void add_gaussian_noise(const double* mu, long long n, double rel_eps, uint64_t seed, double* out);
 }  // namespace fib
@@ -511,6 +512,13 @@ int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x
         fib::unpack_vector(ctx, L, x.p, x_dev);
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
         copy_history(hist, history_host, history_cap);
+    });
+}
+
+int fi_assemble_dense(fi_system* sys, int kind, long long cap, double* M_dev) {
+    return guard([&] {
+        require(sys && M_dev, FI_E_DOMAIN, "fi_assemble_dense: NULL argument");
+        fib::assemble_dense(sys->ctx, sys, kind, cap <= 0 ? 4096 : cap, M_dev);
     });
 }
 
