@@ -545,6 +545,8 @@ def forward_solve(A: SystemOperator, f_source: Optional[np.ndarray] = None,
     eta = A.spec.tgrid.eta
     f = A.spec.f_true if f_source is None else f_source
     Bd = A.laplacian.dense(N) if P is None else None
+    if P is not None and P.inner == "pcg":
+        P.pcg.dropped = False
     states: List[np.ndarray] = []
     for s in range(1, S + 1):
         d1 = A.diags.D1[s - 1]
@@ -553,7 +555,7 @@ def forward_solve(A: SystemOperator, f_source: Optional[np.ndarray] = None,
         for m in range(1, s):
             rhs = rhs - e[s - m] * (d1 * states[m - 1])
         if P is not None:
-            states.append(P.solve_block(s, rhs))
+            states.append(P.solve_block(s, rhs, [states[s - 1 - k] for k in range(1, min(3, s - 1) + 1)]))
             continue
         blk = A.scale_space * d2[:, None] * Bd
         blk[np.diag_indices(N)] += e[0] * d1
@@ -712,9 +714,19 @@ class BlockTriangularPreconditioner:
             return self.factors[s - 1]
         return _lu_checked(self.block(s), s, "precond_build")
 
-    def solve_block(self, s: int, rhs: np.ndarray) -> np.ndarray:
+    def solve_block(self, s: int, rhs: np.ndarray, prev: Optional[Sequence[np.ndarray]] = None) -> np.ndarray:
+        """prev: the solutions of the preceding time levels, latest first (tau-PCG only: their
+        constant / linear / quadratic extrapolation is the initial guess, as on the device)."""
         if self.inner == "pcg":
-            return self.pcg.solve(s, rhs)
+            x0 = None
+            if prev and s <= self.S and self.pcg.warm and not self.pcg.dropped:
+                if len(prev) == 1:
+                    x0 = prev[0].copy()
+                elif len(prev) == 2:
+                    x0 = 2.0 * prev[0] - prev[1]
+                else:
+                    x0 = (3.0 * prev[0] - 3.0 * prev[1]) + prev[2]
+            return self.pcg.solve(s, rhs, x0)
         return sla.lu_solve(self._factor(s), rhs, check_finite=False)
 
     def apply(self, z: np.ndarray) -> np.ndarray:
@@ -727,12 +739,14 @@ class BlockTriangularPreconditioner:
         e = self.A.weights.e
         y = np.empty(self.dim)
         Y = y[: S * N].reshape(S, N)
+        if self.inner == "pcg":
+            self.pcg.dropped = False
         for s in range(1, S + 1):
             rhs = z[(s - 1) * N: s * N].copy()
             if s > 1:
                 acc = e[s - 1:0:-1] @ Y[: s - 1]  # sum_{m<s} e_{s-m} y^(m)
                 rhs -= self.A.diags.D1[s - 1] * acc
-            Y[s - 1] = self.solve_block(s, rhs)
+            Y[s - 1] = self.solve_block(s, rhs, [Y[s - 1 - k] for k in range(1, min(3, s - 1) + 1)])
         rhs = z[S * N:] - Y[S - 1]
         y[S * N:] = self.solve_block(S + 1, rhs)
         return y
@@ -763,6 +777,8 @@ class TauPCG:
             acc = acc + (4.0 * np.sin(t / 2.0) ** 2).reshape(shape)
         self.g = np.power(acc, A.spec.orders.omega / 2.0)
         self.iterations = []
+        self.warm = True  # extrapolated initial guesses for the time levels (the device's FI_TAU_WARM=1)
+        self.dropped = False  # set when a guess was worse than zero: no guesses for the rest of the apply
         S, N = A.steps, A.space_dim
         e0 = A.weights.e[0]
         for s in range(1, S + 1):
@@ -780,7 +796,10 @@ class TauPCG:
         X /= lam
         return self.sf.idstn(X, type=1, norm="ortho").reshape(-1)
 
-    def solve(self, s: int, rhs: np.ndarray) -> np.ndarray:
+    def solve(self, s: int, rhs: np.ndarray, x0: Optional[np.ndarray] = None) -> np.ndarray:
+        """x0 (time levels, EXTENSION identical to the device): an initial guess.  A pre-step sets
+        x = x0, r = b - M x0; the level is done if ||r|| <= tol ||b||, and a guess with ||r|| > ||b||
+        is dropped (x = 0, r = b) before the tau-preconditioned iteration starts."""
         A = self.A
         S = A.steps
         e0 = A.weights.e[0]
@@ -801,6 +820,16 @@ class TauPCG:
             self.iterations.append(0)
             return x
         r = b.copy()
+        if x0 is not None and s <= S:
+            x = x0.copy()
+            r = b - M(x0)
+            if np.linalg.norm(r) <= self.tol * bn:
+                self.iterations.append(0)
+                return x
+            if float(r @ r) > float(b @ b):
+                x = np.zeros_like(b)
+                r = b.copy()
+                self.dropped = True
         z = self._tau_inv(r, lam)
         p = z.copy()
         rz = float(r @ z)

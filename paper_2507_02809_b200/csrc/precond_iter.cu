@@ -48,6 +48,7 @@ struct ItArgs {
     double2* X;   // L1 x L2 complex work
     double* Rr;   // n1 x n2 real DST work
     const int* skip;
+    int warm;    // extrapolated initial guesses for the time levels (FI_TAU_WARM, default 1)
 };
 
 __device__ __forceinline__ bool skipped(const ItArgs& a) { return a.skip && *a.skip; }
@@ -416,9 +417,113 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         return part;
     };
 
+    // the three passes of a CG step (B1 rows, B2 columns, B3 rows; grid barriers between them are the
+    // caller's).  B1 returns the partial p.delta.p, B2 the partial p.Bp (Parseval), B3 the partial ||r||^2.
+    auto passB1 = [&](int lv, int it, double beta) -> double {
+        const long long lo_lv = (long long)min(lv, a.S - 1) * Np;
+        // B1: p = zz + beta p (after the first step), row FFT of the embedded p; partial delta p.p
+        double pdp = 0.0;
+        if (nr > 0) {
+            for (int q = tid; q < nr * a.L2; q += nthr) {
+                const int i = q >> a.lg2, j = q & (a.L2 - 1);
+                double val = 0.0;
+                if (j < a.n2) {
+                    const long long o = (long long)(r0 + i) * a.ld2 + j;
+                    val = a.p[o];
+                    if (it > 0) {
+                        val = a.zz[o] + beta * val;
+                        a.p[o] = val;
+                    }
+                    if (lv < a.S) pdp += a.e0 * a.D1[lo_lv + o] * a.d2inv[lo_lv + o] * val * val;
+                }
+                u[q] = make_double2(val, 0.0);
+            }
+            __syncthreads();
+            const double2* U = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, false, tid, nthr);
+            double2* Xr = a.X + (long long)r0 * a.L2;
+            for (int q = tid; q < nr * a.L2; q += nthr) Xr[q] = U[q];
+            __syncthreads();
+        }
+        return pdp;
+    };
+    auto passB2 = [&]() -> double {
+        // B2: column FFT, times the circulant spectrum, inverse column FFT.  By Parseval the
+        // spectrum also gives p.Bp = sum lam |P^|^2 / (L1 L2), so p.Ap = c p.Bp + p.delta.p is
+        // known here and the inverse row pass can update x and r at once.
+        double pbp = 0.0;
+        for (int g = cta; g < a.L2 / cbf; g += G) {
+            const int k0 = g * cbf;
+            // element q = (row j, column cc) with the column fastest: cbf adjacent values per row
+            double lamv[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int q = tid + t * nthr;
+                const int cc = q & (cbf - 1), j = q >> lgc;
+                if (q < cbf * a.L1) {
+                    u[cc * a.L1 + j] = a.X[(long long)j * a.L2 + k0 + cc];
+                    lamv[t] = a.lamB[(long long)j * a.L2 + k0 + cc];
+                }
+            }
+            __syncthreads();
+            double2* U = fft4_smem(u, v, cbf, a.L1, a.lg1, tws1, false, tid, nthr);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int q = tid + t * nthr;
+                const int cc = q & (cbf - 1), j = q >> lgc;
+                if (q < cbf * a.L1) {
+                    const double2 w = U[cc * a.L1 + j];
+                    pbp += lamv[t] * (w.x * w.x + w.y * w.y);
+                    U[cc * a.L1 + j] = make_double2(w.x * lamv[t], w.y * lamv[t]);
+                }
+            }
+            __syncthreads();
+            double2* W = U == u ? v : u;
+            const double2* Y = fft4_smem(U, W, cbf, a.L1, a.lg1, tws1, true, tid, nthr);
+            for (int q = tid; q < cbf * a.n1; q += nthr) {
+                const int cc = q & (cbf - 1), j = q >> lgc;
+                a.X[(long long)j * a.L2 + k0 + cc] = Y[cc * a.L1 + j];
+            }
+            __syncthreads();
+        }
+        return pbp;
+    };
+    auto passB3 = [&](int lv, double c, double alpha, double* x) -> double {
+        const long long lo_lv = (long long)min(lv, a.S - 1) * Np;
+        double part;
+        // B3: inverse row FFT, Ap = c B p + delta o p; x += alpha p, r -= alpha Ap, ||r||^2, and
+        // the DST rows of the new r (first pass of the next tau solve)
+        part = 0.0;
+        if (nr > 0) {
+            const double2* Xr = a.X + (long long)r0 * a.L2;
+            for (int q = tid; q < nr * a.L2; q += nthr) u[q] = Xr[q];
+            __syncthreads();
+            const double2* Y = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, true, tid, nthr);
+            for (int q = tid; q < nr * a.n2; q += nthr) {
+                const int i = q / a.n2, j = q - i * a.n2;
+                const long long o = (long long)(r0 + i) * a.ld2 + j;
+                const double pv = a.p[o];
+                const double delta = lv < a.S ? a.e0 * a.D1[lo_lv + o] * a.d2inv[lo_lv + o] : 0.0;
+                const double ap = c * (Y[i * a.L2 + j].x * a.inv_LL) + delta * pv;
+                x[o] += alpha * pv;
+                const double rv = a.r[o] - alpha * ap;
+                a.r[o] = rv;
+                part += rv * rv;
+            }
+            __syncthreads();
+            dst_rows(a.r, a.ld2);
+        }
+        return part;
+    };
+
+    // a guess worse than zero (||b - M x0|| > ||b||: the input is not smooth in time) switches the
+    // warm start off for the rest of the apply (the decision is grid-uniform: it uses reduced values)
+    bool warm_ok = true;
     for (int lv = 0; lv < a.levels; ++lv) {
         // ---- level setup: rhs (forward substitution, krylov.cpp:55-68), b = rhs / D2, x = 0
         const bool direct = lv < a.S && a.direct[lv];
+        // warm start: time levels after the first whose predecessors were solved by CG
+        const bool warm = a.warm && warm_ok && lv >= 1 && lv < a.S && !direct && !a.direct[lv - 1] &&
+                          (lv < 2 || !a.direct[lv - 2]) && (lv < 3 || !a.direct[lv - 3]);
         double* x = a.y + (long long)lv * Np;
         double part = 0.0;
         for (long long i = (long long)cta * nthr + tid; i < Np; i += (long long)G * nthr) {
@@ -442,8 +547,18 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                     b = rhs * a.d2inv[(long long)(a.S - 1) * Np + i];
                 }
             }
+            // initial guess of the time levels (not the f-block): the previous levels' solutions
+            // extrapolated in time (constant, linear, quadratic), passed through p to the pre-step
+            double x0 = 0.0;
+            if (warm && i2 < a.n2) {
+                const double y1 = a.y[(long long)(lv - 1) * Np + i];
+                if (lv == 1) x0 = y1;
+                else if (lv == 2) x0 = 2.0 * y1 - a.y[(long long)(lv - 2) * Np + i];
+                else x0 = (3.0 * y1 - 3.0 * a.y[(long long)(lv - 2) * Np + i]) + a.y[(long long)(lv - 3) * Np + i];
+            }
             a.r[i] = b;
-            a.p[i] = 0.0;
+            a.zz[i] = b;
+            a.p[i] = x0;
             x[i] = xv;
             part += b * b;
         }
@@ -454,8 +569,27 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         if (conv) continue;
         const double c = level_c(a, lv);
         const long long lo_lv = (long long)min(lv, a.S - 1) * Np;  // D1, 1/D2 rows of the level
+        bool from_zero = true;
+        if (warm) {
+            // pre-step with alpha = 1 along p = x0: x = x0, r = b - M x0 (and the DST rows of r)
+            passB1(lv, 0, 0.0);
+            gsync();
+            passB2();
+            gsync();
+            const double rn0 = greduce(passB3(lv, c, 1.0, x));
+            if (sqrt(rn0) <= a.tol * sqrt(bn2)) continue;  // the guess already solves the level
+            from_zero = rn0 > bn2;  // a guess worse than 0: restart from x = 0, r = b
+            if (from_zero) {
+                warm_ok = false;
+                for (long long i = (long long)cta * nthr + tid; i < Np; i += (long long)G * nthr) {
+                    a.r[i] = a.zz[i];
+                    x[i] = 0.0;
+                }
+                gsync();
+            }
+        }
         // ---- initial tau solve: zz = tau^{-1} r, p = zz, rz = r.zz
-        dst_rows(a.r, a.ld2);
+        if (from_zero) dst_rows(a.r, a.ld2);
         gsync();
         tau_cols_phase(lv);
         gsync();
@@ -464,93 +598,13 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         double beta = 0.0;
         int it = 0;
         while (true) {
-            // B1: p = zz + beta p (after the first step), row FFT of the embedded p; partial delta p.p
-            double pdp = 0.0;
-            if (nr > 0) {
-                for (int q = tid; q < nr * a.L2; q += nthr) {
-                    const int i = q >> a.lg2, j = q & (a.L2 - 1);
-                    double val = 0.0;
-                    if (j < a.n2) {
-                        const long long o = (long long)(r0 + i) * a.ld2 + j;
-                        val = a.p[o];
-                        if (it > 0) {
-                            val = a.zz[o] + beta * val;
-                            a.p[o] = val;
-                        }
-                        if (lv < a.S) pdp += a.e0 * a.D1[lo_lv + o] * a.d2inv[lo_lv + o] * val * val;
-                    }
-                    u[q] = make_double2(val, 0.0);
-                }
-                __syncthreads();
-                const double2* U = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, false, tid, nthr);
-                double2* Xr = a.X + (long long)r0 * a.L2;
-                for (int q = tid; q < nr * a.L2; q += nthr) Xr[q] = U[q];
-                __syncthreads();
-            }
+            const double pdp = passB1(lv, it, beta);
             gsync();
             stamp(2);
-            // B2: column FFT, times the circulant spectrum, inverse column FFT.  By Parseval the
-            // spectrum also gives p.Bp = sum lam |P^|^2 / (L1 L2), so p.Ap = c p.Bp + p.delta.p is
-            // known here and the inverse row pass can update x and r at once.
-            double pbp = 0.0;
-            for (int g = cta; g < a.L2 / cbf; g += G) {
-                const int k0 = g * cbf;
-                // element q = (row j, column cc) with the column fastest: cbf adjacent values per row
-                double lamv[8];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    const int q = tid + t * nthr;
-                    const int cc = q & (cbf - 1), j = q >> lgc;
-                    if (q < cbf * a.L1) {
-                        u[cc * a.L1 + j] = a.X[(long long)j * a.L2 + k0 + cc];
-                        lamv[t] = a.lamB[(long long)j * a.L2 + k0 + cc];
-                    }
-                }
-                __syncthreads();
-                double2* U = fft4_smem(u, v, cbf, a.L1, a.lg1, tws1, false, tid, nthr);
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    const int q = tid + t * nthr;
-                    const int cc = q & (cbf - 1), j = q >> lgc;
-                    if (q < cbf * a.L1) {
-                        const double2 w = U[cc * a.L1 + j];
-                        pbp += lamv[t] * (w.x * w.x + w.y * w.y);
-                        U[cc * a.L1 + j] = make_double2(w.x * lamv[t], w.y * lamv[t]);
-                    }
-                }
-                __syncthreads();
-                double2* W = U == u ? v : u;
-                const double2* Y = fft4_smem(U, W, cbf, a.L1, a.lg1, tws1, true, tid, nthr);
-                for (int q = tid; q < cbf * a.n1; q += nthr) {
-                    const int cc = q & (cbf - 1), j = q >> lgc;
-                    a.X[(long long)j * a.L2 + k0 + cc] = Y[cc * a.L1 + j];
-                }
-                __syncthreads();
-            }
+            const double pbp = passB2();
             const double alpha = rz / greduce(c * a.inv_LL * pbp + pdp);
             stamp(3);
-            // B3: inverse row FFT, Ap = c B p + delta o p; x += alpha p, r -= alpha Ap, ||r||^2, and
-            // the DST rows of the new r (first pass of the next tau solve)
-            part = 0.0;
-            if (nr > 0) {
-                const double2* Xr = a.X + (long long)r0 * a.L2;
-                for (int q = tid; q < nr * a.L2; q += nthr) u[q] = Xr[q];
-                __syncthreads();
-                const double2* Y = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, true, tid, nthr);
-                for (int q = tid; q < nr * a.n2; q += nthr) {
-                    const int i = q / a.n2, j = q - i * a.n2;
-                    const long long o = (long long)(r0 + i) * a.ld2 + j;
-                    const double pv = a.p[o];
-                    const double delta = lv < a.S ? a.e0 * a.D1[lo_lv + o] * a.d2inv[lo_lv + o] : 0.0;
-                    const double ap = c * (Y[i * a.L2 + j].x * a.inv_LL) + delta * pv;
-                    x[o] += alpha * pv;
-                    const double rv = a.r[o] - alpha * ap;
-                    a.r[o] = rv;
-                    part += rv * rv;
-                }
-                __syncthreads();
-                dst_rows(a.r, a.ld2);
-            }
+            part = passB3(lv, c, alpha, x);
             stamp(4);
             const double rn2 = greduce(part);
             stamp(5);
@@ -616,6 +670,8 @@ ItArgs make_args(fi_precond* P) {
     a.p = P->it_vec.p + 2 * Np;
     a.Ap = P->it_vec.p + 3 * Np;
     a.X = P->it_X.p;
+    static const int warm = std::getenv("FI_TAU_WARM") ? std::atoi(std::getenv("FI_TAU_WARM")) : 1;
+    a.warm = warm;
     a.Rr = P->it_Rr.p;
     return a;
 }
