@@ -555,7 +555,7 @@ def forward_solve(A: SystemOperator, f_source: Optional[np.ndarray] = None,
         for m in range(1, s):
             rhs = rhs - e[s - m] * (d1 * states[m - 1])
         if P is not None:
-            states.append(P.solve_block(s, rhs, [states[s - 1 - k] for k in range(1, min(3, s - 1) + 1)]))
+            states.append(P.solve_block(s, rhs, [states[s - 1 - k] for k in range(1, min(WARM_ORDER, s - 1) + 1)]))
             continue
         blk = A.scale_space * d2[:, None] * Bd
         blk[np.diag_indices(N)] += e[0] * d1
@@ -720,12 +720,12 @@ class BlockTriangularPreconditioner:
         if self.inner == "pcg":
             x0 = None
             if prev and s <= self.S and self.pcg.warm and not self.pcg.dropped:
-                if len(prev) == 1:
-                    x0 = prev[0].copy()
-                elif len(prev) == 2:
-                    x0 = 2.0 * prev[0] - prev[1]
-                else:
-                    x0 = (3.0 * prev[0] - 3.0 * prev[1]) + prev[2]
+                # polynomial extrapolation through the previous k levels (latest first):
+                # x0 = sum_j (-1)^(j+1) C(k, j) y_(s-j), summed in j order as on the device
+                k = len(prev)
+                x0 = np.zeros_like(prev[0])
+                for j in range(1, k + 1):
+                    x0 = x0 + float((-1) ** (j + 1) * math.comb(k, j)) * prev[j - 1]
             return self.pcg.solve(s, rhs, x0)
         return sla.lu_solve(self._factor(s), rhs, check_finite=False)
 
@@ -746,10 +746,13 @@ class BlockTriangularPreconditioner:
             if s > 1:
                 acc = e[s - 1:0:-1] @ Y[: s - 1]  # sum_{m<s} e_{s-m} y^(m)
                 rhs -= self.A.diags.D1[s - 1] * acc
-            Y[s - 1] = self.solve_block(s, rhs, [Y[s - 1 - k] for k in range(1, min(3, s - 1) + 1)])
+            Y[s - 1] = self.solve_block(s, rhs, [Y[s - 1 - k] for k in range(1, min(WARM_ORDER, s - 1) + 1)])
         rhs = z[S * N:] - Y[S - 1]
         y[S * N:] = self.solve_block(S + 1, rhs)
         return y
+
+
+WARM_ORDER = 6  # previous levels in the tau-PCG initial-guess extrapolation (the device's kWarmOrder)
 
 
 class TauPCG:

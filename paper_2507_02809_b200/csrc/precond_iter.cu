@@ -26,6 +26,14 @@ namespace {
 
 constexpr int CB = 4;   // columns per CTA of the setup column FFT (spectrum of B)
 
+// warm start: extrapolation order (previous levels used) and the coefficients
+// (-1)^(j+1) C(k, j) of the degree-(k-1) polynomial through them
+constexpr int kWarmOrder = 6;
+__constant__ double kWarmCoef[kWarmOrder + 1][kWarmOrder + 1] = {
+    {0, 0, 0, 0, 0, 0, 0},          {0, 1, 0, 0, 0, 0, 0},           {0, 2, -1, 0, 0, 0, 0},
+    {0, 3, -3, 1, 0, 0, 0},         {0, 4, -6, 4, -1, 0, 0},         {0, 5, -10, 10, -5, 1, 0},
+    {0, 6, -15, 20, -15, 6, -1}};
+
 struct ItArgs {
     int n1, n2, ld2, L1, L2, lg1, lg2, S, levels, maxit;
     long long Np;
@@ -522,8 +530,9 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         // ---- level setup: rhs (forward substitution, krylov.cpp:55-68), b = rhs / D2, x = 0
         const bool direct = lv < a.S && a.direct[lv];
         // warm start: time levels after the first whose predecessors were solved by CG
-        const bool warm = a.warm && warm_ok && lv >= 1 && lv < a.S && !direct && !a.direct[lv - 1] &&
-                          (lv < 2 || !a.direct[lv - 2]) && (lv < 3 || !a.direct[lv - 3]);
+        const int kx = min(lv, kWarmOrder);  // previous levels in the extrapolation
+        bool warm = a.warm && warm_ok && lv >= 1 && lv < a.S && !direct;
+        for (int j = 1; j <= kx; ++j) warm = warm && !a.direct[lv - j];
         double* x = a.y + (long long)lv * Np;
         double part = 0.0;
         for (long long i = (long long)cta * nthr + tid; i < Np; i += (long long)G * nthr) {
@@ -547,15 +556,12 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
                     b = rhs * a.d2inv[(long long)(a.S - 1) * Np + i];
                 }
             }
-            // initial guess of the time levels (not the f-block): the previous levels' solutions
-            // extrapolated in time (constant, linear, quadratic), passed through p to the pre-step
+            // initial guess of the time levels (not the f-block): the polynomial extrapolation through
+            // the previous kx levels' solutions, x0 = sum_j (-1)^(j+1) C(kx, j) y_(lv-j), passed
+            // through p to the pre-step
             double x0 = 0.0;
-            if (warm && i2 < a.n2) {
-                const double y1 = a.y[(long long)(lv - 1) * Np + i];
-                if (lv == 1) x0 = y1;
-                else if (lv == 2) x0 = 2.0 * y1 - a.y[(long long)(lv - 2) * Np + i];
-                else x0 = (3.0 * y1 - 3.0 * a.y[(long long)(lv - 2) * Np + i]) + a.y[(long long)(lv - 3) * Np + i];
-            }
+            if (warm && i2 < a.n2)
+                for (int j = 1; j <= kx; ++j) x0 += kWarmCoef[kx][j] * a.y[(long long)(lv - j) * Np + i];
             a.r[i] = b;
             a.zz[i] = b;
             a.p[i] = x0;
