@@ -328,6 +328,12 @@ def run_ours(args):
     ms_papply = ms_sweep = ms.value
     assert lib.fi_system_apply_timed(A.handle, y.data_ptr(), out.data_ptr(), reps, ctypes.byref(ms)) == 0
     ms_op = ms.value
+    # K3: one MGS round (w -= c x; h = y.w) over three Krylov-length vectors, L2 flushed before each
+    mw, mx, my = (torch.from_numpy(np.random.default_rng(k).uniform(-1, 1, n)).to(b_dev.device) for k in (5, 6, 7))
+    assert lib.fi_mgs_round_timed(ctx.handle, n, mw.data_ptr(), mx.data_ptr(), my.data_ptr(), reps,
+                                  ctypes.byref(ms)) == 0
+    ms_mgs = ms.value
+    del mw, mx, my
 
     N, S = A.N, A.S
     Np = ((N + 63) // 64) * 64 if spec.sgrid.d == 1 else spec.sgrid.n[0] * ((spec.sgrid.n[1] + 63) // 64) * 64
@@ -407,6 +413,11 @@ def run_ours(args):
                          # profiles/xchg_latency_r01.txt)
                          "exchange_floor_us_per_level": 0.908, "precond_form": form,
                          "peak_source": peak_src},
+            "roofline_arnoldi": {"bound": "hbm", "kernel": "reduce_kernel (K3: one MGS round, fused axpy + dot)",
+                                 "achieved": round(32.0 * n / (ms_mgs * 1e-3) / 1e9, 1), "peak": hbm_peak,
+                                 "unit": "GB/s", "frac": round(32.0 * n / (ms_mgs * 1e-3) / 1e9 / hbm_peak, 4),
+                                 "bytes_per_launch": 32 * n, "ms_per_launch": round(ms_mgs, 5),
+                                 "note": "w read + written, v_(i-1) and v_i read; L2 flushed before each timed round"},
             "roofline_operator": {"bound": "tensor", "kernel": "toeplitz_apply_kernel (K1, FP64 DMMA)",
                                   "achieved": round(op_tflops, 3), "peak": FP64_DMMA_PEAK_TFLOPS,
                                   "unit": "TFLOP/s", "frac": round(op_tflops / FP64_DMMA_PEAK_TFLOPS, 4),

@@ -175,6 +175,10 @@ typedef struct {
 int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x0_dev, double* x_dev,
              const fi_gmres_opts* opts, fi_gmres_report* report, double* history_host, int history_cap);
 /* Host-buffer variant: H2D of b (and x0), solve, D2H of x — the reference-facing call. */
+/* Measurement hook (bench roofline of K3): average time of one MGS round (w -= c x; h = y.w, the
+ * fused axpy + dot of krylov.cpp:127-132) over device vectors of length n, L2 flushed before each. */
+int fi_mgs_round_timed(fi_ctx* ctx, long long n, double* w_dev, const double* x_dev, const double* y_dev, int reps,
+                       double* ms_avg);
 /* Dense realisation (spectra.cpp:14-45, verification only): kind 0 = SystemA, 1 = PreconditionerP,
  * 2 = ForwardAhat; row-major dim x dim into device memory M_dev (dim = (S+1)N, or S N for Ahat);
  * FI_E_RESOURCE above cap (<= 0: 4096).  Bit-for-bit the reference's entries. */

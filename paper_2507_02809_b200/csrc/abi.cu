@@ -515,6 +515,16 @@ int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x
     });
 }
 
+int fi_mgs_round_timed(fi_ctx* ctx, long long n, double* w_dev, const double* x_dev, const double* y_dev, int reps,
+                       double* ms_avg) {
+    return guard([&] {
+        require(ctx && w_dev && x_dev && y_dev && ms_avg && n > 0 && reps > 0, FI_E_DOMAIN,
+                "fi_mgs_round_timed: bad argument");
+        fib::GmresEngine eng(ctx, n);
+        *ms_avg = eng.time_mgs_round(w_dev, x_dev, y_dev, reps);
+    });
+}
+
 int fi_assemble_dense(fi_system* sys, int kind, long long cap, double* M_dev) {
     return guard([&] {
         require(sys && M_dev, FI_E_DOMAIN, "fi_assemble_dense: NULL argument");

@@ -287,6 +287,50 @@ void GmresEngine::reduce(double* w, const double* x, const double* coef, const d
     FI_LAUNCHED(ctx_);
 }
 
+// reads a buffer larger than L2 (leaves L2 full of clean lines: a write flush would leave dirty lines
+// whose write-back the timed kernel would pay for)
+__global__ void flush_read_kernel(const double2* p, long long n2, double* sink) {
+    double acc = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        const double2 v = __ldcg(p + i);
+        acc += v.x + v.y;
+    }
+    if (acc == 12345.678) *sink = acc;  // never true for the zero buffer: keeps the loads
+}
+
+double GmresEngine::time_mgs_round(double* w, const double* x, const double* y, int reps) {
+    // the state's h[] and coefficients: a scratch GmresState on the device
+    DevBuf<GmresState> st(1);
+    DevBuf<double> arr(64), flush((size_t)48 << 20);  // 384 MB: larger than L2
+    GmresState hs{};
+    hs.h = arr.p;
+    hs.c = arr.p + 16;
+    FI_CUDA(cudaMemsetAsync(arr.p, 0, arr.bytes(), ctx_->stream));
+    FI_CUDA(cudaMemcpyAsync(st.p, &hs, sizeof(GmresState), cudaMemcpyHostToDevice, ctx_->stream));
+    GmresState* keep = st_;
+    st_ = st.p;
+    cudaEvent_t e0, e1;
+    FI_CUDA(cudaEventCreate(&e0));
+    FI_CUDA(cudaEventCreate(&e1));
+    float total = 0.f;
+    FI_CUDA(cudaMemsetAsync(flush.p, 0, flush.bytes(), ctx_->stream));
+    for (int r = 0; r <= reps; ++r) {
+        flush_read_kernel<<<ctx_->sm_count * 8, 256, 0, ctx_->stream>>>(reinterpret_cast<const double2*>(flush.p),
+                                                                        (long long)(flush.n / 2), arr.p + 48);
+        FI_CUDA(cudaEventRecord(e0, ctx_->stream));
+        reduce(w, x, arr.p, y, RM_ROUND, 1, 1, arr.p + 32, nullptr, nullptr);
+        FI_CUDA(cudaEventRecord(e1, ctx_->stream));
+        FI_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        FI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (r > 0) total += ms;  // (round 0: warm-up)
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    st_ = keep;
+    return total / reps;
+}
+
 double GmresEngine::norm2(const double* v, int slot) {
     // RM_NORM never writes w (x == nullptr)
     reduce(const_cast<double*>(v), nullptr, nullptr, nullptr, RM_NORM, 0, slot, nullptr, nullptr, nullptr);

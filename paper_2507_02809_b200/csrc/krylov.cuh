@@ -47,6 +47,9 @@ public:
     // Reference semantics of gmres() (krylov.cpp:72-209) + restart extension.
     // optional: w = M^{-1} A v in one operation (used for the Arnoldi step instead of A then M)
     void set_fused(const Op* f) { fused_ = f; }
+    // measurement hook (bench roofline): average time of one MGS round w -= c x; h = y.w over
+    // device vectors of length n(), L2 flushed (a write larger than L2) before every timed round
+    double time_mgs_round(double* w, const double* x, const double* y, int reps);
     void solve(const Op& A, const Op* M, const double* b, const double* x0, double* x, double tol, int maxit,
                int restart, fi_gmres_report* rep, std::vector<double>& history);
 
