@@ -235,6 +235,7 @@ struct HArgs {
     const int* skip;
     unsigned long long* trace;  // optional [8]: per-phase time sums of CTA 0 (FI_HODLR_TRACE=1)
     int dbg;                    // FI_HODLR_DBG experiment bits (0 in production)
+    unsigned long long* ttrace; // optional [nlev][G]: globaltimer of every CTA's publish (FI_HODLR_TTRACE)
 };
 
 
@@ -257,7 +258,8 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int nlev = a.nlev, S = a.S, D = a.tr.D, nb = a.tr.nb;
     const long long Np = a.Np;
-    const int c = blockIdx.x, t = threadIdx.x;
+    // (FI_HODLR_DBG bit 32: logical row block = reversed CTA index, a placement experiment)
+    const int c = (a.dbg & 32) ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x, t = threadIdx.x;
     const int w = t >> 5, lane = t & 31, g = lane >> 3, kq = lane & 7;
     const long long r0 = (long long)c * HR;
     const int b = (int)(r0 / TB);  // leaf block of the CTA (two CTAs per leaf)
@@ -443,6 +445,11 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
             st_tagged(a.proj + pb + my_slot + 4 * kq + g, s, tag);
         }
         stamp(0);
+        if (a.ttrace && t == 0) {
+            unsigned long long gt;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+            a.ttrace[(long long)lv * gridDim.x + c] = gt;
+        }
         load_quarter(lv + 1, 0);
         // next-next level's coefficients pulled into L2 now, so the register loads hit L2
         if (lv + 2 < nlev && !(a.dbg & 1)) {
@@ -812,8 +819,16 @@ void hodlr_sweep(fi_ctx* ctx, HodlrData* h, const fi_system* sys, const double* 
     static const int dbg = std::getenv("FI_HODLR_DBG") ? std::atoi(std::getenv("FI_HODLR_DBG")) : 0;
     a.dbg = dbg;
     static const bool tracing = std::getenv("FI_HODLR_TRACE") != nullptr;
-    DevBuf<unsigned long long> trace;
+    static const char* ttfile = std::getenv("FI_HODLR_TTRACE");  // per-level publish times (diagnostics)
+    DevBuf<unsigned long long> trace, ttr;
+    const int G = (int)(L.Np / HR);
     a.trace = nullptr;
+    a.ttrace = nullptr;
+    if (ttfile) {
+        ttr.alloc((size_t)levels * G);
+        FI_CUDA(cudaMemsetAsync(ttr.p, 0, ttr.bytes(), ctx->stream));
+        a.ttrace = ttr.p;
+    }
     if (tracing) {
         trace.alloc(8);
         FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
@@ -825,6 +840,15 @@ void hodlr_sweep(fi_ctx* ctx, HodlrData* h, const fi_system* sys, const double* 
     FI_CUDA(cudaLaunchCooperativeKernel((const void*)hodlr_sweep_kernel, dim3((unsigned)(L.Np / HR)), dim3(256), args,
                                         smem, ctx->stream));
     FI_LAUNCHED(ctx);
+    if (ttfile) {
+        std::vector<unsigned long long> hv((size_t)levels * G);
+        FI_CUDA(cudaMemcpyAsync(hv.data(), ttr.p, hv.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        FI_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (FILE* f = std::fopen(ttfile, "wb")) {
+            std::fwrite(hv.data(), 8, hv.size(), f);
+            std::fclose(f);
+        }
+    }
     if (tracing) {
         unsigned long long hv[8];
         FI_CUDA(cudaMemcpyAsync(hv, trace.p, sizeof(hv), cudaMemcpyDeviceToHost, ctx->stream));
