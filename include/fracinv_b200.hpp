@@ -191,6 +191,9 @@ public:
     int64_t space_dim() const { return fi_system_space_dim(h_); }
     int steps() const { return spec_.S; }
     int64_t dim() const { return fi_system_dim(h_); }
+    // EXTENSION: Arnoldi steps of gmres() with this system's preconditioner compute P^{-1} A v as
+    // v + P^{-1}((A - P) v) (default, one sweep per step) or in the reference's order (K1, then P^{-1})
+    void set_split_apply(bool on) { check(fi_system_set_split_apply(h_, on ? 1 : 0)); }
 
     // z = A y (system.cpp:144-174)
     std::vector<double> apply(const std::vector<double>& y) const {
