@@ -37,7 +37,7 @@ struct fi_precond {
     std::vector<double> it_dmean;
     std::vector<int> it_direct;
     fib::DevBuf<double2> it_tw1, it_tw2, it_X;
-    fib::DevBuf<double> it_lamT, it_lamB, it_Rr, it_vec, it_dmean_d;
+    fib::DevBuf<double> it_lamT, it_lamB, it_Rr, it_vec, it_dmean_d, it_hb;
     fib::DevBuf<int> it_direct_d;
     int it_fgrid = 0;                            // fused kernel: cooperative grid size
     fib::DevBuf<double> it_fparts;               // fused kernel: 2 x grid block partials

@@ -54,6 +54,7 @@ struct ItArgs {
     double* p;
     double* Ap;
     double2* X;   // L1 x L2 complex work
+    double* hb;   // 8 x Np: old part of the L1 history of the current 8-level block's targets
     double* Rr;   // n1 x n2 real DST work
     const int* skip;
     int warm;    // extrapolated initial guesses for the time levels (FI_TAU_WARM, default 1)
@@ -540,13 +541,26 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
             double b = 0.0, xv = 0.0;
             if (i2 < a.n2) {
                 if (lv < a.S) {
-                    double h[4] = {0.0, 0.0, 0.0, 0.0};
-                    int m = 0;
-                    for (; m + 3 < lv; m += 4)
+                    // L1 history sum_{m < lv} e_{lv-m} y_m, blocked over 8 levels: at a block start
+                    // B0 the old part sum_{m < B0} e_{L-m} y_m of the block's 8 targets L is formed
+                    // reading each y_m once (8x less traffic than per level; this thread owns element
+                    // i at every level, so hb needs no synchronisation); per level the <= 7 recent
+                    // terms m in [B0, lv) are added
+                    const int B0 = lv & ~7, jt = lv & 7;
+                    if (jt == 0 && B0 > 0) {
+                        double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                        const int nt = min(8, a.S - B0);
+                        for (int m = 0; m < B0; ++m) {
+                            const double ym = a.y[(long long)m * Np + i];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) h[q] += a.e[lv - m - q] * a.y[(long long)(m + q) * Np + i];
-                    for (; m < lv; ++m) h[0] += a.e[lv - m] * a.y[(long long)m * Np + i];
-                    const double hist = (h[0] + h[1]) + (h[2] + h[3]);
+                            for (int t = 0; t < 8; ++t)
+                                if (t < nt) acc[t] += a.e[B0 + t - m] * ym;
+                        }
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) a.hb[(long long)t * Np + i] = acc[t];
+                    }
+                    double hist = B0 > 0 ? a.hb[(long long)jt * Np + i] : 0.0;
+                    for (int m = B0; m < lv; ++m) hist += a.e[lv - m] * a.y[(long long)m * Np + i];
                     const long long o = (long long)lv * Np + i;
                     const double rhs = a.z_in[o] - a.D1[o] * hist;
                     if (direct) xv = rhs / (a.e0 * a.D1[o]);
@@ -676,6 +690,7 @@ ItArgs make_args(fi_precond* P) {
     a.p = P->it_vec.p + 2 * Np;
     a.Ap = P->it_vec.p + 3 * Np;
     a.X = P->it_X.p;
+    a.hb = P->it_hb.p;
     static const int warm = std::getenv("FI_TAU_WARM") ? std::atoi(std::getenv("FI_TAU_WARM")) : 1;
     a.warm = warm;
     a.Rr = P->it_Rr.p;
@@ -771,6 +786,7 @@ void precond_build_iterative(fi_precond* P, double tol, int maxit) {
     P->it_Rr.alloc((size_t)N);
     P->it_lamB.alloc((size_t)L1 * L2);
     P->it_vec.alloc((size_t)4 * Np);  // r, z, p, Ap
+    P->it_hb.alloc((size_t)8 * Np);   // blocked L1 history
     FI_CUDA(cudaMemset(P->it_vec.p, 0, P->it_vec.bytes()));
     // circulant spectrum of B with the same FFT kernels
     allow_column_smem();
