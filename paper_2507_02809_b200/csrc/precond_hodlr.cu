@@ -452,11 +452,13 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         }
         load_quarter(lv + 1, 0);
         // next-next level's coefficients pulled into L2 now, so the register loads hit L2
-        if (lv + 2 < nlev && !(a.dbg & 1)) {
+        if (lv + 2 < nlev && !(a.dbg & 1) && lane == 0) {
+            // one bulk L2 prefetch per warp (8 KB: the warp's own 16 x 32 double2) instead of 512
+            // per-line prefetch instructions per CTA
             const char* pf = reinterpret_cast<const char*>(a.hd + (long long)(lv + 2) * lvstride +
                                                            (long long)c * (RK / 2) * 256);
-            for (int q = t; q < (RK / 2) * 256 * 16 / 128; q += blockDim.x)
-                asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pf + (long long)q * 128));
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(pf + (long long)w * 8192), "r"(8192)
+                         : "memory");
         }
         // ---- the own leaf half (its x is the CTA's own): no remote input
         double ypart = 0.0;
