@@ -99,3 +99,52 @@ def test_spectral_summary_counts_the_cluster_at_one():
     s = SP.spectral_summary(torch.linalg.solve(Pd, Ad))
     assert s.cluster_count + s.outlier_count == (S + 1) * n
     assert s.cluster_count >= S * n and s.outlier_count <= n and s.cond_2 > 1.0
+
+
+def test_preconditioner_is_a_rank_N_correction_with_a_cluster_at_one():
+    """test_krylov.cpp:184-202 — also the structural fact the split Arnoldi step rests on (A - P is
+    the f column of the time rows only)."""
+    import torch
+    N, S = 16, 8
+    A = F.SystemOperator(paper(F, 0.1, 1.9, N, S))
+    Ad = SP.assemble_dense_system(A, SP.SYSTEM_A)
+    Pd = SP.assemble_dense_system(A, SP.PRECONDITIONER_P)
+    sv = torch.linalg.svdvals(Ad - Pd).cpu().numpy()
+    assert int((sv > 1e-10 * sv[0]).sum()) <= N
+    ev = SP.eigenvalues_preconditioned(Pd, Ad)
+    assert int((np.abs(ev - 1.0) <= 1e-6).sum()) >= S * N
+
+
+@pytest.mark.parametrize("S", [8, 16])
+def test_preconditioned_iterations_bounded_by_N_plus_1(S):
+    """test_krylov.cpp:204-216 (reference GMRES settings: full GMRES, tol 1e-8)."""
+    A = F.SystemOperator(paper(F, 0.5, 1.5, 16, S))
+    P = F.BlockTriangularPreconditioner(A)
+    z = F.build_rhs(A, F.add_noise(F.forward_solve(A, P).mu, 0.01, 1)).z
+    _, rep = F.gmres(A, P, z)
+    assert rep.converged and rep.iterations <= 17
+
+
+def test_concurrent_contexts_are_bitwise_identical():
+    """test_toeplitz.cpp:123-143: two host threads, each with its own context (stream and
+    workspaces), apply operators of the same problem 50 times; the results equal a serial apply
+    bit for bit."""
+    import threading
+    spec = paper(F, 0.3, 1.3, 64, 16)
+    ops = [F.SystemOperator(spec, ctx=F.Context(0)) for _ in range(2)]
+    rng = np.random.default_rng(3)
+    xs = [rng.uniform(-1, 1, ops[0].dim()) for _ in range(2)]
+    ref = [ops[k].apply(xs[k]) for k in range(2)]
+    out = [None, None]
+
+    def work(k):
+        for _ in range(50):
+            out[k] = ops[k].apply(xs[k])
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for k in range(2):
+        assert np.array_equal(out[k], ref[k])
