@@ -3,25 +3,30 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
-A step is one GMRES(50) solve (tol 1e-10, block-triangular preconditioner) of BASELINE config 1
-(1D, M=4095 interior points, N=512 time steps; all-at-once dimension 2,100,735).  Setup
-(operator assembly, preconditioner build, forward solve for mu, noise) is untimed.
+A step is one GMRES(50) solve with the block-triangular preconditioner of BASELINE config 4 by
+default — the largest single-GPU configuration (2D, 255 x 255 interior points, N = 512 time steps;
+all-at-once dimension 33,357,825; tol 1e-8).  Setup (operator assembly, preconditioner build, forward
+solve for mu, noise) is untimed.
 
-  value  GMRES iterations/s, device-resident right-hand side (CUDA events on the library stream)
+  value  GMRES iterations/s of the device-resident solve (CUDA events on the library stream)
   e2e    the same metric through the reference-facing host call fi_gmres_host: pinned host b,
          H2D + solve + D2H of x inside the timed region
-  roofline  the dominant kernel (K2, the preconditioner sweep, HBM-bound) timed live with CUDA
-         events on the library stream; roofline_operator = K1 (FP64 DMMA-bound)
-  cpu_baseline  the CPU oracle (numpy/scipy restatement of the reference) on a bounded sample
+  roofline  the dominant kernel of the solve, timed live with CUDA events on the library stream:
+         for the 2D configs the tau-PCG forward substitution (tau_pcg_fused, K5) on the input an
+         Arnoldi step feeds it; roofline_operator = K1 (FP64 DMMA), roofline_arnoldi = one MGS round
+  configs  time-to-solve and iterations/s of every BASELINE config (one solve each after a warm-up)
+         and of the unpreconditioned config-4 solve (one GMRES(50) cycle timed)
+  cpu_baseline  the CPU oracle (numpy/scipy restatement of the reference) on a bounded sample of
+         the same workload, at 1 core (the reference is single-threaded) and at all cores
 
 Multi-GPU: the solve does not shard — N ranks run N independent replicas
 (weak scaling); value = all ranks' iterations / max-over-ranks time.
 --impl reference times the reference algorithm's CPU restatement (the reference itself needs
-Eigen/FFTW, absent here) on the host cores; under torchrun only rank 0 works.
+Eigen/FFTW, absent here) on all host cores; under torchrun only rank 0 works.  It never imports the
+product library (paper_2507_02809_b200.configs is pure Python and the package loads the .so lazily).
 """
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -34,7 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GMRES time-to-solve & iters/s; operator-apply FP64 TFLOP/s as % of roofline"
-FP64_DMMA_PEAK_TFLOPS = 37.0  # measured: profiles/fp64_peak_r01.jsonl (register-only DMMA loop, best of 10)
+DEFAULT_CONFIG = 4
 
 
 def load_peaks():
@@ -44,6 +49,12 @@ def load_peaks():
         return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (burst copy)"
     except Exception:
         return 6650.0, "fallback B200_PROFILING.md 6.65 TB/s"
+
+
+def load_fp64_peak():
+    with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+        p = json.load(f)
+    return float(p[p["roofline_peak"]]), "profiles/fp64_peak.json " + p["roofline_peak"] + " (measured DMMA loop)"
 
 
 class ClockSampler:
@@ -119,82 +130,200 @@ def dist_env():
     return ws, rank, local
 
 
-# --------------------------------------------------------------------------- CPU baseline (oracle)
-def cpu_reference_sample(cfg: int, iters_hint: int, seconds_budget: float = 20.0):
-    """Time the reference algorithm's CPU restatement on a bounded sample of config `cfg` and
-    extrapolate GMRES iterations/s (= 1 / (A-apply + P-apply + MGS step)).
+def workload_config(cfg: int, ws: int = 1) -> dict:
+    """The config keys of the JSON line — identical in both arms (no measured quantities)."""
+    from paper_2507_02809_b200.configs import NAMES, NOISE, RESTART, SEED_BASE, SHAPES, TOL
+    n, S = SHAPES[cfg]
+    N = int(np.prod(n))
+    return {"workload": NAMES[cfg], "M": "x".join(str(v) for v in n), "N_t": S, "dim": (S + 1) * N,
+            "restart": RESTART, "tol": TOL[cfg], "precond": "block-triangular",
+            "noise": f"{NOISE[cfg] * 100:g}% gaussian rel-L2 seed {SEED_BASE + cfg}",
+            "l2": ("inputs larger than L2: every solve streams Krylov vectors of %.0f MB and the operator's "
+                   "%.0f MB of coefficient fields" % (8e-6 * (S + 1) * N, 8e-6 * 2 * S * N)
+                   if 8 * (S + 1) * N > 126e6 else
+                   "the working set is not flushed from L2 between solves (Krylov vectors of %.1f MB)"
+                   % (8e-6 * (S + 1) * N)),
+            "parallelism": f"replicas x{ws}"}
 
-    P-apply = S+1 dense LU solves + the O(S^2 N) history (krylov.cpp:48-70); its LU factors
-    (68.8 GB for config 1) are built for a uniform sample of levels only and the per-level
-    solve time is scaled to all levels.  A-apply is timed whole (FFT matvecs, system.cpp:144-174).
+
+def golden_iterations(cfg: int, default: int = 12) -> int:
+    try:
+        return int(np.load(os.path.join(ROOT, "tests", "golden", f"oracle_config{cfg}.npz"))["iterations"])
+    except Exception:
+        return default
+
+
+# --------------------------------------------------------------------------- CPU baseline (oracle)
+def cpu_reference_sample(cfg: int, iters: int, threads: int, nlev: int = 12):
+    """Time the reference algorithm's CPU restatement (oracle/) on a bounded sample of config `cfg`
+    with `threads` host threads (BLAS pool and FFT workers) and extrapolate GMRES iterations/s
+    (= 1 / (A-apply + P-apply + MGS step), the reference's order: krylov.cpp:123-132).
+
+    A-apply: one whole apply (system.cpp:144-174).  P-apply (krylov.cpp:48-70): the first `nlev` time
+    levels of the forward substitution on the input an Arnoldi step feeds P (A v with v the f-block
+    direction), timed level by level with the oracle's own per-block solve (dense LU, or the
+    substituted tau-PCG with its warm start); the remaining levels are extrapolated with the mean of the
+    levels that already have the full warm start, plus the history sum at its true length.
     """
-    import scipy.linalg as sla
+    import threadpoolctl
 
     from oracle import fracinv_oracle as O
     from paper_2507_02809_b200.configs import baseline_problem
 
-    t_setup = time.perf_counter()
-    A = O.SystemOperator(baseline_problem(O, cfg))
-    N, S = A.N, A.steps
-    rng = np.random.default_rng(0)
-    v = rng.uniform(-1, 1, A.dim)
-    A.apply(v)  # warm-up (plans, E matrix)
-    t_apply = float("inf")
-    for _ in range(2):
+    t_wall = time.perf_counter()
+    O.FFT_WORKERS = threads
+    with threadpoolctl.threadpool_limits(threads):
+        A = O.SystemOperator(baseline_problem(O, cfg))
+        N, S = A.N, A.steps
+        rng = np.random.default_rng(0)
+        v = rng.uniform(-1, 1, A.dim)
+        A.apply(v)  # warm-up (E matrix)
         t0 = time.perf_counter()
         A.apply(v)
-        t_apply = min(t_apply, time.perf_counter() - t0)
-
-    # sample of levels for the P-apply: factor + solve incl. history sums
-    nsamp = 24 if S > 64 else S + 1
-    levels = sorted(set(int(round(x)) for x in np.linspace(1, S + 1, nsamp)))
-    Bd = A.laplacian.dense(N)
-    e = A.weights.e
-    Y = rng.uniform(-1, 1, (S, N))
-    t_fact = t_solve = 0.0
-    for s in levels:
-        if s <= S:
-            blk = A.scale_space * A.diags.D2[s - 1][:, None] * Bd
-            blk[np.diag_indices(N)] += e[0] * A.diags.D1[s - 1]
+        t_apply = time.perf_counter() - t0
+        dense = not (A.spec.sgrid.d == 2 and N > 4096)
+        e = A.weights.e
+        D1 = A.diags.D1
+        t_build = 0.0
+        if dense:
+            P = O.BlockTriangularPreconditioner(A, cache=False, inner="lu") if N > 2048 else \
+                O.BlockTriangularPreconditioner(A, inner="lu")
         else:
-            blk = A.scale_reg * A.diags.D2[S - 1][:, None] * Bd
+            P = O.BlockTriangularPreconditioner(A, inner="pcg")
+        # the preconditioner's input in the first Arnoldi step: A v0 with v0 = P^{-1} b / |P^{-1} b|.  The
+        # time rows of b are b_{s-1} D1 rho (zero for the 2D configs), so v0 is (nearly) the f-block solve
+        # of the observation: v0 ~ [0; G_f^{-1} mu_eps]
+        try:
+            mu_eps = np.load(os.path.join(ROOT, "tests", "golden", f"oracle_config{cfg}.npz"))["mu_eps"]
+        except Exception:
+            mu_eps = A.spec.f_true
+        fv = P.solve_block(S + 1, mu_eps)
+        u = np.zeros(A.dim)
+        u[S * N:] = fv / np.linalg.norm(fv)
+        z = A.apply(u)
+        if dense:
+            # dense blocks: factor (untimed build) and time the solves of a uniform sample of levels
+            levels = sorted(set(int(round(x)) for x in np.linspace(1, S + 1, min(nlev, S + 1))))
+            Y = rng.uniform(-1, 1, (S, N))
+            t_solve = 0.0
+            for s in levels:
+                t0 = time.perf_counter()
+                lu = P._factor(s)
+                t_build += time.perf_counter() - t0
+                t0 = time.perf_counter()
+                rhs = z[(s - 1) * N: s * N].copy()
+                if 1 < s <= S:
+                    rhs -= D1[s - 1] * (e[s - 1:0:-1] @ Y[: s - 1])
+                O.sla.lu_solve(lu, rhs, check_finite=False)
+                t_solve += time.perf_counter() - t0
+            t_P = t_solve / len(levels) * (S + 1)
+            t_build = t_build / len(levels) * (S + 1)
+            how = f"P: {len(levels)} of {S + 1} levels' dense LU solves (factors built untimed) scaled to all levels"
+        else:
+            P.pcg.dropped = False
+            P.pcg.iterations = []
+            k = min(nlev, S)
+            Y = np.zeros((k, N))
+            t_lev = []
+            for s in range(1, k + 1):
+                t0 = time.perf_counter()
+                rhs = z[(s - 1) * N: s * N].copy()
+                if s > 1:
+                    rhs -= D1[s - 1] * (e[s - 1:0:-1] @ Y[: s - 1])
+                Y[s - 1] = P.solve_block(s, rhs, [Y[s - 1 - j] for j in range(1, min(O.WARM_ORDER, s - 1) + 1)])
+                t_lev.append(time.perf_counter() - t0)
+            steady = float(np.mean(t_lev[O.WARM_ORDER:])) if k > O.WARM_ORDER else float(np.mean(t_lev))
+            # the history sum at full depth (S - 1 previous levels), scaled linearly in s
+            Yh = rng.uniform(-1, 1, (S - 1, N))
+            t0 = time.perf_counter()
+            _ = e[S - 1:0:-1] @ Yh
+            t_hist = time.perf_counter() - t0
+            del Yh
+            t0 = time.perf_counter()
+            P.solve_block(S + 1, z[S * N:] - Y[k - 1])
+            t_f = time.perf_counter() - t0
+            t_P = sum(t_lev) + (S - k) * steady + sum(t_hist * s / S for s in range(k + 1, S + 1)) + t_f
+            its = P.pcg.iterations
+            how = (f"P: the first {k} of {S} time levels of the tau-PCG substitution timed (CG steps "
+                   f"{its[:k]}), the rest at the warm-start steady state ({steady * 1e3:.1f} ms/level) plus "
+                   f"the history sum at its true length, f-block timed")
+        # one MGS step at k = iters/2 (k+1 dots + axpys over the (S+1)N vector, krylov.cpp:127-132)
+        kk = max(1, iters // 2)
+        w = v.copy()
+        V = rng.uniform(-1, 1, (2, A.dim))
+        tmp = np.empty_like(w)
         t0 = time.perf_counter()
-        lu = sla.lu_factor(blk, check_finite=False)
-        t_fact += time.perf_counter() - t0
-        t0 = time.perf_counter()
-        rhs = v[:N].copy()
-        if 1 < s <= S:
-            rhs -= A.diags.D1[s - 1] * (e[s - 1:0:-1] @ Y[: s - 1])
-        sla.lu_solve(lu, rhs, check_finite=False)
-        t_solve += time.perf_counter() - t0
-    t_P = t_solve / len(levels) * (S + 1)
-    t_build = t_fact / len(levels) * (S + 1)
-    # one MGS step at k = iters_hint/2 (dots + axpys over the (S+1)N vector)
-    k = max(1, iters_hint // 2)
-    w = v.copy()
-    V = rng.uniform(-1, 1, (2, A.dim))
-    t0 = time.perf_counter()
-    for i in range(k + 1):
-        h = V[i % 2] @ w
-        w -= h * V[i % 2]
-    t_mgs = time.perf_counter() - t0
+        for i in range(kk + 1):
+            h = float(V[i % 2] @ w)
+            np.multiply(V[i % 2], h, out=tmp)
+            np.subtract(w, tmp, out=w)
+        t_mgs = time.perf_counter() - t0
     t_iter = t_apply + t_P + t_mgs
     return {
         "iters_per_s": 1.0 / t_iter,
         "time_per_iteration_s": t_iter,
+        # the reference's time-to-solve: iters Arnoldi steps + P^{-1} b + the final true residual's A x
+        "time_to_solve_s_extrapolated": iters * t_iter + t_P + t_apply,
         "a_apply_s": t_apply,
         "p_apply_s_extrapolated": t_P,
         "p_build_s_extrapolated": t_build,
         "mgs_step_s": t_mgs,
-        "cores": os.cpu_count(),
-        "sample": (f"config {cfg}: 1 full A-apply (FFT), P-apply from {len(levels)} of {S + 1} levels' dense LU "
-                   f"factor+solve scaled to all levels, 1 MGS step at k={k}; iters/s = 1/(A+P+MGS); "
-                   f"wall {time.perf_counter() - t_setup:.1f}s"),
+        "cores": threads,
+        "sample": (f"config {cfg} with {threads} host thread(s): 1 full A-apply (FFT); {how}; 1 MGS step at "
+                   f"k={kk}; iters/s = 1/(A+P+MGS); wall {time.perf_counter() - t_wall:.1f}s"),
     }
 
 
+def cpu_baseline_entry(cfg, iters):
+    one = cpu_reference_sample(cfg, iters, 1)
+    n = os.cpu_count() or 1
+    alln = cpu_reference_sample(cfg, iters, n)
+    return {"value": round(one["iters_per_s"], 6), "unit": "iters/s", "cores": 1, "kind": "port",
+            "sample": one["sample"], "time_per_iteration_s": round(one["time_per_iteration_s"], 3),
+            "time_to_solve_s_extrapolated": round(one["time_to_solve_s_extrapolated"], 2),
+            "all_cores": {"value": round(alln["iters_per_s"], 6), "cores": n,
+                          "time_per_iteration_s": round(alln["time_per_iteration_s"], 3),
+                          "time_to_solve_s_extrapolated": round(alln["time_to_solve_s_extrapolated"], 2),
+                          "sample": alln["sample"]}}
+
+
 # --------------------------------------------------------------------------- GPU arm
+def build_case(F, ctx, cfg, seed_offset=0):
+    from paper_2507_02809_b200.configs import NOISE, SEED_BASE, baseline_problem
+    t0 = time.perf_counter()
+    spec = baseline_problem(F, cfg)
+    A = F.SystemOperator(spec, ctx=ctx)
+    t_asm = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    P = F.BlockTriangularPreconditioner(A, inner="auto")
+    ctx.synchronize()
+    t_pb = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    mu = F.forward_solve(A, P).mu
+    t_fwd = time.perf_counter() - t0
+    mu_eps = F.add_gaussian_noise(mu, NOISE[cfg], SEED_BASE + cfg + seed_offset)
+    z = F.build_rhs(A, mu_eps).z
+    return spec, A, P, z, {"assembly": round(t_asm, 3), "precond_build": round(t_pb, 3),
+                           "forward_solve": round(t_fwd, 3)}
+
+
+def time_solves(F, A, P, b_dev, opts, stream, steps):
+    import torch
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    its = 0
+    ev0.record(stream)
+    for _ in range(steps):
+        x, rep = F.gmres(A, P, b_dev, opts)
+        its += rep.iterations
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    return ev0.elapsed_time(ev1), its, x, rep
+
+
 def run_ours(args):
+    import ctypes
+
     import torch
 
     ws, rank, local = dist_env()
@@ -202,108 +331,68 @@ def run_ours(args):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from oracle import fracinv_oracle as O  # noqa: F401  (cpu_baseline leg only)
     from paper_2507_02809_b200 import fracinv as F
-    from paper_2507_02809_b200.configs import NAMES, NOISE, RESTART, SEED_BASE, TOL, baseline_problem
+    from paper_2507_02809_b200._lib import GmresOpts, GmresReport, last_error, lib
+    from paper_2507_02809_b200.configs import NAMES, RESTART, TOL
 
     cfg = args.config
     ctx = F.Context(local if ws > 1 else 0)
-    t0 = time.perf_counter()
-    spec = baseline_problem(F, cfg)
-    A = F.SystemOperator(spec, ctx=ctx)
-    t_asm = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    P = F.BlockTriangularPreconditioner(A)
-    t_pbuild = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    mu = F.forward_solve(A, P).mu
-    t_fwd = time.perf_counter() - t0
-    mu_eps = F.add_gaussian_noise(mu, NOISE[cfg], SEED_BASE + cfg + rank)
-    z = F.build_rhs(A, mu_eps).z
+    spec, A, P, z, setup_s = build_case(F, ctx, cfg, rank)
     opts = F.GmresOptions(TOL[cfg], 0, RESTART)
     n = A.dim()
-
     stream = torch.cuda.ExternalStream(ctx.stream)
     b_dev = torch.from_numpy(z).to(f"cuda:{ctx.device}")
     torch.cuda.synchronize()
 
-    def solve_dev():
-        return F.gmres(A, P, b_dev, opts)
-
-    # warm-up
     for _ in range(args.warmup):
-        x, rep = solve_dev()
-    f_star = spec.f_true
-    recon_err = F.relative_error(f_star, x[-A.N:].cpu().numpy())
+        x, rep = F.gmres(A, P, b_dev, opts)
+    recon_err = F.relative_error(spec.f_true, x[-A.N:].cpu().numpy())
 
     # ---- timed region: device-resident value
     sampler = ClockSampler(local)
     sampler.start()
     launches0 = ctx.kernel_launches
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()
-    torch.cuda.synchronize()
-    iters = []
     if args.profile:  # ncu --profile-from-start off captures exactly the timed region
+        torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStart()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        x, rep = solve_dev()
-        iters.append(rep.iterations)
-    ev1.record(stream)
-    torch.cuda.synchronize()
+    ms_total, total_iters, x, rep = time_solves(F, A, P, b_dev, opts, stream, args.steps)
     if args.profile:
         torch.cuda.cudart().cudaProfilerStop()
     if ws > 1:
         dist.barrier()
     clocks = sampler.stop()
-    ms_total = ev0.elapsed_time(ev1)
     launches = ctx.kernel_launches - launches0
-    total_iters = sum(iters)
 
-    # the same solves with the Arnoldi step in the reference's order (K1 operator apply, then P^{-1})
+    # the same solve with the Arnoldi step in the reference's order (K1 operator apply, then P^{-1})
     # instead of the default split P^{-1} A v = v + P^{-1}((A - P) v)
     A.set_split_apply(False)
-    solve_dev()
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    u_iters = 0
-    for _ in range(args.steps):
-        _, rep_u = solve_dev()
-        u_iters += rep_u.iterations
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    ms_unsplit = ev0.elapsed_time(ev1)
+    F.gmres(A, P, b_dev, opts)
+    ms_unsplit, u_iters, _, rep_u = time_solves(F, A, P, b_dev, opts, stream, max(1, min(2, args.steps)))
     A.set_split_apply(True)
 
     # ---- e2e: host (pinned) b -> fi_gmres_host -> host x
     b_host = torch.from_numpy(z).pin_memory()
     x_host = torch.empty(n, dtype=torch.float64).pin_memory()
-    import ctypes
-
-    from paper_2507_02809_b200._lib import GmresOpts, GmresReport, last_error, lib
     o = GmresOpts(opts.tol, opts.maxit, opts.restart)
     r = GmresReport()
     hist = np.zeros(4096)
     dp = lambda t: ctypes.cast(t.data_ptr(), ctypes.POINTER(ctypes.c_double))
-    e_iters = 0
-    for _ in range(max(1, args.warmup)):  # untimed: first-call staging allocation, warm caches
-        rc = lib.fi_gmres_host(A.handle, P.handle, dp(b_host), None, dp(x_host), ctypes.byref(o), ctypes.byref(r),
-                               hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 4096)
-        assert rc == 0, last_error()
-    # three timed passes of K solves each; the median pass is reported (a host-side hiccup in one
-    # pass, e.g. the thread descheduled while it waits on the look-ahead event, would otherwise
-    # decide the number)
+    hp = hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    for _ in range(max(1, min(args.warmup, 2))):  # untimed: first-call staging allocation
+        assert lib.fi_gmres_host(A.handle, P.handle, dp(b_host), None, dp(x_host), ctypes.byref(o), ctypes.byref(r),
+                                 hp, 4096) == 0, last_error()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     passes = []
-    for _ in range(3):
+    for _ in range(3):  # median of three timed passes of K solves
         torch.cuda.synchronize()
         e_iters = 0
         ev0.record(stream)
         for _ in range(args.steps):
             rc = lib.fi_gmres_host(A.handle, P.handle, dp(b_host), None, dp(x_host), ctypes.byref(o), ctypes.byref(r),
-                                   hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 4096)
+                                   hp, 4096)
             assert rc == 0, last_error()
             e_iters += r.iterations
         ev1.record(stream)
@@ -311,62 +400,120 @@ def run_ours(args):
         passes.append((ev0.elapsed_time(ev1), e_iters))
     ms_e2e, e_iters = sorted(passes)[1]
 
-    # ---- roofline: K2 preconditioner sweep (dominant) and K1 operator, live CUDA events
-    reps = 5
-    y = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, n)).to(b_dev.device)
-    out = torch.empty_like(y)
+    # ---- roofline: the dominant kernel, timed live with CUDA events on the library stream
+    reps = 3
     ms = ctypes.c_double()
-    form = P.form
-    # P^{-1} as the solve uses it: the inverses are polished at build, so one
-    # sweep (one hodlr_sweep_kernel or sweep_kernel launch) with refinement off; the refined apply
-    # (second sweep + K1 residual) is reported beside it
-    P.set_refine(True)
-    assert lib.fi_precond_apply_timed(P.handle, y.data_ptr(), out.data_ptr(), reps, ctypes.byref(ms)) == 0
-    ms_refined = ms.value
-    P.set_refine(False)
-    assert lib.fi_precond_apply_timed(P.handle, y.data_ptr(), out.data_ptr(), reps, ctypes.byref(ms)) == 0
-    ms_papply = ms_sweep = ms.value
-    assert lib.fi_system_apply_timed(A.handle, y.data_ptr(), out.data_ptr(), reps, ctypes.byref(ms)) == 0
+    hbm_peak, peak_src = load_peaks()
+    N, S = A.N, A.S
+    Np = ((N + 63) // 64) * 64 if spec.sgrid.d == 1 else spec.sgrid.n[0] * ((spec.sgrid.n[1] + 63) // 64) * 64
+    # P^{-1} on the input an Arnoldi step feeds it: (A - P) v = (-eta q_s f_v)_s for the first basis vector
+    v0 = P.apply(b_dev)
+    v0 = v0 / torch.linalg.norm(v0)
+    u = torch.zeros_like(v0)
+    fv = v0[S * N:]
+    qv = torch.from_numpy(A.q).to(u.device)
+    u[: S * N] = (-spec.tgrid.eta * qv[:, None] * fv[None, :]).reshape(-1)
+    out = torch.empty_like(u)
+    if P.inner == "pcg":
+        P.stats(reset=True)
+    assert lib.fi_precond_apply_timed(P.handle, u.data_ptr(), out.data_ptr(), reps, ctypes.byref(ms)) == 0, last_error()
+    ms_sweep = ms.value
+    if P.inner == "pcg":
+        st = P.stats(reset=True)
+        applies = max(st["applies"], 1)
+        steps_per_level = st["cg_steps"] / applies / (S + 1)
+        # algorithmic HBM bytes of one apply: every level reads its right-hand side, D1 and 1/D2 rows and
+        # writes its solution once, and the blocked L1 history reads each earlier level once per 8-level
+        # block (sum over block starts B0 of B0 levels); the CG iterations themselves work on an
+        # L2-resident set of ~10 MB per level (vectors and transform buffers), so the kernel is bound by
+        # the latency of its dependent passes, not by HBM
+        hist_levels = sum(b0 for b0 in range(8, S, 8))
+        sweep_bytes = 8 * Np * (4 * (S + 1) + 8 + hist_levels)
+        passes_per_level = 4 * steps_per_level + 3
+        roof = {"bound": "hbm", "kernel": "tau_pcg_fused (K5: tau-preconditioned CG block solves, one cooperative "
+                                          "kernel per P^-1; chain of S+1 dependent levels)",
+                "achieved": round(sweep_bytes / (ms_sweep * 1e-3) / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(sweep_bytes / (ms_sweep * 1e-3) / 1e9 / hbm_peak, 4), "traffic": None,
+                "bytes_per_launch": sweep_bytes, "ms_per_launch": round(ms_sweep, 4),
+                "us_per_level": round(ms_sweep * 1e3 / (S + 1), 2), "cg_steps_per_level": round(steps_per_level, 2),
+                "passes_per_level": round(passes_per_level, 1),
+                "us_per_pass": round(ms_sweep * 1e3 / (S + 1) / passes_per_level, 2),
+                "inner_nonconverged": st["nonconverged_blocks"], "input": "(A - P) v0, the first Arnoldi step's",
+                "note": "latency-bound: per CG step 4 grid-synchronised transform passes (rows, columns, rows, "
+                        "columns) on an L2-resident working set; us_per_pass is the number to watch",
+                "peak_source": peak_src}
+    else:
+        # HODLR / packed-tile sweep over the dense-block inverses (1D)
+        form = P.form
+        nb = Np // 64
+        T = nb * (nb + 1) // 2
+        sweep_bytes = (int(P.device_bytes()) + 4 * 8 * Np * (S + 1) if form == "hodlr" else
+                       (S + 1) * T * 64 * 64 * 8 + 4 * 8 * Np * (S + 1))
+        roof = {"bound": "hbm", "kernel": ("hodlr_sweep_kernel (K2h: substitution over HODLR inverses)" if form == "hodlr"
+                                           else "sweep_kernel (K2: substitution over packed tiles)"),
+                "achieved": round(sweep_bytes / (ms_sweep * 1e-3) / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(sweep_bytes / (ms_sweep * 1e-3) / 1e9 / hbm_peak, 4), "traffic": None,
+                "bytes_per_launch": sweep_bytes, "ms_per_launch": round(ms_sweep, 4),
+                "us_per_level": round(ms_sweep * 1e3 / (S + 1), 3), "precond_form": form, "peak_source": peak_src}
+    del out
+    y = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, n)).to(b_dev.device)
+    o2 = torch.empty_like(y)
+    assert lib.fi_system_apply_timed(A.handle, y.data_ptr(), o2.data_ptr(), reps, ctypes.byref(ms)) == 0
     ms_op = ms.value
-    # K3: one MGS round (w -= c x; h = y.w) over three Krylov-length vectors, L2 flushed before each
+    del o2
+    op_flops = 2.0 * N * N * (S + 1)
+    op_tflops = op_flops / (ms_op * 1e-3) / 1e12
+    fp64_peak, fp64_src = load_fp64_peak()
     mw, mx, my = (torch.from_numpy(np.random.default_rng(k).uniform(-1, 1, n)).to(b_dev.device) for k in (5, 6, 7))
     assert lib.fi_mgs_round_timed(ctx.handle, n, mw.data_ptr(), mx.data_ptr(), my.data_ptr(), reps,
                                   ctypes.byref(ms)) == 0
     ms_mgs = ms.value
-    del mw, mx, my
-
-    N, S = A.N, A.S
-    Np = ((N + 63) // 64) * 64 if spec.sgrid.d == 1 else spec.sgrid.n[0] * ((spec.sgrid.n[1] + 63) // 64) * 64
-    nb = Np // 64
-    T = nb * (nb + 1) // 2
-    if form == "hodlr":
-        # algorithmic bytes of one sweep: every level's HODLR rows once
-        # (fi_precond_bytes: 64 leaf + 32 per ancestor doubles per row) + z, D1, 1/D2 read, y written
-        sweep_bytes = int(P.device_bytes()) + 4 * 8 * Np * (S + 1)
-        sweep_kernel = "hodlr_sweep_kernel (K2: substitution over HODLR inverses; chain of S+1 dependent levels)"
-    else:
-        # the packed lower-triangular FP64 tiles of all S+1 levels once, plus per level row z, D1, 1/D2
-        # read and y written
-        sweep_bytes = (S + 1) * T * 64 * 64 * 8 + 4 * 8 * Np * (S + 1)
-        sweep_kernel = "sweep_kernel (K2: FP64 substitution over packed tiles)"
-    hbm_peak, peak_src = load_peaks()
-    achieved = sweep_bytes / (ms_sweep * 1e-3) / 1e9
-    op_flops = 2.0 * N * N * (S + 1)
-    op_tflops = op_flops / (ms_op * 1e-3) / 1e12
+    del mw, mx, my, y
 
     # max over ranks for times, sum over ranks for the work done (replicas)
     ms_total_max, iters_all = replica_aggregate(ms_total, total_iters, b_dev.device)
     ms_e2e_max, e_iters_all = replica_aggregate(ms_e2e, e_iters, b_dev.device)
     value = iters_all / (ms_total_max * 1e-3)
     e2e_value = e_iters_all / (ms_e2e_max * 1e-3)
-    ms_unsplit_max, u_iters_all = replica_aggregate(ms_unsplit, u_iters, b_dev.device)
-    value_unsplit = u_iters_all / (ms_unsplit_max * 1e-3)
+
+    # ---- the other configurations (rank 0, single process): time-to-solve of each
+    configs = {}
+    if rank == 0 and ws == 1 and not args.no_configs:
+        # config 4 unpreconditioned (BASELINE: GMRES(50), max 2000 iterations): one cycle timed
+        ou = F.GmresOptions(TOL[cfg], RESTART, RESTART)
+        F.gmres(A, None, b_dev, F.GmresOptions(TOL[cfg], 1, RESTART))
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        _, rep_n = F.gmres(A, None, b_dev, ou)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        t_n = ev0.elapsed_time(ev1) * 1e-3
+        configs[NAMES[cfg] + "_unpreconditioned"] = {
+            "iters_per_s": round(rep_n.iterations / t_n, 3), "iterations_timed": rep_n.iterations,
+            "seconds_timed": round(t_n, 3), "note": "one GMRES(50) cycle of the unpreconditioned solve timed; the full "
+            "solve runs to maxit = 2000 without reaching tol 1e-8 (tests/golden/oracle_config4_unprec.npz)"}
+        del P, A, b_dev, x
+        torch.cuda.empty_cache()
+        for c in [c for c in (0, 1, 2, 3, 4) if c != cfg]:
+            sp, Ac, Pc, zc, su = build_case(F, ctx, c)
+            bc = torch.from_numpy(zc).to(f"cuda:{ctx.device}")
+            oc = F.GmresOptions(TOL[c], 0, RESTART)
+            F.gmres(Ac, Pc, bc, oc)
+            msc, itc, xc, repc = time_solves(F, Ac, Pc, bc, oc, stream, 2)
+            configs[NAMES[c]] = {"time_to_solve_s": round(msc * 1e-3 / 2, 5), "iterations": repc.iterations,
+                                 "iters_per_s": round(itc / (msc * 1e-3), 3), "setup_s": su,
+                                 "precond": Pc.inner if Pc.inner == "pcg" else Pc.form,
+                                 "recon_error_vs_fstar": F.relative_error(sp.f_true, xc[-Ac.N:].cpu().numpy())}
+            del Ac, Pc, bc, xc
+            torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_reference_sample(cfg, max(iters))
+        cpu = cpu_baseline_entry(cfg, golden_iterations(cfg, rep.iterations))
 
     if rank == 0:
+        configs[NAMES[cfg]] = {"time_to_solve_s": round(ms_total_max / args.steps * 1e-3, 5),
+                               "iterations": rep.iterations, "iters_per_s": round(value / ws, 3)}
         line = {
             "metric": METRIC,
             "value": round(value, 3),
@@ -376,62 +523,38 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": round(ms_total_max / args.steps, 3),
             "time_to_solve_s": round(ms_total_max / args.steps * 1e-3, 5),
-            "iterations_per_solve": iters[-1],
+            "iterations_per_solve": rep.iterations,
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (BASELINE.json config, manufactured mu via forward solve, seeded Gaussian noise)",
-            "config": {
-                "workload": NAMES[cfg],
-                "M": N, "N_t": S, "dim": n, "restart": RESTART, "tol": TOL[cfg], "precond": "block-triangular",
-                "noise": f"{NOISE[cfg] * 100:g}% gaussian rel-L2 seed {SEED_BASE + cfg}",
-                "l2": ("inputs larger than L2: each P apply streams the HODLR inverses once (%.1f GB)"
-                       % (P.device_bytes() / 1e9) if form == "hodlr" else
-                       "inputs larger than L2: each P apply streams the packed FP64 tiles once (%.1f GB)"
-                       % ((S + 1) * T * 64 * 64 * 8 / 1e9)),
-                "parallelism": f"replicas x{ws}",
-                "recon_error_vs_fstar": recon_err,
-                "final_true_residual": rep.final_true_residual,
-                "setup_s": {"assembly": round(t_asm, 3), "precond_build": round(t_pbuild, 3),
-                            "forward_solve": round(t_fwd, 3)},
-            },
+            "data": "synthetic (BASELINE.json config; observation by the forward solve of f* + seeded Gaussian noise)",
+            "config": workload_config(cfg, ws),
+            "setup_s": setup_s,
+            "recon_error_vs_fstar": recon_err,
+            "final_true_residual": rep.final_true_residual,
             "e2e": {"value": round(e2e_value, 3), "unit": "iters/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n, "timing": "median of 3 timed passes of K solves"},
             "gpu_launches": int(launches),
-            "arnoldi_step": "split: P^-1 A v = v + P^-1((A - P) v), one preconditioner sweep per step (exact identity)",
-            "value_operator_then_precond": {"value": round(value_unsplit, 3), "unit": "iters/s",
+            "arnoldi_step": "split: P^-1 A v = v + P^-1((A - P) v), one preconditioner apply per step (exact identity)",
+            "value_operator_then_precond": {"value": round(u_iters / (ms_unsplit * 1e-3), 3), "unit": "iters/s",
                                             "iterations_per_solve": rep_u.iterations,
                                             "note": "reference order: K1 operator apply, then P^-1, every Arnoldi step"},
-            "roofline": {"bound": "hbm", "kernel": sweep_kernel,
-                         "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                         "bytes_per_launch": sweep_bytes, "ms_per_launch": round(ms_sweep, 4),
-                         "us_per_level": round(ms_sweep * 1e3 / (S + 1), 3),
-                         # the level chain's floor: one all-to-all exchange round among the sweep's 128
-                         # CTAs, 1785 cycles = 0.91 us at 1965 MHz (tools/xchg_latency.cu,
-                         # profiles/xchg_latency_r01.txt)
-                         "exchange_floor_us_per_level": 0.908, "precond_form": form,
-                         "peak_source": peak_src},
+            "roofline": roof,
+            "roofline_operator": {"bound": "tensor", "kernel": "toeplitz_apply_kernel (K1, FP64 DMMA)",
+                                  "achieved": round(op_tflops, 3), "peak": fp64_peak, "unit": "TFLOP/s",
+                                  "frac": round(op_tflops / fp64_peak, 4), "flops_per_launch": op_flops,
+                                  "ms_per_launch": round(ms_op, 4), "peak_source": fp64_src},
             "roofline_arnoldi": {"bound": "hbm", "kernel": "reduce_kernel (K3: one MGS round, fused axpy + dot)",
                                  "achieved": round(32.0 * n / (ms_mgs * 1e-3) / 1e9, 1), "peak": hbm_peak,
                                  "unit": "GB/s", "frac": round(32.0 * n / (ms_mgs * 1e-3) / 1e9 / hbm_peak, 4),
                                  "bytes_per_launch": 32 * n, "ms_per_launch": round(ms_mgs, 5),
                                  "note": "w read + written, v_(i-1) and v_i read; L2 flushed before each timed round"},
-            "roofline_operator": {"bound": "tensor", "kernel": "toeplitz_apply_kernel (K1, FP64 DMMA)",
-                                  "achieved": round(op_tflops, 3), "peak": FP64_DMMA_PEAK_TFLOPS,
-                                  "unit": "TFLOP/s", "frac": round(op_tflops / FP64_DMMA_PEAK_TFLOPS, 4),
-                                  "flops_per_launch": op_flops, "ms_per_launch": round(ms_op, 4),
-                                  "peak_source": "profiles/fp64_peak_r01.jsonl (measured DMMA loop)"},
-            "precond_apply_ms": round(ms_papply, 4),
-            "precond_apply_refined_ms": round(ms_refined, 4),
+            "configs": configs,
             "clocks": clocks,
         }
         if cpu is not None:
-            line["cpu_baseline"] = {"value": round(cpu["iters_per_s"], 5), "unit": "iters/s", "cores": cpu["cores"],
-                                    "kind": "port", "sample": cpu["sample"],
-                                    "time_per_iteration_s": round(cpu["time_per_iteration_s"], 3),
-                                    "p_build_s_extrapolated": round(cpu["p_build_s_extrapolated"], 1)}
+            line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
@@ -443,10 +566,12 @@ def run_reference(args):
     ws, rank, local = dist_env()
     if rank != 0:
         return
-    from paper_2507_02809_b200.configs import NAMES, RESTART, TOL
+    cfg = args.config
+    iters = golden_iterations(cfg, args.iters_hint)
+    threads = os.cpu_count() or 1
     samples = []
     for i in range(args.warmup + args.steps):
-        r = cpu_reference_sample(args.config, args.iters_hint)
+        r = cpu_reference_sample(cfg, iters, threads)
         if i >= args.warmup:
             samples.append(r)
     v = float(np.mean([s["iters_per_s"] for s in samples]))
@@ -454,23 +579,26 @@ def run_reference(args):
     line = {
         "impl": "reference",
         "metric": METRIC,
-        "value": round(v, 5),
+        "value": round(v, 6),
         "unit": "iters/s",
         "n_gpus": ws,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(t_iter * 1e3, 1),
+        "time_to_solve_s": round(float(np.mean([s["time_to_solve_s_extrapolated"] for s in samples])), 2),
+        "iterations_per_solve": iters,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": NAMES[args.config], "restart": RESTART, "tol": TOL[args.config],
-                   "note": "CPU restatement of the reference (oracle/, numpy+scipy); the reference needs "
-                           "Eigen3/FFTW3 which are absent, so it cannot be built here"},
-        "cpu_baseline": {"value": round(v, 5), "unit": "iters/s", "cores": samples[-1]["cores"], "kind": "port",
+        "data": "synthetic (BASELINE.json config; observation by the forward solve of f* + seeded Gaussian noise)",
+        "config": workload_config(cfg, ws),
+        "note": "CPU restatement of the reference (oracle/, numpy+scipy, reference order of operations); the "
+                "reference needs Eigen3/FFTW3, absent here, so it cannot be built; each step is a bounded sample "
+                "(one A apply, sampled P levels, one MGS step) extrapolated to one GMRES iteration",
+        "cpu_baseline": {"value": round(v, 6), "unit": "iters/s", "cores": threads, "kind": "port",
                          "sample": samples[-1]["sample"]},
-        "e2e": {"value": round(v, 5), "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": round(v, 6), "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -481,9 +609,10 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--iters-hint", type=int, default=12, help="GMRES iterations per solve assumed by the CPU arm")
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
+    ap.add_argument("--iters-hint", type=int, default=12, help="GMRES iterations per solve if no golden exists")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config table")
     ap.add_argument("--profile", action="store_true", help="bracket the timed region with cudaProfilerStart/Stop")
     args = ap.parse_args()
     if args.warmup < 3:

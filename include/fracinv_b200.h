@@ -30,7 +30,8 @@ extern "C" {
  *   FI_E_SINGULAR  SingularBlockError (time index via fi_last_error_time_index)
  *   FI_E_DOMAIN    std::domain_error (invalid parameters)
  *   FI_E_CUDA      CUDA runtime failure / no device
- *   FI_E_NOCONV    reserved (non-convergence is reported in fi_gmres_report, not as an error)
+ *   FI_E_NOCONV    a tau-PCG block solve stopped at maxit above its tolerance (fi_precond_apply_host;
+ *                  GMRES non-convergence itself is reported in fi_gmres_report, not as an error)
  *   FI_E_CONFIG    ConfigError
  */
 enum {
@@ -131,6 +132,11 @@ void fi_precond_destroy(fi_precond* P);
 /* y = P^{-1} z (forward block substitution), device vectors, async. */
 int fi_precond_apply(fi_precond* P, const double* z_dev, double* y_dev);
 int fi_precond_apply_host(fi_precond* P, const double* z_host, double* y_host);
+/* Inner-solve counters of the tau-PCG block solve (inner = 1), accumulated on the device since the last
+ * reset (fi_gmres resets them when it starts): out[0] CG steps, out[1] block solves that stopped at maxit
+ * above their tolerance, out[2] most CG steps of one block solve, out[3] preconditioner applies.  All zero
+ * for dense blocks.  Synchronises the context's stream; reset != 0 zeroes the counters after reading. */
+int fi_precond_stats(fi_precond* P, long long out[4], int reset);
 /* Device memory held by the preconditioner's per-level inverses (bytes). */
 long long fi_precond_bytes(const fi_precond* P);
 /* refine == 0 (default for dense blocks): one FP64 sweep over the polished inverses (built to the
@@ -169,6 +175,8 @@ typedef struct {
     double wall_time_seconds;
     double final_true_residual;
     int history_len;
+    int inner_nonconverged; /* EXTENSION: tau-PCG block solves of this solve that stopped at maxit above
+                               their tolerance (0 for dense blocks; see fi_precond_stats) */
 } fi_gmres_report;
 
 /* P may be NULL (no preconditioning); x0_dev may be NULL (zero start). */

@@ -32,8 +32,16 @@ import math
 import time
 from typing import Callable, List, Optional, Sequence
 
+import os
+
 import numpy as np
+import scipy.fft as _sfft
 import scipy.linalg as sla
+
+# Threads for the oracle's batched FFTs (scipy.fft / pocketfft; the arithmetic does not depend on
+# the thread count).  The reference's FFTW plans are single-threaded (fft.cpp:47-50): set
+# FI_ORACLE_WORKERS=1 for a reference-faithful 1-core timing.
+FFT_WORKERS = int(os.environ.get("FI_ORACLE_WORKERS", "0")) or (os.cpu_count() or 1)
 
 # --------------------------------------------------------------------------- errors
 # errors.hpp:9-43
@@ -318,8 +326,8 @@ class ToeplitzOperator:
         d = self.grid.d
         xs = x.reshape(batch + tuple(self.grid.n))
         axes = tuple(range(len(batch), len(batch) + d))
-        X = np.fft.rfftn(xs, s=self.embed, axes=axes)
-        y = np.fft.irfftn(X * self.spectrum, s=self.embed, axes=axes)
+        X = _sfft.rfftn(xs, s=self.embed, axes=axes, workers=FFT_WORKERS)
+        y = _sfft.irfftn(X * self.spectrum, s=self.embed, axes=axes, workers=FFT_WORKERS)
         sl = (Ellipsis,) + tuple(slice(0, v) for v in self.grid.n)
         return np.ascontiguousarray(y[sl]).reshape(batch + (self.dim,))
 
@@ -922,15 +930,19 @@ def gmres(apply_A, apply_M_inv, b: np.ndarray, tol: float = 1e-8, maxit: int = 0
             w = prec(apply_A(V[k]))
             pre_norm = float(np.linalg.norm(w))
             h = [0.0] * (k + 2)
+            tmp = np.empty_like(w)  # w -= h V[i] without temporaries (same arithmetic)
             for i in range(k + 1):  # modified Gram-Schmidt (krylov.cpp:127-132)
                 hik = float(V[i] @ w)
                 h[i] += hik
-                w = w - hik * V[i]
+                np.multiply(V[i], hik, out=tmp)
+                np.subtract(w, tmp, out=w)
             if np.linalg.norm(w) < pre_norm * 0.70710678118654752:  # krylov.cpp:134-140
                 for i in range(k + 1):
                     corr = float(V[i] @ w)
                     h[i] += corr
-                    w = w - corr * V[i]
+                    np.multiply(V[i], corr, out=tmp)
+                    np.subtract(w, tmp, out=w)
+            del tmp
             hnext = float(np.linalg.norm(w))
             h[k + 1] = hnext
             if hnext > breakdown_tol:

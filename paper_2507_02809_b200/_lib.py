@@ -49,6 +49,7 @@ class GmresReport(ctypes.Structure):
         ("wall_time_seconds", ctypes.c_double),
         ("final_true_residual", ctypes.c_double),
         ("history_len", ctypes.c_int),
+        ("inner_nonconverged", ctypes.c_int),
     ]
 
 
@@ -89,6 +90,7 @@ _SIGS = {
     "fi_precond_apply_host": (ctypes.c_int, [c_void_p, c_double_p, c_double_p]),
     "fi_precond_apply_timed": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, ctypes.c_int, c_double_p]),
     "fi_precond_bytes": (ctypes.c_longlong, [c_void_p]),
+    "fi_precond_stats": (ctypes.c_int, [c_void_p, ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]),
     "fi_precond_set_refine": (ctypes.c_int, [c_void_p, ctypes.c_int]),
     "fi_precond_create_ex": (ctypes.c_int, [c_void_p, ctypes.c_longlong, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                              ctypes.POINTER(c_void_p)]),

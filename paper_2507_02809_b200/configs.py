@@ -15,6 +15,8 @@ NOISE = {0: 0.01, 1: 0.005, 2: 0.01, 3: 0.01, 4: 0.05}
 TOL = {0: 1e-10, 1: 1e-10, 2: 1e-10, 3: 1e-10, 4: 1e-8}
 RESTART = 50
 SEED_BASE = 1000
+# (interior points per direction, time steps) per config: the shapes both bench arms report
+SHAPES = {0: ((255,), 64), 1: ((4095,), 512), 2: ((127, 127), 128), 3: ((255, 255), 256), 4: ((255, 255), 512)}
 NAMES = {0: "config0_1d_M255_N64", 1: "config1_1d_M4095_N512", 2: "config2_2d_M127x127_N128",
          3: "config3_2d_M255x255_N256", 4: "config4_2d_M255x255_N512"}
 

@@ -2,8 +2,11 @@
 // into status codes; the message and SingularBlockError time index are kept per host
 // thread (fi_last_error, fi_last_error_time_index).
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "krylov.cuh"
@@ -50,6 +53,12 @@ int guard(F&& f) {
 
 void require(bool ok, int code, const std::string& msg) {
     if (!ok) throw fib::Error(code, msg);
+}
+
+// every context-bound entry point runs on the context's device, whatever the calling thread's
+// current device is (a host thread may drive contexts on several devices)
+void bind(const fi_ctx* ctx) {
+    if (ctx) FI_CUDA(cudaSetDevice(ctx->device));
 }
 
 __global__ void pack_kernel(const double* ref, double* pad, long long total, long long Np, long long N, int n2,
@@ -113,6 +122,18 @@ fi_precond* build_precond(fi_system* sys, long long block_cap, int mode = -1, do
 }  // namespace
 
 namespace fib {
+void ensure_smem_attr(const void* func, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> set;  // (device, kernel) -> bytes allowed
+    int dev = 0;
+    FI_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = set[{dev, func}];
+    if (bytes <= have) return;
+    FI_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
+}
+
 void pack_vector(fi_ctx* ctx, const Layout& L, const double* ref, double* pad) { pack_levels(ctx, L, ref, pad, L.S + 1); }
 void unpack_vector(fi_ctx* ctx, const Layout& L, const double* pad, double* ref) {
     unpack_levels(ctx, L, pad, ref, L.S + 1);
@@ -157,7 +178,11 @@ void fi_ctx_destroy(fi_ctx* ctx) {
 void* fi_ctx_stream(fi_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 int fi_ctx_synchronize(fi_ctx* ctx) {
-    return guard([&] { FI_CUDA(cudaStreamSynchronize(ctx->stream)); });
+    return guard([&] {
+        require(ctx != nullptr, FI_E_DOMAIN, "fi_ctx_synchronize: NULL context");
+        bind(ctx);
+        FI_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
 }
 
 const char* fi_last_error(void) { return g_err.c_str(); }
@@ -183,6 +208,7 @@ int fi_symbol_coeffs_md(double omega, int d, const int* n, long long sample_cap,
 int fi_symbol_coeffs_md_dev(fi_ctx* ctx, double omega, int d, const int* n, long long sample_cap, double* coeffs) {
     return guard([&] {
         require(ctx && n && coeffs, FI_E_DOMAIN, "fi_symbol_coeffs_md_dev: NULL argument");
+        bind(ctx);
         const long long cap = sample_cap <= 0 ? (1LL << 26) : sample_cap;
         if (d == 2) fib::symbol_coeffs_2d_dev(ctx, omega, n[0], n[1], cap, coeffs);
         else fib::symbol_coeffs_md(omega, d, n, cap, coeffs);  // d = 1: the host sum (1D uses the recursion)
@@ -208,7 +234,7 @@ int fi_system_create(fi_ctx* ctx, const fi_system_desc* desc, fi_system** out) {
         for (int s = 1; s <= S; ++s)
             require(desc->q[s - 1] > 0.0, FI_E_DOMAIN,
                     "q(t) must be positive at every time level, violated at s = " + std::to_string(s));
-        FI_CUDA(cudaSetDevice(ctx->device));
+        bind(ctx);
         fi_system* sys = new fi_system();
         try {
             sys->ctx = ctx;
@@ -280,6 +306,7 @@ long long fi_system_space_dim(const fi_system* sys) { return sys ? sys->L.N : 0;
 int fi_system_apply(fi_system* sys, const double* y_dev, double* z_dev) {
     return guard([&] {
         require(sys && y_dev && z_dev, FI_E_DOMAIN, "fi_system_apply: NULL argument");
+        bind(sys->ctx);
         fi_ctx* ctx = sys->ctx;
         fib::pack_vector(ctx, sys->L, y_dev, sys->ubuf.p);
         fib::toeplitz_apply(ctx, sys->view(), sys->ubuf.p, sys->zbuf.p, nullptr);
@@ -290,6 +317,7 @@ int fi_system_apply(fi_system* sys, const double* y_dev, double* z_dev) {
 int fi_system_apply_host(fi_system* sys, const double* y_host, double* z_host) {
     return guard([&] {
         require(sys && y_host && z_host, FI_E_DOMAIN, "fi_system_apply_host: NULL argument");
+        bind(sys->ctx);
         fi_ctx* ctx = sys->ctx;
         const size_t bytes = (size_t)sys->L.nRef() * sizeof(double);
         fib::DevBuf<double> y((size_t)sys->L.nRef()), z((size_t)sys->L.nRef());
@@ -305,6 +333,7 @@ int fi_system_apply_host(fi_system* sys, const double* y_host, double* z_host) {
 int fi_system_apply_timed(fi_system* sys, const double* y_dev, double* z_dev, int reps, double* ms_avg) {
     return guard([&] {
         require(sys && y_dev && z_dev && ms_avg && reps > 0, FI_E_DOMAIN, "fi_system_apply_timed: bad argument");
+        bind(sys->ctx);
         fi_ctx* ctx = sys->ctx;
         fib::pack_vector(ctx, sys->L, y_dev, sys->ubuf.p);
         fib::toeplitz_apply(ctx, sys->view(), sys->ubuf.p, sys->zbuf.p, nullptr);  // warm-up
@@ -324,6 +353,7 @@ int fi_system_apply_timed(fi_system* sys, const double* y_dev, double* z_dev, in
 int fi_precond_create(fi_system* sys, long long block_cap, fi_precond** out) {
     return guard([&] {
         require(sys && out, FI_E_DOMAIN, "fi_precond_create: NULL argument");
+        bind(sys->ctx);
         *out = build_precond(sys, block_cap);
         sys->refs++;
     });
@@ -332,6 +362,7 @@ int fi_precond_create(fi_system* sys, long long block_cap, fi_precond** out) {
 int fi_precond_create_ex(fi_system* sys, long long block_cap, int inner, double tol, int maxit, fi_precond** out) {
     return guard([&] {
         require(sys && out, FI_E_DOMAIN, "fi_precond_create_ex: NULL argument");
+        bind(sys->ctx);
         require(inner >= -1 && inner <= 1, FI_E_DOMAIN, "fi_precond_create_ex: inner must be -1, 0 or 1");
         require(tol > 0.0 && maxit > 0, FI_E_DOMAIN, "fi_precond_create_ex: tol > 0 and maxit > 0 required");
         *out = build_precond(sys, block_cap, inner, tol, maxit);
@@ -364,6 +395,7 @@ int fi_precond_set_refine(fi_precond* P, int refine) {
 int fi_precond_apply(fi_precond* P, const double* z_dev, double* y_dev) {
     return guard([&] {
         require(P && z_dev && y_dev, FI_E_DOMAIN, "fi_precond_apply: NULL argument");
+        bind(P->sys->ctx);
         fi_ctx* ctx = P->sys->ctx;
         fib::pack_vector(ctx, P->sys->L, z_dev, P->zbuf.p);
         fib::precond_apply(ctx, P, P->zbuf.p, P->ybuf.p, P->sys->L.S + 1, nullptr);
@@ -374,9 +406,12 @@ int fi_precond_apply(fi_precond* P, const double* z_dev, double* y_dev) {
 int fi_precond_apply_host(fi_precond* P, const double* z_host, double* y_host) {
     return guard([&] {
         require(P && z_host && y_host, FI_E_DOMAIN, "fi_precond_apply_host: NULL argument");
+        bind(P->sys->ctx);
         fi_ctx* ctx = P->sys->ctx;
         const fib::Layout& L = P->sys->L;
         const size_t bytes = (size_t)L.nRef() * sizeof(double);
+        unsigned long long before[4] = {0, 0, 0, 0}, after[4] = {0, 0, 0, 0};
+        if (P->mode == 1) fib::precond_iterative_stats(P, before, false);
         fib::DevBuf<double> z((size_t)L.nRef()), y((size_t)L.nRef());
         FI_CUDA(cudaMemcpyAsync(z.p, z_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
         fib::pack_vector(ctx, L, z.p, P->zbuf.p);
@@ -384,12 +419,30 @@ int fi_precond_apply_host(fi_precond* P, const double* z_host, double* y_host) {
         fib::unpack_vector(ctx, L, P->ybuf.p, y.p);
         FI_CUDA(cudaMemcpyAsync(y_host, y.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (P->mode == 1) {
+            fib::precond_iterative_stats(P, after, false);
+            if (after[1] > before[1])
+                throw fib::Error(FI_E_NOCONV, "precond_apply: " + std::to_string(after[1] - before[1]) +
+                                                  " tau-PCG block solve(s) stopped at maxit = " +
+                                                  std::to_string(P->it_maxit) + " above tol");
+        }
+    });
+}
+
+int fi_precond_stats(fi_precond* P, long long out[4], int reset) {
+    return guard([&] {
+        require(P && out, FI_E_DOMAIN, "fi_precond_stats: NULL argument");
+        bind(P->sys->ctx);
+        unsigned long long v[4] = {0, 0, 0, 0};
+        if (P->mode == 1) fib::precond_iterative_stats(P, v, reset != 0);
+        for (int i = 0; i < 4; ++i) out[i] = (long long)v[i];
     });
 }
 
 int fi_precond_apply_timed(fi_precond* P, const double* z_dev, double* y_dev, int reps, double* ms_avg) {
     return guard([&] {
         require(P && z_dev && y_dev && ms_avg && reps > 0, FI_E_DOMAIN, "fi_precond_apply_timed: bad argument");
+        bind(P->sys->ctx);
         fi_ctx* ctx = P->sys->ctx;
         const fib::Layout& L = P->sys->L;
         fib::pack_vector(ctx, L, z_dev, P->zbuf.p);
@@ -424,6 +477,7 @@ int fi_forward_solve(fi_system* sys, fi_precond* P, const double* rho_host, cons
                      double* mu_host) {
     return guard([&] {
         require(sys && rho_host && f_host && mu_host, FI_E_DOMAIN, "fi_forward_solve: NULL argument");
+        bind(sys->ctx);
         fi_ctx* ctx = sys->ctx;
         const fib::Layout& L = sys->L;
         fi_precond* own = nullptr;
@@ -466,6 +520,7 @@ int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x
              const fi_gmres_opts* opts, fi_gmres_report* report, double* history_host, int history_cap) {
     return guard([&] {
         require(sys && b_dev && x_dev && opts && report, FI_E_DOMAIN, "fi_gmres: NULL argument");
+        bind(sys->ctx);
         require(!P || P->sys == sys, FI_E_DIM, "fi_gmres: preconditioner belongs to another system");
         fi_ctx* ctx = sys->ctx;
         const fib::Layout& L = sys->L;
@@ -506,9 +561,16 @@ int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x
         }
         sys->engine->set_fused(split && P ? &Fz : nullptr);
         std::vector<double> hist;
+        if (P && P->mode == 1) FI_CUDA(cudaMemsetAsync(P->it_stats.p, 0, P->it_stats.bytes(), ctx->stream));
         sys->engine->solve(A, P ? &M : nullptr, b.p, x0_dev ? x0.p : nullptr, x.p, opts->tol, maxit, opts->restart,
                            report, hist);
         sys->engine->set_fused(nullptr);
+        report->inner_nonconverged = 0;
+        if (P && P->mode == 1) {
+            unsigned long long st[4];
+            fib::precond_iterative_stats(P, st, false);
+            report->inner_nonconverged = (int)st[1];
+        }
         fib::unpack_vector(ctx, L, x.p, x_dev);
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
         copy_history(hist, history_host, history_cap);
@@ -520,6 +582,7 @@ int fi_mgs_round_timed(fi_ctx* ctx, long long n, double* w_dev, const double* x_
     return guard([&] {
         require(ctx && w_dev && x_dev && y_dev && ms_avg && n > 0 && reps > 0, FI_E_DOMAIN,
                 "fi_mgs_round_timed: bad argument");
+        bind(ctx);
         fib::GmresEngine eng(ctx, n);
         *ms_avg = eng.time_mgs_round(w_dev, x_dev, y_dev, reps);
     });
@@ -528,6 +591,7 @@ int fi_mgs_round_timed(fi_ctx* ctx, long long n, double* w_dev, const double* x_
 int fi_assemble_dense(fi_system* sys, int kind, long long cap, double* M_dev) {
     return guard([&] {
         require(sys && M_dev, FI_E_DOMAIN, "fi_assemble_dense: NULL argument");
+        bind(sys->ctx);
         fib::assemble_dense(sys->ctx, sys, kind, cap <= 0 ? 4096 : cap, M_dev);
     });
 }
@@ -544,6 +608,7 @@ int fi_gmres_host(fi_system* sys, fi_precond* P, const double* b_host, const dou
     int rc = FI_OK;
     int rc2 = guard([&] {
         require(sys && b_host && x_host, FI_E_DOMAIN, "fi_gmres_host: NULL argument");
+        bind(sys->ctx);
         fi_ctx* ctx = sys->ctx;
         const size_t n = (size_t)sys->L.nRef();
         // staging for the reference-layout host vectors: [b | x | x0], kept across calls
@@ -567,6 +632,7 @@ int fi_gmres_op(fi_ctx* ctx, long long n, fi_linop_fn apply_A, void* user_A, fi_
                 fi_gmres_report* report, double* history_host, int history_cap) {
     return guard([&] {
         require(ctx && apply_A && b_dev && x_dev && opts && report && n > 0, FI_E_DOMAIN, "fi_gmres_op: bad argument");
+        bind(ctx);
         fib::Op A = [apply_A, user_A](const double* in, double* out, const int*) {
             if (apply_A(user_A, in, out) != 0) throw fib::Error(FI_E_DOMAIN, "fi_gmres_op: apply_A callback failed");
         };
@@ -577,6 +643,7 @@ int fi_gmres_op(fi_ctx* ctx, long long n, fi_linop_fn apply_A, void* user_A, fi_
         fib::GmresEngine eng(ctx, n);
         std::vector<double> hist;
         eng.solve(A, apply_M ? &M : nullptr, b_dev, x0_dev, x_dev, opts->tol, maxit, opts->restart, report, hist);
+        report->inner_nonconverged = 0;
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
         copy_history(hist, history_host, history_cap);
     });

@@ -116,6 +116,11 @@ namespace fib {
 
 struct SystemDev;  // defined in system.cuh
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute: raise it to at least `bytes`
+// once per (device, kernel).  Thread-safe; the calling thread's current device must be the context's
+// (every C-ABI entry binds it, abi.cu).
+void ensure_smem_attr(const void* func, size_t bytes);
+
 // Layout conversion: reference (S+1)*N <-> padded (S+1)*Np.
 void pack_vector(fi_ctx* ctx, const Layout& L, const double* ref, double* pad);
 void unpack_vector(fi_ctx* ctx, const Layout& L, const double* pad, double* ref);

@@ -38,6 +38,8 @@ struct fi_precond {
     std::vector<int> it_direct;
     fib::DevBuf<double2> it_tw1, it_tw2, it_X;
     fib::DevBuf<double> it_lamT, it_lamB, it_Rr, it_vec, it_dmean_d, it_hb;
+    fib::DevBuf<double2> it_F;                   // fused kernel: Zh, Xp, Yb half-spectrum buffers
+    fib::DevBuf<unsigned long long> it_stats;    // CG steps, levels stopped at maxit, max steps, applies
     fib::DevBuf<int> it_direct_d;
     int it_fgrid = 0;                            // fused kernel: cooperative grid size
     fib::DevBuf<double> it_fparts;               // fused kernel: 2 x grid block partials
@@ -58,6 +60,9 @@ void precond_times_operator(fi_ctx* ctx, fi_precond* P, const double* v, double*
 bool iterative_supported(const Layout& L);
 void precond_build_iterative(fi_precond* P, double tol, int maxit);
 void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip);
+// inner-solve counters accumulated on the device since the last reset: [0] CG steps, [1] levels that
+// stopped at maxit without reaching the tolerance, [2] most steps of one level, [3] applies (synchronises)
+void precond_iterative_stats(fi_precond* P, unsigned long long out[4], bool reset);
 void precond_build(fi_precond* P);
 // build-time polish of the explicit inverses (precond_polish.cu): W <- W - Q Z^T, a rank-32
 // sketch of W - G_x^{-1} D2 from double-double residuals

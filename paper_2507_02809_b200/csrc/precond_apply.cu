@@ -496,12 +496,8 @@ __global__ void add_kernel(const double* __restrict__ a, const double* __restric
 template <typename T>
 void launch_sweep(fi_ctx* ctx, fi_precond* P, const T* H, const double* z, double* y, int levels, int refine_f,
                   const int* skip) {
-    static bool configured = false;
     const int smem = sweep_smem_bytes<T>();
-    if (!configured) {
-        FI_CUDA(cudaFuncSetAttribute(sweep_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        configured = true;
-    }
+    ensure_smem_attr((const void*)sweep_kernel<T>, (size_t)smem);
     const fi_system* sys = P->sys;
     SweepArgs a;
     a.H = H;
@@ -582,8 +578,7 @@ void launch_sweep(fi_ctx* ctx, fi_precond* P, const T* H, const double* z, doubl
 
 int precond_apply_grid(fi_ctx* ctx, long long T, long long Np) {
     int per_sm = 0;
-    FI_CUDA(cudaFuncSetAttribute(sweep_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 sweep_smem_bytes<double>()));
+    ensure_smem_attr((const void*)sweep_kernel<double>, (size_t)sweep_smem_bytes<double>());
     FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<double>, THREADS,
                                                           sweep_smem_bytes<double>()));
     if (per_sm < 1) throw Error(FI_E_CUDA, "precond sweep kernel cannot be resident");

@@ -797,11 +797,7 @@ void hodlr_sweep(fi_ctx* ctx, HodlrData* h, const fi_system* sys, const double* 
                  int levels, const int* skip) {
     const Layout& L = sys->L;
     const size_t smem = hodlr_sweep_smem(levels, h->nb);
-    static size_t configured = 0;
-    if (smem > configured) {
-        FI_CUDA(cudaFuncSetAttribute(hodlr_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
-    }
+    ensure_smem_attr((const void*)hodlr_sweep_kernel, smem);
     HArgs a;
     a.hd = h->hd.p;
     a.nlev = levels;

@@ -53,7 +53,10 @@ struct ItArgs {
     double* zz;  // PCG z
     double* p;
     double* Ap;
-    double2* X;   // L1 x L2 complex work
+    double2* X;   // L1 x L2 complex work (setup: spectrum of B)
+    double2* Zh;  // n1 x (L2/2 + 1): row FFTs (half spectra) of z (or of the warm-start guess x0)
+    double2* Xp;  // n1 x (L2/2 + 1): row FFTs of the search direction p
+    double2* Yb;  // n1 x (L2/2 + 1): output of the column pass of B p
     double* hb;   // 8 x Np: old part of the L1 history of the current 8-level block's targets
     double* Rr;   // n1 x n2 real DST work
     const int* skip;
@@ -86,74 +89,6 @@ __device__ double2* fft_smem(double2* src, double2* dst, int cnt, int L, int lg,
             const double2 x1 = cmul(sc[j + half], w);
             dc[2 * j - k] = make_double2(x0.x + x1.x, x0.y + x1.y);
             dc[2 * j - k + p] = make_double2(x0.x - x1.x, x0.y - x1.y);
-        }
-        __syncthreads();
-        double2* t = src;
-        src = dst;
-        dst = t;
-    }
-    return src;
-}
-
-// Radix-4 Stockham variant for the fused kernel: half the passes (and __syncthreads) of fft_smem,
-// power-of-two index arithmetic, twiddles from a shared-memory copy of the half table
-// (tw[t] = exp(-2 pi i t / L), t < L/2; t >= L/2 uses -tw[t - L/2]).  Same transform as fft_smem.
-__device__ __forceinline__ double2 tw_at(const double2* tw, int t, int half) {
-    if (t < half) return tw[t];
-    const double2 w = tw[t - half];
-    return make_double2(-w.x, -w.y);
-}
-__device__ double2* fft4_smem(double2* src, double2* dst, int cnt, int L, int lg, const double2* tw, bool inverse,
-                              int tid, int nthr) {
-    const int half = L >> 1;
-    int s = 0, p = 1;
-    if (lg & 1) {  // one radix-2 pass first (p = 1: no twiddles)
-        for (int q = tid; q < cnt * half; q += nthr) {
-            const int c = q >> (lg - 1), j = q & (half - 1);
-            const double2* sc = src + c * L;
-            double2* dc = dst + c * L;
-            const double2 x0 = sc[j], x1 = sc[j + half];
-            dc[2 * j] = make_double2(x0.x + x1.x, x0.y + x1.y);
-            dc[2 * j + 1] = make_double2(x0.x - x1.x, x0.y - x1.y);
-        }
-        __syncthreads();
-        double2* t = src;
-        src = dst;
-        dst = t;
-        s = 1;
-        p = 2;
-    }
-    const int quarter = L >> 2;
-    for (; s < lg; s += 2, p <<= 2) {
-        const int lgp = s;  // p = 2^s
-        const int tstep = L >> (lgp + 2);  // L / (4p)
-        for (int q = tid; q < cnt * quarter; q += nthr) {
-            const int c = q >> (lg - 2), j = q & (quarter - 1);
-            const int k = j & (p - 1);
-            const double2* sc = src + c * L;
-            double2* dc = dst + c * L;
-            double2 a0 = sc[j], a1 = sc[j + quarter], a2 = sc[j + 2 * quarter], a3 = sc[j + 3 * quarter];
-            if (k) {
-                double2 w1 = tw_at(tw, k * tstep, half), w2 = tw_at(tw, 2 * k * tstep, half),
-                        w3 = tw_at(tw, 3 * k * tstep, half);
-                if (inverse) {
-                    w1.y = -w1.y;
-                    w2.y = -w2.y;
-                    w3.y = -w3.y;
-                }
-                a1 = cmul(a1, w1);
-                a2 = cmul(a2, w2);
-                a3 = cmul(a3, w3);
-            }
-            const double2 s02 = make_double2(a0.x + a2.x, a0.y + a2.y), d02 = make_double2(a0.x - a2.x, a0.y - a2.y);
-            const double2 s13 = make_double2(a1.x + a3.x, a1.y + a3.y), d13 = make_double2(a1.x - a3.x, a1.y - a3.y);
-            // forward: y1 = d02 - i d13, y3 = d02 + i d13 (inverse: signs of i swapped)
-            const double2 id13 = inverse ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x);  // -/+ i d13
-            const int o = 4 * (j - k) + k;
-            dc[o] = make_double2(s02.x + s13.x, s02.y + s13.y);
-            dc[o + p] = make_double2(d02.x + id13.x, d02.y + id13.y);
-            dc[o + 2 * p] = make_double2(s02.x - s13.x, s02.y - s13.y);
-            dc[o + 3 * p] = make_double2(d02.x - id13.x, d02.y - id13.y);
         }
         __syncthreads();
         double2* t = src;
@@ -203,26 +138,36 @@ __global__ void fft_cols_to_spec(ItArgs a, double* lamB) {
 }
 
 // ------------------------------------------------------------------ fused persistent solve
-// The whole forward substitution of a tau-PCG preconditioner apply in ONE cooperative kernel: the
-// level loop and the CG loop run on the device, the FFT passes of a CG step are phases separated
-// by grid barriers (6 per step instead of 7 dependent kernel launches), the scalars of the
-// recurrence (alpha, beta, rz, ...) live in every CTA's registers, and the global dot products are
-// summed in a fixed order (every CTA obtains the identical, bit-reproducible value).
+// The whole forward substitution of a tau-PCG preconditioner apply is ONE cooperative kernel: the level
+// loop and the CG loop run on the device, the transform passes of a CG step are phases separated by grid
+// barriers, the scalars of the recurrence live in every CTA's registers, and the global dot products
+// are summed in a fixed order (every CTA obtains the identical, bit-reproducible value).
+//
+// A CG step is four passes (R = rows, C = columns; the recurrence is the oracle's TauPCG.solve):
+//   T3  (R)  z = S2(w) (last DST of the tau solve), r.z, z.delta.z, z.delta.p, and F2(z) (row FFTs of z)
+//   B2  (C)  X = F2(z) + beta F2(p_old) = F2(p) (linearity: the row FFT of p = z + beta p_old is never
+//            taken), column FFT, x lambda_B, p.Bp by Parseval, inverse column FFT
+//   B3  (R)  inverse row FFT -> B p; p = z + beta p_old; Ap = c Bp + delta p; x, r updates; ||r||^2;
+//            S2(r) (first DST of the next tau solve)
+//   T2  (C)  S1, divide by the tau eigenvalues, S1
+// p.delta.p of the new direction follows from z.delta.z + 2 beta z.delta.p_old + beta^2 p_old.delta.p_old.
+// Real data are packed two rows (two columns) per complex transform; the column pass of B works on the
+// L2/2 + 1 columns of the half spectrum.  The FFTs are radix-8 Stockham passes in registers, one group
+// of L/8 threads per transform, exchanging through padded shared memory.
+constexpr int FT = 256;      // threads per CTA of the fused kernel
+constexpr int kRedMax = 4;   // scalars per grid reduction
+
 struct FusedCtl {
-    unsigned* bar;    // monotone grid-barrier counter (zeroed before the launch)
-    double* parts;    // 2 x G block partials (ping-pong by reduction index)
-    unsigned long long* trace;  // optional [10] per-phase time sums of CTA 0 (FI_ITER_TRACE=1)
-    int rpc;    // rows per CTA in the row passes (G * rpc >= n1)
-    int cbf;    // columns per CTA in the column passes (power of two, cbf * L1 <= 8 * 256)
-    int lgcbf;
-    int cbt, lgcbt;  // the same for the tau column pass (n2 columns instead of L2)
+    unsigned* bar;                // monotone grid-barrier counter (zeroed before the launch)
+    double* parts;                // 2 parities x G x kRedMax block partials
+    unsigned long long* trace;    // optional [10] per-phase time sums of CTA 0 (FI_ITER_TRACE=1)
+    unsigned long long* stats;    // [0] CG steps, [1] levels stopped at maxit, [2] max steps of a level, [3] applies
 };
 __device__ __forceinline__ unsigned long long gtime_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -234,15 +179,124 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     return v;
 }
 
-__global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 mul_i(double2 a, bool inv) {  // -i a (forward), +i a (inverse)
+    return inv ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+// shared-memory index with one pad element per 8 (the radix-8 scatter of the first pass is conflict-free)
+__device__ __forceinline__ int pad8(int i) { return i + (i >> 3); }
+
+// in-register DFT of length 8 (decimation in frequency), forward or inverse (conjugate twiddles)
+__device__ __forceinline__ void dft8(double2 (&a)[8], bool inv) {
+    constexpr double r = 0.70710678118654752440;
+    double2 b[8];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        b[m] = cadd(a[m], a[m + 4]);
+        b[m + 4] = csub(a[m], a[m + 4]);
+    }
+    if (!inv) {
+        b[5] = make_double2(r * (b[5].x + b[5].y), r * (b[5].y - b[5].x));    // x (1 - i)/sqrt2
+        b[7] = make_double2(r * (b[7].y - b[7].x), -r * (b[7].x + b[7].y));   // x (-1 - i)/sqrt2
+    } else {
+        b[5] = make_double2(r * (b[5].x - b[5].y), r * (b[5].x + b[5].y));    // x (1 + i)/sqrt2
+        b[7] = make_double2(-r * (b[7].x + b[7].y), r * (b[7].x - b[7].y));  // x (-1 + i)/sqrt2
+    }
+    b[6] = mul_i(b[6], inv);
+    const double2 c0 = cadd(b[0], b[2]), c2 = csub(b[0], b[2]), c1 = cadd(b[1], b[3]), c3 = mul_i(csub(b[1], b[3]), inv);
+    const double2 c4 = cadd(b[4], b[6]), c6 = csub(b[4], b[6]), c5 = cadd(b[5], b[7]), c7 = mul_i(csub(b[5], b[7]), inv);
+    a[0] = cadd(c0, c1);
+    a[4] = csub(c0, c1);
+    a[2] = cadd(c2, c3);
+    a[6] = csub(c2, c3);
+    a[1] = cadd(c4, c5);
+    a[5] = csub(c4, c5);
+    a[3] = cadd(c6, c7);
+    a[7] = csub(c6, c7);
+}
+__device__ __forceinline__ double2 twv(const double2* tw, int t, int half, bool inv) {
+    double2 w = t < half ? tw[t] : make_double2(-tw[t - half].x, -tw[t - half].y);
+    if (inv) w.y = -w.y;
+    return w;
+}
+
+// Stockham FFT of length L = 2^lg by the nt threads (index t) of one group, between the group's two
+// padded shared buffers (index pad8(i)).  Input in src (natural order); returns the buffer holding the
+// output (natural order).  Every thread of the CTA must call it (it contains __syncthreads); groups
+// without a unit pass active = false.  Passes: one radix-2 or radix-4 pass if lg % 3 != 0, then radix-8.
+__device__ double2* fft_group(double2* src, double2* dst, int L, int lg, const double2* tw, bool inv, int t, int nt,
+                              bool active) {
+    const int half = L >> 1;
+    int p = 1;
+    const int rem = lg % 3;
+    if (rem == 1) {
+        if (active)
+            for (int j = t; j < half; j += nt) {
+                const double2 x0 = src[pad8(j)], x1 = src[pad8(j + half)];
+                dst[pad8(2 * j)] = cadd(x0, x1);
+                dst[pad8(2 * j + 1)] = csub(x0, x1);
+            }
+        __syncthreads();
+        double2* tt = src;
+        src = dst;
+        dst = tt;
+        p = 2;
+    } else if (rem == 2) {
+        const int q = L >> 2;
+        if (active)
+            for (int j = t; j < q; j += nt) {
+                const double2 a0 = src[pad8(j)], a1 = src[pad8(j + q)], a2 = src[pad8(j + 2 * q)], a3 = src[pad8(j + 3 * q)];
+                const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = mul_i(csub(a1, a3), inv);
+                dst[pad8(4 * j)] = cadd(s02, s13);
+                dst[pad8(4 * j + 1)] = cadd(d02, d13);
+                dst[pad8(4 * j + 2)] = csub(s02, s13);
+                dst[pad8(4 * j + 3)] = csub(d02, d13);
+            }
+        __syncthreads();
+        double2* tt = src;
+        src = dst;
+        dst = tt;
+        p = 4;
+    }
+    const int q = L >> 3;
+    for (; p < L; p <<= 3) {
+        const int tstep = L / (8 * p);
+        if (active)
+            for (int j = t; j < q; j += nt) {
+                const int k = j & (p - 1);
+                double2 v[8];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) v[m] = src[pad8(j + m * q)];
+                if (k) {
+#pragma unroll
+                    for (int m = 1; m < 8; ++m) {
+                        const double2 w = twv(tw, m * k * tstep, half, inv);
+                        v[m] = make_double2(v[m].x * w.x - v[m].y * w.y, v[m].x * w.y + v[m].y * w.x);
+                    }
+                }
+                dft8(v, inv);
+                const int o = (j - k) * 8 + k;
+#pragma unroll
+                for (int m = 0; m < 8; ++m) dst[pad8(o + m * p)] = v[m];
+            }
+        __syncthreads();
+        double2* tt = src;
+        src = dst;
+        dst = tt;
+    }
+    return src;
+}
+
+__global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     if (skipped(a)) return;
     extern __shared__ double2 sm[];
-    __shared__ double wred[8];
-    __shared__ double bcast;
-    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
+    __shared__ double wred[FT / 32][kRedMax];
+    __shared__ double bsum[kRedMax];
+    const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
     const long long Np = a.Np;
-    const int rpc = ctl.rpc, cbf = ctl.cbf, lgc = ctl.lgcbf, cbt = ctl.cbt, lgt = ctl.lgcbt;
+    const int n1 = a.n1, n2 = a.n2, L1 = a.L1, L2 = a.L2, H2 = a.L2 / 2 + 1, ld2 = a.ld2;
     unsigned target = 0;
     int rk = 0;
     unsigned long long tlast = 0;
@@ -274,371 +328,635 @@ __global__ void __launch_bounds__(256, 2) tau_pcg_fused(ItArgs a, FusedCtl ctl) 
         }
         __syncthreads();
     };
-    // deterministic grid sum: block partials in fixed order, every CTA gets the same total
-    auto greduce = [&](double v) -> double {
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == 0) wred[warp] = v;
+    // deterministic grid sum of cnt scalars: block partials in fixed order, every CTA gets the same totals
+    auto greduce = [&](double* v, int cnt) {
+        for (int c = 0; c < cnt; ++c) {
+            double x = v[c];
+            for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+            if (lane == 0) wred[warp][c] = x;
+        }
         __syncthreads();
-        double* pp = ctl.parts + (rk & 1) * G;
-        if (tid == 0) {
+        double* pp = ctl.parts + (size_t)(rk & 1) * G * kRedMax;
+        if (tid < cnt) {
             double b = 0.0;
-            for (int w = 0; w < nwarp; ++w) b += wred[w];
-            __stcg(pp + cta, b);
+            for (int w = 0; w < FT / 32; ++w) b += wred[w][tid];
+            __stcg(pp + (size_t)cta * kRedMax + tid, b);
         }
         gsync();
         if (warp == 0) {
-            // all of a lane's partials in flight at once (G <= 320), then a fixed-order sum
-            double pv[10];
-#pragma unroll
-            for (int u2 = 0; u2 < 10; ++u2) {
-                const int k = lane + 32 * u2;
-                pv[u2] = k < G ? __ldcg(pp + k) : 0.0;
+            for (int c = 0; c < cnt; ++c) {
+                double t = 0.0;
+                for (int k = lane; k < G; k += 32) t += __ldcg(pp + (size_t)k * kRedMax + c);
+                for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+                if (lane == 0) bsum[c] = t;
             }
-            double t = 0.0;
-#pragma unroll
-            for (int u2 = 0; u2 < 10; ++u2) t += pv[u2];
-            for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-            if (lane == 0) bcast = t;
         }
         __syncthreads();
         ++rk;
-        return bcast;
+        for (int c = 0; c < cnt; ++c) v[c] = bsum[c];
     };
-    const double sc1 = sqrt(2.0 / (a.n1 + 1)) * -0.5, sc2 = sqrt(2.0 / (a.n2 + 1)) * -0.5;
-    const int hs = max(rpc * a.L2, cbf * a.L1);
-    double2* u = sm;
-    double2* v = sm + hs;           // ping-pong halves
-    double2* tws1 = sm + 2 * hs;    // twiddle half tables in shared memory
-    double2* tws2 = tws1 + a.L1 / 2;
-    for (int t = tid; t < a.L1 / 2; t += nthr) tws1[t] = a.tw1[t];
-    for (int t = tid; t < a.L2 / 2; t += nthr) tws2[t] = a.tw2[t];
+    const double sc1 = sqrt(2.0 / (n1 + 1)) * -0.5, sc2 = sqrt(2.0 / (n2 + 1)) * -0.5;
+    double2* tws1 = sm;             // twiddle half tables in shared memory
+    double2* tws2 = sm + L1 / 2;
+    double2* gbuf = tws2 + L2 / 2;  // transform groups: two padded buffers each
+    for (int t = tid; t < L1 / 2; t += FT) tws1[t] = a.tw1[t];
+    for (int t = tid; t < L2 / 2; t += FT) tws2[t] = a.tw2[t];
     __syncthreads();
-    // this CTA's rows for every row pass (G * rpc >= n1): r0 .. r0 + nr - 1, transformed together
-    const int r0 = cta * rpc, nr = max(0, min(rpc, a.n1 - r0));
+    // group geometry of the row (length L2) and column (length L1) passes
+    const int ntR = max(L2 >> 3, 1), ngR = FT / ntR, gR = tid / ntR, tR = tid % ntR;
+    const int ntC = max(L1 >> 3, 1), ngC = FT / ntC, gC = tid / ntC, tC = tid % ntC;
+    const int PLR = pad8(L2) + 1, PLC = pad8(L1) + 1;  // padded buffer lengths
+    const int nuR = (n1 + 1) / 2, nuB = H2, nuT = (n2 + 1) / 2;  // units of the row, B-column, tau-column passes
+    const int rdR = (nuR + G * ngR - 1) / (G * ngR), rdB = (nuB + G * ngC - 1) / (G * ngC),
+              rdT = (nuT + G * ngC - 1) / (G * ngC);
 
-    // rows n1..L1-1 of the embedded B input stay zero for the whole apply
-    for (long long q = (long long)cta * nthr + tid; q < (long long)(a.L1 - a.n1) * a.L2; q += (long long)G * nthr)
-        a.X[(long long)a.n1 * a.L2 + q] = make_double2(0.0, 0.0);
-
-    // DST-I along this CTA's rows of `src` (row stride sstride, n2 values) into the same rows of Rr
-    auto dst_rows = [&](const double* src, long long sstride) {
-        if (nr == 0) return;
-        for (int q = tid; q < nr * a.L2; q += nthr) {
-            const int i = q >> a.lg2, j = q & (a.L2 - 1);
-            const double* row = src + (long long)(r0 + i) * sstride;
-            double val = 0.0;
-            if (j >= 1 && j <= a.n2) val = row[j - 1];
-            else if (j >= a.n2 + 2) val = -row[a.L2 - j - 1];
-            u[q] = make_double2(val, 0.0);
-        }
-        __syncthreads();
-        const double2* U = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, false, tid, nthr);
-        for (int q = tid; q < nr * a.n2; q += nthr) {
-            const int i = q / a.n2, k = q - i * a.n2;
-            a.Rr[(long long)(r0 + i) * a.n2 + k] = sc2 * U[i * a.L2 + k + 1].y;
-        }
-        __syncthreads();
+    // ---- group buffers and transforms.  Slot s of a pass owns the group buffers of group s; in round rd
+    // it holds the unit cta + G (s + ng rd).  Element work (loads, stores, dot products) is spread over
+    // all FT threads of the CTA, the transforms run on the groups.  Element loops load everything a
+    // thread needs for UF (or 2) elements into registers before the first store, so the loads of a
+    // thread are in flight together (a generic shared-memory store would otherwise pin every later
+    // global load behind it).
+    auto rbuf = [&](int g, int w) { return gbuf + (size_t)g * 2 * PLR + (size_t)w * PLR; };
+    auto cbuf = [&](int g, int w) { return gbuf + (size_t)g * 2 * PLC + (size_t)w * PLC; };
+    const int npR = (a.lg2 % 3 ? 1 : 0) + a.lg2 / 3, npC = (a.lg1 % 3 ? 1 : 0) + a.lg1 / 3;
+    // active slots of this CTA in round rd (a prefix: the unit index grows with the slot)
+    auto nact = [&](int nu, int ng, int rd) {
+        const int first = cta + G * ng * rd;
+        return first >= nu ? 0 : min(ng, (nu - first + G - 1) / G);
     };
-    // column pass of the tau solve: DST along columns, divide by the tau eigenvalues, DST back
-    auto tau_cols_phase = [&](int lv) {
-        const double c = level_c(a, lv), dmean = level_dmean(a, lv);
-        const int ngroups = (a.n2 + cbt - 1) / cbt;
-        for (int g = cta; g < ngroups; g += G) {
-            const int k0 = g * cbt, nc = min(cbt, a.n2 - k0);
-            // the tau eigenvalues of the element each thread divides later are loaded with the data
-            double ilam[8];
+    auto fftR = [&](int w, bool inv, int rd) -> int {
+        const bool act = cta + G * (gR + ngR * rd) < nuR;
+        fft_group(rbuf(gR, w), rbuf(gR, 1 - w), L2, a.lg2, tws2, inv, tR, ntR, act);
+        return w ^ (npR & 1);
+    };
+    auto fftC = [&](int w, bool inv, int rd, int nunits) -> int {
+        const bool act = cta + G * (gC + ngC * rd) < nunits;
+        fft_group(cbuf(gC, w), cbuf(gC, 1 - w), L1, a.lg1, tws1, inv, tC, ntC, act);
+        return w ^ (npC & 1);
+    };
+    constexpr int UF = 8;  // element-loop unroll: na * L / FT <= 8 always (na <= ng = 8 FT / L)
+    // fill buffer 0 of the active row slots with the odd extensions of rows i0, i1 of src (stride sstride)
+    auto fill_dst_rows = [&](const double* src, long long sstride, int rd) {
+        const int lim = nact(nuR, ngR, rd) * L2;
+        double2 v[UF];
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const int q = tid + t * nthr;
-                const int cc = q & (cbt - 1), j = q >> lgt;  // column fastest: adjacent loads
-                ilam[t] = 0.0;
-                if (q < cbt * a.L1) {
-                    double val = 0.0;
-                    if (cc < nc) {
-                        int k = -1;
-                        if (j >= 1 && j <= a.n1) {
-                            val = a.Rr[(long long)(j - 1) * a.n2 + k0 + cc];
-                            k = j;
-                        } else if (j >= a.n1 + 2) {
-                            val = -a.Rr[(long long)(a.L1 - j - 1) * a.n2 + k0 + cc];
-                            k = a.L1 - j;
-                        }
-                        if (k > 0) ilam[t] = a.lamT[(long long)(k - 1) * a.n2 + k0 + cc];
-                    }
-                    u[cc * a.L1 + j] = make_double2(val, 0.0);
+        for (int q = 0; q < UF; ++q) {
+            const int e = tid + q * FT;
+            v[q] = make_double2(0.0, 0.0);
+            if (e < lim) {
+                const int s = e / L2, j = e - s * L2, i0 = 2 * (cta + G * (s + ngR * rd));
+                const bool v1 = i0 + 1 < n1;
+                int jj = -1;
+                double sg = 1.0;
+                if (j >= 1 && j <= n2) jj = j - 1;
+                else if (j >= n2 + 2) {
+                    jj = L2 - j - 1;
+                    sg = -1.0;
+                }
+                if (jj >= 0) {
+                    v[q].x = sg * src[(long long)i0 * sstride + jj];
+                    if (v1) v[q].y = sg * src[(long long)(i0 + 1) * sstride + jj];
                 }
             }
-            __syncthreads();
-            double2* U = fft4_smem(u, v, cbt, a.L1, a.lg1, tws1, false, tid, nthr);
-            double2* W = U == u ? v : u;
+        }
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const int q = tid + t * nthr;
-                if (q < cbt * a.L1) {
-                    const int cc = q & (cbt - 1), j = q >> lgt;
-                    double val = 0.0;
-                    if (cc < nc) {
-                        int k = -1;
-                        double sgn = 1.0;
-                        if (j >= 1 && j <= a.n1) k = j;
-                        else if (j >= a.n1 + 2) {
-                            k = a.L1 - j;
-                            sgn = -1.0;
-                        }
-                        if (k > 0) val = sgn * (sc1 * U[cc * a.L1 + k].y) / (c * ilam[t] + dmean);
-                    }
-                    W[cc * a.L1 + j] = make_double2(val, 0.0);
-                }
+        for (int q = 0; q < UF; ++q) {
+            const int e = tid + q * FT;
+            if (e < lim) {
+                const int s = e / L2;
+                rbuf(s, 0)[pad8(e - s * L2)] = v[q];
             }
-            __syncthreads();
-            double2* V = W == u ? v : u;
-            const double2* R = fft4_smem(W, V, cbt, a.L1, a.lg1, tws1, false, tid, nthr);
-            for (int q = tid; q < nc * a.n1; q += nthr) {
-                const int cc = q % nc, k = q / nc;
-                a.Rr[(long long)k * a.n2 + k0 + cc] = sc1 * R[cc * a.L1 + k + 1].y;
-            }
-            __syncthreads();
         }
+        __syncthreads();
     };
-    // final row pass of the tau solve: zz = DST rows of Rr, returns the partial r.zz; init: p = zz
-    auto tau_out_phase = [&](bool init) -> double {
-        double part = 0.0;
-        if (nr == 0) return part;
-        for (int q = tid; q < nr * a.L2; q += nthr) {
-            const int i = q >> a.lg2, j = q & (a.L2 - 1);
-            const double* src = a.Rr + (long long)(r0 + i) * a.n2;
-            double val = 0.0;
-            if (j >= 1 && j <= a.n2) val = src[j - 1];
-            else if (j >= a.n2 + 2) val = -src[a.L2 - j - 1];
-            u[q] = make_double2(val, 0.0);
+    // DST-I along the rows of the active row pairs (buffer 0 filled) into the same rows of Rr.  Two real
+    // odd sequences share one complex FFT: FFT(oe(a) + i oe(b)) = i A - B with A, B real: A = Im, B = -Re.
+    auto dst_rows_out = [&](int rd) {
+        const int w = fftR(0, false, rd);
+        const int lim = nact(nuR, ngR, rd) * n2;
+        for (int e = tid; e < lim; e += FT) {
+            const int s = e / n2, k = e - s * n2, i0 = 2 * (cta + G * (s + ngR * rd));
+            const double2 c = rbuf(s, w)[pad8(k + 1)];
+            a.Rr[(long long)i0 * n2 + k] = sc2 * c.y;
+            if (i0 + 1 < n1) a.Rr[(long long)(i0 + 1) * n2 + k] = -sc2 * c.x;
         }
         __syncthreads();
-        const double2* U = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, false, tid, nthr);
-        for (int q = tid; q < nr * a.n2; q += nthr) {
-            const int i = q / a.n2, k = q - i * a.n2;
-            const long long o = (long long)(r0 + i) * a.ld2 + k;
-            const double zv = sc2 * U[i * a.L2 + k + 1].y;
-            a.zz[o] = zv;
-            if (init) a.p[o] = zv;
-            part += a.r[o] * zv;
+    };
+    // row FFTs of the real row pairs in buffer w0 (row i0 in .x, row i1 in .y, zero beyond n2): the half
+    // spectra k = 0 .. L2/2 into rows i0, i1 of dst (row stride H2)
+    auto f2_rows = [&](double2* dst, int w0, int rd) {
+        const int w = fftR(w0, false, rd);
+        const int lim = nact(nuR, ngR, rd) * H2;
+        for (int e = tid; e < lim; e += FT) {
+            const int s = e / H2, k = e - s * H2, i0 = 2 * (cta + G * (s + ngR * rd));
+            const double2 P = rbuf(s, w)[pad8(k)], Qc = rbuf(s, w)[pad8((L2 - k) & (L2 - 1))];
+            const double2 Q = make_double2(Qc.x, -Qc.y);
+            dst[(long long)i0 * H2 + k] = make_double2(0.5 * (P.x + Q.x), 0.5 * (P.y + Q.y));
+            if (i0 + 1 < n1) dst[(long long)(i0 + 1) * H2 + k] = make_double2(0.5 * (P.y - Q.y), -0.5 * (P.x - Q.x));
         }
         __syncthreads();
-        return part;
+    };
+    // element (row, column < n2) of the active row pairs: e in [0, na * 2 n2) -> padded index, or -1
+    auto row_elem = [&](int e, int rd, int& s, int& hi, int& j) -> long long {
+        s = e / (2 * n2);
+        const int rem = e - s * 2 * n2;
+        hi = rem >= n2;
+        j = rem - hi * n2;
+        const int ii = 2 * (cta + G * (s + ngR * rd)) + hi;
+        return ii < n1 ? (long long)ii * ld2 + j : -1;
     };
 
-    // the three passes of a CG step (B1 rows, B2 columns, B3 rows; grid barriers between them are the
-    // caller's).  B1 returns the partial p.delta.p, B2 the partial p.Bp (Parseval), B3 the partial ||r||^2.
-    auto passB1 = [&](int lv, int it, double beta) -> double {
-        const long long lo_lv = (long long)min(lv, a.S - 1) * Np;
-        // B1: p = zz + beta p (after the first step), row FFT of the embedded p; partial delta p.p
-        double pdp = 0.0;
-        if (nr > 0) {
-            for (int q = tid; q < nr * a.L2; q += nthr) {
-                const int i = q >> a.lg2, j = q & (a.L2 - 1);
-                double val = 0.0;
-                if (j < a.n2) {
-                    const long long o = (long long)(r0 + i) * a.ld2 + j;
-                    val = a.p[o];
-                    if (it > 0) {
-                        val = a.zz[o] + beta * val;
-                        a.p[o] = val;
+    // ---- the passes
+    // R0: level setup of the CTA's rows: history, b = rhs / D2 (r = zz = b), x0 -> p, x; then F2(x0) -> Zh
+    // (warm start) or S2(b) -> Rr (from zero).  Returns the partial ||b||^2.
+    auto passR0 = [&](int lv, bool direct, bool warm, int kx) -> double {
+        double bn = 0.0;
+        double* x = a.y + (long long)lv * Np;
+        const int B0 = lv & ~7, jt = lv & 7, nrec = lv - B0;
+        if (lv < a.S && jt == 0 && B0 > 0) {
+            // the blocked L1 history: at a block start B0 the old part sum_{m < B0} e_{L-m} y_m of the
+            // block's 8 targets L is formed reading each y_m once (element pairs, 8 levels in flight);
+            // per level the <= 7 recent terms are added
+            const int nt8 = min(8, a.S - B0);
+            const int tot = nact(nuR, ngR, 0) > 0 ? ngR * rdR * n2 : 0;  // element pairs (2 rows per unit)
+            for (int e = tid; e < tot; e += FT) {
+                const int s = e / n2, j = e - s * n2, u = cta + G * s;
+                if (u >= nuR) continue;
+                const int i0 = 2 * u;
+                const bool v1 = i0 + 1 < n1;
+                const long long o0 = (long long)i0 * ld2 + j, o1 = v1 ? o0 + ld2 : o0;
+                double acc0[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, acc1[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                for (int m0 = 0; m0 < B0; m0 += 8) {
+                    double y0[8], y1[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        y0[q] = a.y[(long long)(m0 + q) * Np + o0];
+                        y1[q] = a.y[(long long)(m0 + q) * Np + o1];
                     }
-                    if (lv < a.S) pdp += a.e0 * a.D1[lo_lv + o] * a.d2inv[lo_lv + o] * val * val;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+#pragma unroll
+                        for (int t8 = 0; t8 < 8; ++t8)
+                            if (t8 < nt8) {
+                                const double ev = a.e[B0 + t8 - m0 - q];
+                                acc0[t8] += ev * y0[q];
+                                acc1[t8] += ev * y1[q];
+                            }
                 }
-                u[q] = make_double2(val, 0.0);
+#pragma unroll
+                for (int t8 = 0; t8 < 8; ++t8) {
+                    a.hb[(long long)t8 * Np + o0] = acc0[t8];
+                    if (v1) a.hb[(long long)t8 * Np + o1] = acc1[t8];
+                }
             }
             __syncthreads();
-            const double2* U = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, false, tid, nthr);
-            double2* Xr = a.X + (long long)r0 * a.L2;
-            for (int q = tid; q < nr * a.L2; q += nthr) Xr[q] = U[q];
-            __syncthreads();
         }
-        return pdp;
+        for (int rd = 0; rd < rdR; ++rd) {
+            const int lim = nact(nuR, ngR, rd) * 2 * n2;
+            for (int base = 0; base < lim; base += 2 * FT) {
+                double bq[2], x0q[2], xvq[2];
+                long long oq[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int e = base + tid + q * FT;
+                    int s, hi, j;
+                    oq[q] = e < lim ? row_elem(e, rd, s, hi, j) : -1;
+                    bq[q] = x0q[q] = xvq[q] = 0.0;
+                    const long long o = oq[q];
+                    if (o < 0) continue;
+                    if (lv < a.S) {
+                        double hist = B0 > 0 ? a.hb[(long long)jt * Np + o] : 0.0;
+                        double yr[7];
+#pragma unroll
+                        for (int m = 0; m < 7; ++m) yr[m] = m < nrec ? a.y[(long long)(B0 + m) * Np + o] : 0.0;
+#pragma unroll
+                        for (int m = 0; m < 7; ++m)
+                            if (m < nrec) hist += a.e[lv - B0 - m] * yr[m];
+                        const long long oo = (long long)lv * Np + o;
+                        const double rhs = a.z_in[oo] - a.D1[oo] * hist;
+                        if (direct) xvq[q] = rhs / (a.e0 * a.D1[oo]);
+                        else bq[q] = rhs * a.d2inv[oo];
+                    } else {
+                        const double rhs = a.z_in[(long long)a.S * Np + o] - a.y[(long long)(a.S - 1) * Np + o];
+                        bq[q] = rhs * a.d2inv[(long long)(a.S - 1) * Np + o];
+                    }
+                    // initial guess of the time levels: the polynomial extrapolation through the previous kx
+                    // levels' solutions, x0 = sum_j (-1)^(j+1) C(kx, j) y_(lv-j)
+                    if (warm) {
+                        double yw[kWarmOrder];
+#pragma unroll
+                        for (int jj = 0; jj < kWarmOrder; ++jj)
+                            yw[jj] = jj < kx ? a.y[(long long)(lv - 1 - jj) * Np + o] : 0.0;
+#pragma unroll
+                        for (int jj = 0; jj < kWarmOrder; ++jj)
+                            if (jj < kx) x0q[q] += kWarmCoef[kx][jj + 1] * yw[jj];
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const long long o = oq[q];
+                    if (o < 0) continue;
+                    a.r[o] = bq[q];
+                    a.zz[o] = bq[q];
+                    a.p[o] = x0q[q];
+                    x[o] = xvq[q];
+                    bn += bq[q] * bq[q];
+                }
+            }
+            if (direct) continue;  // grid-uniform
+            __syncthreads();
+            if (warm) {
+                // (row i0, row i1) pairs of x0 (zero beyond n2) into buffer 0, then F2 -> Zh
+                const int limf = nact(nuR, ngR, rd) * L2;
+                for (int e = tid; e < limf; e += FT) {
+                    const int s = e / L2, j = e - s * L2, i0 = 2 * (cta + G * (s + ngR * rd));
+                    double2 v = make_double2(0.0, 0.0);
+                    if (j < n2) {
+                        v.x = a.p[(long long)i0 * ld2 + j];
+                        if (i0 + 1 < n1) v.y = a.p[(long long)(i0 + 1) * ld2 + j];
+                    }
+                    rbuf(s, 0)[pad8(j)] = v;
+                }
+                __syncthreads();
+                f2_rows(a.Zh, 0, rd);
+            } else {
+                fill_dst_rows(a.r, ld2, rd);
+                dst_rows_out(rd);
+            }
+        }
+        return bn;
     };
-    auto passB2 = [&]() -> double {
-        // B2: column FFT, times the circulant spectrum, inverse column FFT.  By Parseval the
-        // spectrum also gives p.Bp = sum lam |P^|^2 / (L1 L2), so p.Ap = c p.Bp + p.delta.p is
-        // known here and the inverse row pass can update x and r at once.
+    // B2: columns k of the half spectrum: X = Zh + beta Xp (F2 of the new direction; stored to Xp when
+    // keep), column FFT, x lambda_B, partial p.Bp (Parseval), inverse column FFT -> Yb
+    auto passB2 = [&](double beta, bool keep) -> double {
         double pbp = 0.0;
-        for (int g = cta; g < a.L2 / cbf; g += G) {
-            const int k0 = g * cbf;
-            // element q = (row j, column cc) with the column fastest: cbf adjacent values per row
-            double lamv[8];
+        for (int rd = 0; rd < rdB; ++rd) {
+            const int lim = nact(nuB, ngC, rd) * L1;
+            double2 v[UF];
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const int q = tid + t * nthr;
-                const int cc = q & (cbf - 1), j = q >> lgc;
-                if (q < cbf * a.L1) {
-                    u[cc * a.L1 + j] = a.X[(long long)j * a.L2 + k0 + cc];
-                    lamv[t] = a.lamB[(long long)j * a.L2 + k0 + cc];
+            for (int q = 0; q < UF; ++q) {
+                const int e = tid + q * FT;
+                v[q] = make_double2(0.0, 0.0);
+                if (e < lim) {
+                    const int s = e / L1, j = e - s * L1, k = cta + G * (s + ngC * rd);
+                    if (j < n1) {
+                        const long long o = (long long)j * H2 + k;
+                        v[q] = a.Zh[o];
+                        if (beta != 0.0) {
+                            const double2 xp = a.Xp[o];
+                            v[q].x += beta * xp.x;
+                            v[q].y += beta * xp.y;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < UF; ++q) {
+                const int e = tid + q * FT;
+                if (e < lim) {
+                    const int s = e / L1, j = e - s * L1, k = cta + G * (s + ngC * rd);
+                    if (keep && j < n1) a.Xp[(long long)j * H2 + k] = v[q];
+                    cbuf(s, 0)[pad8(j)] = v[q];
                 }
             }
             __syncthreads();
-            double2* U = fft4_smem(u, v, cbf, a.L1, a.lg1, tws1, false, tid, nthr);
+            const int w = fftC(0, false, rd, nuB);
+            double lam[UF];
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const int q = tid + t * nthr;
-                const int cc = q & (cbf - 1), j = q >> lgc;
-                if (q < cbf * a.L1) {
-                    const double2 w = U[cc * a.L1 + j];
-                    pbp += lamv[t] * (w.x * w.x + w.y * w.y);
-                    U[cc * a.L1 + j] = make_double2(w.x * lamv[t], w.y * lamv[t]);
+            for (int q = 0; q < UF; ++q) {
+                const int e = tid + q * FT;
+                lam[q] = 0.0;
+                if (e < lim) {
+                    const int s = e / L1, j = e - s * L1, k = cta + G * (s + ngC * rd);
+                    lam[q] = a.lamB[(long long)j * L2 + k];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < UF; ++q) {
+                const int e = tid + q * FT;
+                if (e < lim) {
+                    const int s = e / L1, j = e - s * L1, k = cta + G * (s + ngC * rd);
+                    const double wk = (k == 0 || k == L2 / 2) ? 1.0 : 2.0;
+                    double2* cell = cbuf(s, w) + pad8(j);
+                    const double2 c = *cell;
+                    pbp += wk * lam[q] * (c.x * c.x + c.y * c.y);
+                    *cell = make_double2(c.x * lam[q], c.y * lam[q]);
                 }
             }
             __syncthreads();
-            double2* W = U == u ? v : u;
-            const double2* Y = fft4_smem(U, W, cbf, a.L1, a.lg1, tws1, true, tid, nthr);
-            for (int q = tid; q < cbf * a.n1; q += nthr) {
-                const int cc = q & (cbf - 1), j = q >> lgc;
-                a.X[(long long)j * a.L2 + k0 + cc] = Y[cc * a.L1 + j];
+            const int w2 = fftC(w, true, rd, nuB);
+            const int limo = nact(nuB, ngC, rd) * n1;
+            for (int e = tid; e < limo; e += FT) {
+                const int s = e / n1, j = e - s * n1, k = cta + G * (s + ngC * rd);
+                a.Yb[(long long)j * H2 + k] = cbuf(s, w2)[pad8(j)];
             }
             __syncthreads();
         }
         return pbp;
     };
-    auto passB3 = [&](int lv, double c, double alpha, double* x) -> double {
-        const long long lo_lv = (long long)min(lv, a.S - 1) * Np;
-        double part;
-        // B3: inverse row FFT, Ap = c B p + delta o p; x += alpha p, r -= alpha Ap, ||r||^2, and
-        // the DST rows of the new r (first pass of the next tau solve)
-        part = 0.0;
-        if (nr > 0) {
-            const double2* Xr = a.X + (long long)r0 * a.L2;
-            for (int q = tid; q < nr * a.L2; q += nthr) u[q] = Xr[q];
-            __syncthreads();
-            const double2* Y = fft4_smem(u, v, nr, a.L2, a.lg2, tws2, true, tid, nthr);
-            for (int q = tid; q < nr * a.n2; q += nthr) {
-                const int i = q / a.n2, j = q - i * a.n2;
-                const long long o = (long long)(r0 + i) * a.ld2 + j;
-                const double pv = a.p[o];
-                const double delta = lv < a.S ? a.e0 * a.D1[lo_lv + o] * a.d2inv[lo_lv + o] : 0.0;
-                const double ap = c * (Y[i * a.L2 + j].x * a.inv_LL) + delta * pv;
-                x[o] += alpha * pv;
-                const double rv = a.r[o] - alpha * ap;
-                a.r[o] = rv;
-                part += rv * rv;
+    // B3: inverse row FFT of the Yb row pairs -> B p; p = zz + beta p (cg) or p as is (pre-step); Ap = c Bp +
+    // delta p; x += alpha p; r -= alpha Ap; partial ||r||^2; S2(r) -> Rr
+    auto passB3 = [&](int lv, double c, double alpha, double beta, bool cg) -> double {
+        const long long lo = (long long)min(lv, a.S - 1) * Np;
+        double* x = a.y + (long long)lv * Np;
+        double part = 0.0;
+        for (int rd = 0; rd < rdR; ++rd) {
+            const int lim = nact(nuR, ngR, rd) * L2;
+            double2 v[UF];
+#pragma unroll
+            for (int q = 0; q < UF; ++q) {
+                // packed spectrum D = Y0 + i Y1 of the row pair from the two Hermitian half spectra
+                const int e = tid + q * FT;
+                v[q] = make_double2(0.0, 0.0);
+                if (e < lim) {
+                    const int s = e / L2, k = e - s * L2, i0 = 2 * (cta + G * (s + ngR * rd));
+                    const int kk = k <= L2 / 2 ? k : L2 - k;
+                    double2 y0 = a.Yb[(long long)i0 * H2 + kk];
+                    double2 y1 = i0 + 1 < n1 ? a.Yb[(long long)(i0 + 1) * H2 + kk] : make_double2(0.0, 0.0);
+                    if (kk == 0 || kk == L2 / 2) {
+                        y0.y = 0.0;
+                        y1.y = 0.0;
+                    }
+                    if (k > L2 / 2) {
+                        y0.y = -y0.y;
+                        y1.y = -y1.y;
+                    }
+                    v[q] = make_double2(y0.x - y1.y, y0.y + y1.x);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < UF; ++q) {
+                const int e = tid + q * FT;
+                if (e < lim) {
+                    const int s = e / L2;
+                    rbuf(s, 0)[pad8(e - s * L2)] = v[q];
+                }
             }
             __syncthreads();
-            dst_rows(a.r, a.ld2);
+            const int w = fftR(0, true, rd);
+            const int lime = nact(nuR, ngR, rd) * 2 * n2;
+            for (int base = 0; base < lime; base += 2 * FT) {
+                double pq[2], zq[2], dq[2], xq[2], rq[2], bpq[2];
+                long long oq[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int e = base + tid + q * FT;
+                    int s, hi, j;
+                    oq[q] = e < lime ? row_elem(e, rd, s, hi, j) : -1;
+                    const long long o = oq[q];
+                    pq[q] = zq[q] = dq[q] = xq[q] = rq[q] = bpq[q] = 0.0;
+                    if (o < 0) continue;
+                    const double2 yv = rbuf(s, w)[pad8(j)];
+                    bpq[q] = (hi ? yv.y : yv.x) * a.inv_LL;
+                    pq[q] = a.p[o];
+                    if (cg) zq[q] = a.zz[o];
+                    if (lv < a.S) dq[q] = a.e0 * a.D1[lo + o] * a.d2inv[lo + o];
+                    xq[q] = x[o];
+                    rq[q] = a.r[o];
+                }
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const long long o = oq[q];
+                    if (o < 0) continue;
+                    double pv = pq[q];
+                    if (cg) {
+                        pv = beta != 0.0 ? zq[q] + beta * pv : zq[q];
+                        a.p[o] = pv;
+                    }
+                    const double ap = c * bpq[q] + dq[q] * pv;
+                    x[o] = xq[q] + alpha * pv;
+                    const double rv = rq[q] - alpha * ap;
+                    a.r[o] = rv;
+                    part += rv * rv;
+                }
+            }
+            __syncthreads();
+            fill_dst_rows(a.r, ld2, rd);
+            dst_rows_out(rd);
         }
         return part;
     };
+    // fallback of the pre-step (a guess worse than zero): x = 0, r = b (kept in zz), S2(r) -> Rr
+    auto passFallback = [&](int lv) {
+        double* x = a.y + (long long)lv * Np;
+        for (int rd = 0; rd < rdR; ++rd) {
+            const int lime = nact(nuR, ngR, rd) * 2 * n2;
+            for (int e = tid; e < lime; e += FT) {
+                int s, hi, j;
+                const long long o = row_elem(e, rd, s, hi, j);
+                if (o < 0) continue;
+                a.r[o] = a.zz[o];
+                x[o] = 0.0;
+            }
+            __syncthreads();
+            fill_dst_rows(a.r, ld2, rd);
+            dst_rows_out(rd);
+        }
+    };
+    // T2: tau column pass on the column pairs (k0, k0 + 1) of Rr: S1, divide by c g(theta) + mean(delta), S1
+    auto passT2 = [&](int lv) {
+        const double c = level_c(a, lv), dmean = level_dmean(a, lv);
+        for (int rd = 0; rd < rdT; ++rd) {
+            const int lim = nact(nuT, ngC, rd) * L1;
+            double2 v[UF];
+#pragma unroll
+            for (int q = 0; q < UF; ++q) {
+                const int e = tid + q * FT;
+                v[q] = make_double2(0.0, 0.0);
+                if (e < lim) {
+                    const int s = e / L1, j = e - s * L1, k0 = 2 * (cta + G * (s + ngC * rd));
+                    int jj = -1;
+                    double sg = 1.0;
+                    if (j >= 1 && j <= n1) jj = j - 1;
+                    else if (j >= n1 + 2) {
+                        jj = L1 - j - 1;
+                        sg = -1.0;
+                    }
+                    if (jj >= 0) {
+                        v[q].x = sg * a.Rr[(long long)jj * n2 + k0];
+                        if (k0 + 1 < n2) v[q].y = sg * a.Rr[(long long)jj * n2 + k0 + 1];
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < UF; ++q) {
+                const int e = tid + q * FT;
+                if (e < lim) {
+                    const int s = e / L1;
+                    cbuf(s, 0)[pad8(e - s * L1)] = v[q];
+                }
+            }
+            __syncthreads();
+            const int w = fftC(0, false, rd, nuT);
+            double2 il[UF];
+#pragma unroll
+            for (int q = 0; q < UF; ++q) {
+                const int e = tid + q * FT;
+                il[q] = make_double2(0.0, 0.0);
+                if (e < lim) {
+                    const int s = e / L1, j = e - s * L1, k0 = 2 * (cta + G * (s + ngC * rd));
+                    const int kk = (j >= 1 && j <= n1) ? j : (j >= n1 + 2 ? L1 - j : -1);
+                    if (kk > 0) {
+                        il[q].x = a.lamT[(long long)(kk - 1) * n2 + k0];
+                        if (k0 + 1 < n2) il[q].y = a.lamT[(long long)(kk - 1) * n2 + k0 + 1];
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < UF; ++q) {
+                const int e = tid + q * FT;
+                if (e < lim) {
+                    const int s = e / L1, j = e - s * L1, k0 = 2 * (cta + G * (s + ngC * rd));
+                    double x0 = 0.0, x1 = 0.0;
+                    int kk = -1;
+                    double sg = 1.0;
+                    if (j >= 1 && j <= n1) kk = j;
+                    else if (j >= n1 + 2) {
+                        kk = L1 - j;
+                        sg = -1.0;
+                    }
+                    if (kk > 0) {
+                        const double2 cv = cbuf(s, w)[pad8(kk)];
+                        x0 = sg * (sc1 * cv.y) / (c * il[q].x + dmean);
+                        if (k0 + 1 < n2) x1 = sg * (-sc1 * cv.x) / (c * il[q].y + dmean);
+                    }
+                    cbuf(s, 1 - w)[pad8(j)] = make_double2(x0, x1);
+                }
+            }
+            __syncthreads();
+            const int w2 = fftC(1 - w, false, rd, nuT);
+            const int limo = nact(nuT, ngC, rd) * n1;
+            for (int e = tid; e < limo; e += FT) {
+                const int s = e / n1, j = e - s * n1, k0 = 2 * (cta + G * (s + ngC * rd));
+                const double2 cv = cbuf(s, w2)[pad8(j + 1)];
+                a.Rr[(long long)j * n2 + k0] = sc1 * cv.y;
+                if (k0 + 1 < n2) a.Rr[(long long)j * n2 + k0 + 1] = -sc1 * cv.x;
+            }
+            __syncthreads();
+        }
+    };
+    // T3: zz = S2(Rr rows); partials r.z, z.delta.z, z.delta.p (p = the previous direction); F2(z) -> Zh
+    auto passT3 = [&](int lv, double* part3) {
+        const long long lo = (long long)min(lv, a.S - 1) * Np;
+        part3[0] = part3[1] = part3[2] = 0.0;
+        for (int rd = 0; rd < rdR; ++rd) {
+            fill_dst_rows(a.Rr, n2, rd);
+            const int w = fftR(0, false, rd);
+            // z values into buffer 1 - w (pairs, zero beyond n2), zz stores and the dot-product partials
+            const int limz = nact(nuR, ngR, rd) * L2;
+            for (int e = tid; e < limz; e += FT) {
+                const int s = e / L2, k = e - s * L2, i0 = 2 * (cta + G * (s + ngR * rd));
+                double2 zv = make_double2(0.0, 0.0);
+                if (k < n2) {
+                    const double2 cv = rbuf(s, w)[pad8(k + 1)];
+                    zv = make_double2(sc2 * cv.y, i0 + 1 < n1 ? -sc2 * cv.x : 0.0);
+                }
+                rbuf(s, 1 - w)[pad8(k)] = zv;
+            }
+            __syncthreads();
+            const int lime = nact(nuR, ngR, rd) * 2 * n2;
+            for (int base = 0; base < lime; base += 2 * FT) {
+                double zq[2], rq[2], pq[2], dq[2];
+                long long oq[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int e = base + tid + q * FT;
+                    int s, hi, j;
+                    oq[q] = e < lime ? row_elem(e, rd, s, hi, j) : -1;
+                    const long long o = oq[q];
+                    zq[q] = rq[q] = pq[q] = dq[q] = 0.0;
+                    if (o < 0) continue;
+                    const double2 zv = rbuf(s, 1 - w)[pad8(j)];
+                    zq[q] = hi ? zv.y : zv.x;
+                    rq[q] = a.r[o];
+                    pq[q] = a.p[o];
+                    if (lv < a.S) dq[q] = a.e0 * a.D1[lo + o] * a.d2inv[lo + o];
+                }
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const long long o = oq[q];
+                    if (o < 0) continue;
+                    a.zz[o] = zq[q];
+                    part3[0] += rq[q] * zq[q];
+                    part3[1] += dq[q] * zq[q] * zq[q];
+                    part3[2] += dq[q] * zq[q] * pq[q];
+                }
+            }
+            f2_rows(a.Zh, 1 - w, rd);
+        }
+    };
 
-    // a guess worse than zero (||b - M x0|| > ||b||: the input is not smooth in time) switches the
-    // warm start off for the rest of the apply (the decision is grid-uniform: it uses reduced values)
+    // a guess worse than zero (||b - M x0|| > ||b||: the input is not smooth in time) switches the warm
+    // start off for the rest of the apply (the decision is grid-uniform: it uses reduced values)
     bool warm_ok = true;
     for (int lv = 0; lv < a.levels; ++lv) {
-        // ---- level setup: rhs (forward substitution, krylov.cpp:55-68), b = rhs / D2, x = 0
         const bool direct = lv < a.S && a.direct[lv];
-        // warm start: time levels after the first whose predecessors were solved by CG
-        const int kx = min(lv, kWarmOrder);  // previous levels in the extrapolation
+        const int kx = min(lv, kWarmOrder);
         bool warm = a.warm && warm_ok && lv >= 1 && lv < a.S && !direct;
         for (int j = 1; j <= kx; ++j) warm = warm && !a.direct[lv - j];
-        double* x = a.y + (long long)lv * Np;
-        double part = 0.0;
-        for (long long i = (long long)cta * nthr + tid; i < Np; i += (long long)G * nthr) {
-            const int i2 = (int)(i % a.ld2);
-            double b = 0.0, xv = 0.0;
-            if (i2 < a.n2) {
-                if (lv < a.S) {
-                    // L1 history sum_{m < lv} e_{lv-m} y_m, blocked over 8 levels: at a block start
-                    // B0 the old part sum_{m < B0} e_{L-m} y_m of the block's 8 targets L is formed
-                    // reading each y_m once (8x less traffic than per level; this thread owns element
-                    // i at every level, so hb needs no synchronisation); per level the <= 7 recent
-                    // terms m in [B0, lv) are added
-                    const int B0 = lv & ~7, jt = lv & 7;
-                    if (jt == 0 && B0 > 0) {
-                        double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-                        const int nt = min(8, a.S - B0);
-                        for (int m = 0; m < B0; ++m) {
-                            const double ym = a.y[(long long)m * Np + i];
-#pragma unroll
-                            for (int t = 0; t < 8; ++t)
-                                if (t < nt) acc[t] += a.e[B0 + t - m] * ym;
-                        }
-#pragma unroll
-                        for (int t = 0; t < 8; ++t) a.hb[(long long)t * Np + i] = acc[t];
-                    }
-                    double hist = B0 > 0 ? a.hb[(long long)jt * Np + i] : 0.0;
-                    for (int m = B0; m < lv; ++m) hist += a.e[lv - m] * a.y[(long long)m * Np + i];
-                    const long long o = (long long)lv * Np + i;
-                    const double rhs = a.z_in[o] - a.D1[o] * hist;
-                    if (direct) xv = rhs / (a.e0 * a.D1[o]);
-                    else b = rhs * a.d2inv[o];
-                } else {
-                    const double rhs = a.z_in[(long long)a.S * Np + i] - a.y[(long long)(a.S - 1) * Np + i];
-                    b = rhs * a.d2inv[(long long)(a.S - 1) * Np + i];
-                }
-            }
-            // initial guess of the time levels (not the f-block): the polynomial extrapolation through
-            // the previous kx levels' solutions, x0 = sum_j (-1)^(j+1) C(kx, j) y_(lv-j), passed
-            // through p to the pre-step
-            double x0 = 0.0;
-            if (warm && i2 < a.n2)
-                for (int j = 1; j <= kx; ++j) x0 += kWarmCoef[kx][j] * a.y[(long long)(lv - j) * Np + i];
-            a.r[i] = b;
-            a.zz[i] = b;
-            a.p[i] = x0;
-            x[i] = xv;
-            part += b * b;
-        }
-        stamp(7);
-        const double bn2 = greduce(part);
+        double red[kRedMax];
+        red[0] = passR0(lv, direct, warm, kx);
+        greduce(red, 1);
+        const double bn2 = red[0];
         stamp(0);
-        const bool conv = bn2 == 0.0 || direct;
-        if (conv) continue;
+        if (bn2 == 0.0 || direct) continue;
         const double c = level_c(a, lv);
-        const long long lo_lv = (long long)min(lv, a.S - 1) * Np;  // D1, 1/D2 rows of the level
-        bool from_zero = true;
+        const double stop2 = a.tol * a.tol * bn2;
         if (warm) {
             // pre-step with alpha = 1 along p = x0: x = x0, r = b - M x0 (and the DST rows of r)
-            passB1(lv, 0, 0.0);
+            passB2(0.0, false);
             gsync();
-            passB2();
-            gsync();
-            const double rn0 = greduce(passB3(lv, c, 1.0, x));
+            red[0] = passB3(lv, c, 1.0, 0.0, false);
+            greduce(red, 1);
+            const double rn0 = red[0];
+            stamp(1);
             if (sqrt(rn0) <= a.tol * sqrt(bn2)) continue;  // the guess already solves the level
-            from_zero = rn0 > bn2;  // a guess worse than 0: restart from x = 0, r = b
-            if (from_zero) {
+            if (rn0 > bn2) {                                // a guess worse than 0: restart from x = 0, r = b
                 warm_ok = false;
-                for (long long i = (long long)cta * nthr + tid; i < Np; i += (long long)G * nthr) {
-                    a.r[i] = a.zz[i];
-                    x[i] = 0.0;
-                }
+                passFallback(lv);
                 gsync();
+                stamp(1);
             }
         }
+        (void)stop2;
         // ---- initial tau solve: zz = tau^{-1} r, p = zz, rz = r.zz
-        if (from_zero) dst_rows(a.r, a.ld2);
+        passT2(lv);
         gsync();
-        tau_cols_phase(lv);
-        gsync();
-        double rz = greduce(tau_out_phase(true));
-        stamp(1);
-        double beta = 0.0;
+        stamp(2);
+        passT3(lv, red);
+        greduce(red, 3);
+        stamp(3);
+        double rz = red[0], pdp = red[1], beta = 0.0;
         int it = 0;
+        bool conv = false;
         while (true) {
-            const double pdp = passB1(lv, it, beta);
-            gsync();
-            stamp(2);
-            const double pbp = passB2();
-            const double alpha = rz / greduce(c * a.inv_LL * pbp + pdp);
-            stamp(3);
-            part = passB3(lv, c, alpha, x);
+            red[0] = passB2(beta, true);
+            greduce(red, 1);
             stamp(4);
-            const double rn2 = greduce(part);
+            const double alpha = rz / (c * a.inv_LL * red[0] + pdp);
+            red[0] = passB3(lv, c, alpha, beta, true);
+            greduce(red, 1);
             stamp(5);
             ++it;
-            if (sqrt(rn2) <= a.tol * sqrt(bn2) || it >= a.maxit) break;
-            tau_cols_phase(lv);
+            conv = sqrt(red[0]) <= a.tol * sqrt(bn2);
+            if (conv || it >= a.maxit) break;
+            passT2(lv);
             gsync();
-            stamp(6);
-            const double rz_new = greduce(tau_out_phase(false));
-            stamp(7);
-            beta = rz_new / rz;
-            rz = rz_new;
+            stamp(2);
+            passT3(lv, red);
+            greduce(red, 3);
+            stamp(3);
+            beta = red[0] / rz;
+            rz = red[0];
+            pdp = red[1] + 2.0 * beta * red[2] + beta * beta * pdp;
+        }
+        if (ctl.stats && cta == 0 && tid == 0) {
+            ctl.stats[0] += (unsigned long long)it;
+            if (!conv) ctl.stats[1] += 1;
+            if ((unsigned long long)it > ctl.stats[2]) ctl.stats[2] = it;
         }
     }
+    if (ctl.stats && cta == 0 && tid == 0) ctl.stats[3] += 1;
 }
 
 int ilog2(int v) {
@@ -649,11 +967,7 @@ int ilog2(int v) {
 
 // column kernels stage 2 x CB x L1 complex values (64 KiB at L1 = 512): above the 48 KiB default
 void allow_column_smem() {
-    static bool done = false;
-    if (done) return;
-    const int bytes = 2 * CB * 1024 * (int)sizeof(double2);
-    FI_CUDA(cudaFuncSetAttribute(fft_cols_to_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    done = true;
+    ensure_smem_attr((const void*)fft_cols_to_spec, 2 * CB * 1024 * sizeof(double2));
 }
 
 ItArgs make_args(fi_precond* P) {
@@ -690,6 +1004,10 @@ ItArgs make_args(fi_precond* P) {
     a.p = P->it_vec.p + 2 * Np;
     a.Ap = P->it_vec.p + 3 * Np;
     a.X = P->it_X.p;
+    const long long nh = (long long)L.n1 * (a.L2 / 2 + 1);
+    a.Zh = P->it_F.p;
+    a.Xp = P->it_F.p + nh;
+    a.Yb = P->it_F.p + 2 * nh;
     a.hb = P->it_hb.p;
     static const int warm = std::getenv("FI_TAU_WARM") ? std::atoi(std::getenv("FI_TAU_WARM")) : 1;
     a.warm = warm;
@@ -787,6 +1105,9 @@ void precond_build_iterative(fi_precond* P, double tol, int maxit) {
     P->it_lamB.alloc((size_t)L1 * L2);
     P->it_vec.alloc((size_t)4 * Np);  // r, z, p, Ap
     P->it_hb.alloc((size_t)8 * Np);   // blocked L1 history
+    P->it_F.alloc((size_t)3 * L.n1 * (L2 / 2 + 1));  // Zh, Xp, Yb
+    P->it_stats.alloc(4);
+    FI_CUDA(cudaMemset(P->it_stats.p, 0, P->it_stats.bytes()));
     FI_CUDA(cudaMemset(P->it_vec.p, 0, P->it_vec.bytes()));
     // circulant spectrum of B with the same FFT kernels
     allow_column_smem();
@@ -801,64 +1122,59 @@ void precond_build_iterative(fi_precond* P, double tol, int maxit) {
 }
 
 void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip) {
-    {
-        // one cooperative kernel for the whole substitution (tau_pcg_fused)
-        ItArgs a = make_args(P);
-        a.z_in = z;
-        a.y = y;
-        a.levels = levels;
-        a.skip = skip;
-        // grid: one row (pair of columns) per CTA when the GPU holds that many CTAs (two per SM),
-        // otherwise each CTA transforms rpc rows / cbf columns at once; every pass is one round
-        if (P->it_fgrid == 0) {
-            const size_t smem_max = (2 * (size_t)std::max(4 * a.L2, 4 * a.L1) + a.L1 / 2 + a.L2 / 2) * sizeof(double2);
-            FI_CUDA(cudaFuncSetAttribute(tau_pcg_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)std::min<size_t>(smem_max, 227 * 1024)));
-            const size_t smem1 = (2 * (size_t)std::max(a.L2, 2 * a.L1) + a.L1 / 2 + a.L2 / 2) * sizeof(double2);
-            int per_sm = 0;
-            FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tau_pcg_fused, 256, smem1));
-            if (per_sm < 1) throw Error(FI_E_CUDA, "tau_pcg_fused cannot be resident");
-            P->it_fgrid = std::min(ctx->sm_count * std::min(per_sm, 2), std::max(a.n1, (a.L2 + 1) / 2));
-            P->it_fparts.alloc((size_t)2 * P->it_fgrid);
-            P->it_fbar.alloc(1);
-        }
-        const int G = P->it_fgrid;
-        const int rpc = (a.n1 + G - 1) / G;
-        int cbf = 1;
-        while (cbf * G < a.L2 && cbf * 2 * a.L1 <= 8 * 256) cbf *= 2;
-        const size_t hs = (size_t)std::max(rpc * a.L2, cbf * a.L1);
-        const size_t smem = (2 * hs + a.L1 / 2 + a.L2 / 2) * sizeof(double2);
-        if (smem > 227 * 1024) throw Error(FI_E_RESOURCE, "tau_pcg_fused: shared memory");
-        static const bool tracing = std::getenv("FI_ITER_TRACE") != nullptr;
-        DevBuf<unsigned long long> trace;
-        if (tracing) {
-            trace.alloc(10);
-            FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
-        }
-        int lgc = 0;
-        while ((1 << lgc) < cbf) ++lgc;
-        int cbt = 1, lgt = 0;  // tau column pass: n2 columns over the grid
-        while (cbt * G < a.n2 && cbt < cbf) {
-            cbt *= 2;
-            ++lgt;
-        }
-        FusedCtl ctl{P->it_fbar.p, P->it_fparts.p, tracing ? trace.p : nullptr, rpc, cbf, lgc, cbt, lgt};
-        FI_CUDA(cudaMemsetAsync(P->it_fbar.p, 0, sizeof(unsigned), ctx->stream));
-        void* args[] = {&a, &ctl};
-        FI_CUDA(cudaLaunchCooperativeKernel((const void*)tau_pcg_fused, dim3(P->it_fgrid), dim3(256), args, smem,
-                                            ctx->stream));
-        FI_LAUNCHED(ctx);
-        if (tracing) {
-            unsigned long long h[10];
-            FI_CUDA(cudaMemcpyAsync(h, trace.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-            FI_CUDA(cudaStreamSynchronize(ctx->stream));
-            std::fprintf(stderr,
-                         "[tau_pcg_fused] ms: setup %.3f | tau0 %.3f | B1 %.3f | B2 %.3f | B3+red %.3f | U+T1+red %.3f | "
-                         "T2 %.3f | T3+red %.3f | barrier wait (CTA 0) %.3f over %llu barriers\n",
-                         h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6, h[4] * 1e-6, h[5] * 1e-6, h[6] * 1e-6,
-                         h[7] * 1e-6, h[8] * 1e-6, h[9]);
-        }
+    // one cooperative kernel for the whole substitution (tau_pcg_fused), one CTA per SM
+    ItArgs a = make_args(P);
+    a.z_in = z;
+    a.y = y;
+    a.levels = levels;
+    a.skip = skip;
+    const int H2 = a.L2 / 2 + 1;
+    const int plr = a.L2 + a.L2 / 8 + 1, plc = a.L1 + a.L1 / 8 + 1;
+    const int ngr = FT / std::max(a.L2 / 8, 1), ngc = FT / std::max(a.L1 / 8, 1);
+    const size_t smem = ((size_t)a.L1 / 2 + a.L2 / 2 + std::max((size_t)ngr * 2 * plr, (size_t)ngc * 2 * plc)) *
+                        sizeof(double2);
+    if (smem > 227 * 1024) throw Error(FI_E_RESOURCE, "tau_pcg_fused: shared memory");
+    if (P->it_fgrid == 0) {
+        ensure_smem_attr((const void*)tau_pcg_fused, smem);
+        int per_sm = 0;
+        FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tau_pcg_fused, FT, smem));
+        if (per_sm < 1) throw Error(FI_E_CUDA, "tau_pcg_fused cannot be resident");
+        // one CTA per SM, or fewer when the passes have fewer units (small grids)
+        const int units = std::max(std::max((a.n1 + 1) / 2, (a.n2 + 1) / 2), H2);
+        P->it_fgrid = std::min(ctx->sm_count, units);
+        P->it_fparts.alloc((size_t)2 * kRedMax * P->it_fgrid);
+        P->it_fbar.alloc(1);
+    } else {
+        ensure_smem_attr((const void*)tau_pcg_fused, smem);
     }
+    static const bool tracing = std::getenv("FI_ITER_TRACE") != nullptr;
+    DevBuf<unsigned long long> trace;
+    if (tracing) {
+        trace.alloc(10);
+        FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
+    }
+    FusedCtl ctl{P->it_fbar.p, P->it_fparts.p, tracing ? trace.p : nullptr, P->it_stats.p};
+    FI_CUDA(cudaMemsetAsync(P->it_fbar.p, 0, sizeof(unsigned), ctx->stream));
+    void* args[] = {&a, &ctl};
+    FI_CUDA(cudaLaunchCooperativeKernel((const void*)tau_pcg_fused, dim3(P->it_fgrid), dim3(FT), args, smem,
+                                        ctx->stream));
+    FI_LAUNCHED(ctx);
+    if (tracing) {
+        unsigned long long h[10];
+        FI_CUDA(cudaMemcpyAsync(h, trace.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        FI_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::fprintf(stderr,
+                     "[tau_pcg_fused] ms: setup %.3f | pre-step %.3f | T2 %.3f | T3+red %.3f | B2+red %.3f | "
+                     "B3+red %.3f | barrier wait (CTA 0) %.3f over %llu barriers\n",
+                     h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6, h[4] * 1e-6, h[5] * 1e-6, h[8] * 1e-6, h[9]);
+    }
+}
+
+void precond_iterative_stats(fi_precond* P, unsigned long long out[4], bool reset) {
+    fi_ctx* ctx = P->sys->ctx;
+    FI_CUDA(cudaMemcpyAsync(out, P->it_stats.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    if (reset) FI_CUDA(cudaMemsetAsync(P->it_stats.p, 0, P->it_stats.bytes(), ctx->stream));
+    FI_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 }  // namespace fib

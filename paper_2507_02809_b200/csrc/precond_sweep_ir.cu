@@ -760,15 +760,13 @@ bool sweep_ir_available(const fi_precond* P) {
 }
 
 void launch_sweep_ir(fi_ctx* ctx, fi_precond* P, const double* z, double* y, int levels, const int* skip) {
-    static bool configured = false;
     const int smem = sweep_ir_smem_bytes();
     const void* kern = (const void*)sweep_ir_kernel;
-    if (!configured) {
-        FI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    ensure_smem_attr(kern, (size_t)smem);
+    {
         int per_sm = 0;
         FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
         if (per_sm < 1) throw Error(FI_E_CUDA, "sweep_ir_kernel cannot be resident");
-        configured = true;
     }
     const fi_system* sys = P->sys;
     const Layout& L = sys->L;

@@ -270,11 +270,7 @@ __global__ void __launch_bounds__(256) fcol_kernel(OperatorView op, const double
 
 void toeplitz_apply(fi_ctx* ctx, const OperatorView& op, const double* U, double* Z, const int* skip,
                     const double* minus_from, bool precond_matrix) {
-    static bool configured = false;
-    if (!configured) {
-        FI_CUDA(cudaFuncSetAttribute(toeplitz_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        configured = true;
-    }
+    ensure_smem_attr((const void*)toeplitz_apply_kernel, SMEM_BYTES);
     // the f column (fcol_kernel) on the side stream, overlapping the time-level GEMM
     FI_CUDA(cudaEventRecord(ctx->fork, ctx->stream));
     FI_CUDA(cudaStreamWaitEvent(ctx->side, ctx->fork, 0));

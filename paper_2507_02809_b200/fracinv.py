@@ -26,7 +26,8 @@ from typing import Callable, List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (FI_E_CONFIG, FI_E_CUDA, FI_E_DIM, FI_E_DOMAIN, FI_E_RESOURCE, FI_E_SINGULAR, LINOP, GmresOpts,
+from ._lib import (FI_E_CONFIG, FI_E_CUDA, FI_E_DIM, FI_E_DOMAIN, FI_E_NOCONV, FI_E_RESOURCE, FI_E_SINGULAR, LINOP,
+                   GmresOpts,
                    GmresReport, SystemDesc, c_double_p, last_error, lib)
 
 # --------------------------------------------------------------------------- errors (errors.hpp:9-43)
@@ -57,6 +58,10 @@ class CudaError(RuntimeError):
     pass
 
 
+class NoConvergenceError(RuntimeError):
+    """A tau-PCG block solve stopped at maxit above its tolerance (FI_E_NOCONV, EXTENSION)."""
+
+
 _SHUTDOWN = [False]
 
 
@@ -80,6 +85,8 @@ def _check(rc: int):
         raise ValueError(msg)  # std::domain_error
     if rc == FI_E_CONFIG:
         raise ConfigError(msg)
+    if rc == FI_E_NOCONV:
+        raise NoConvergenceError(msg)
     raise CudaError(msg or f"fracinv_b200 error {rc}")
 
 
@@ -111,6 +118,16 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return int(lib.fi_ctx_kernel_launches(self.handle))
+
+    def after_torch(self):
+        """Order this context's stream after the work torch has queued on its current stream (inputs a
+        pending torch kernel still writes, outputs whose memory the caching allocator recycles)."""
+        import torch
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        if getattr(self, "_ext", None) is None:
+            self._ext = torch.cuda.ExternalStream(self.stream, device=torch.device("cuda", self.device))
+        self._ext.wait_event(ev)
 
     def __del__(self, _shutdown=_SHUTDOWN, _lib=lib):
         if getattr(self, "handle", None) and not _shutdown[0]:
@@ -421,6 +438,7 @@ class SystemOperator:
             import torch
             yp = _device_ptr(y, n)
             z = torch.empty_like(y)
+            self.ctx.after_torch()
             _check(lib.fi_system_apply(self.handle, yp, z.data_ptr()))
             self.ctx.synchronize()
             return z
@@ -451,6 +469,9 @@ class BlockTriangularPreconditioner:
         the cap, tau-PCG above it for 2D — configs 2-4, which the reference cannot run)."""
         self.A = A
         mode = {"auto": -1, "lu": 0, "pcg": 1}[inner]
+        if block_cap <= 0 and mode != 1:
+            # krylov.cpp:27-29: N > block_cap throws (the C-ABI reads block_cap <= 0 as the default)
+            raise ResourceLimitError(f"BlockTriangularPreconditioner: block dimension {A.N} exceeds cap {block_cap}")
         h = ctypes.c_void_p()
         _check(lib.fi_precond_create_ex(A.handle, int(block_cap), mode, float(tol), int(maxit), ctypes.byref(h)))
         self.handle = h
@@ -470,6 +491,13 @@ class BlockTriangularPreconditioner:
     def device_bytes(self) -> int:
         return int(lib.fi_precond_bytes(self.handle))
 
+    def stats(self, reset: bool = False) -> dict:
+        """tau-PCG inner-solve counters since the last reset (fi_precond_stats; zeros for dense blocks)."""
+        out = (ctypes.c_longlong * 4)()
+        _check(lib.fi_precond_stats(self.handle, out, 1 if reset else 0))
+        return {"cg_steps": int(out[0]), "nonconverged_blocks": int(out[1]), "max_steps_per_block": int(out[2]),
+                "applies": int(out[3])}
+
     def set_refine(self, refine: bool):
         """Refinement sweep off (default: one FP64 sweep over the polished inverses, forward parity
         with LU solves) or on (an extra sweep; LU-grade residual as well)."""
@@ -482,6 +510,7 @@ class BlockTriangularPreconditioner:
             import torch
             zp = _device_ptr(z, n)
             y = torch.empty_like(z)
+            self.A.ctx.after_torch()
             _check(lib.fi_precond_apply(self.handle, zp, y.data_ptr()))
             self.A.ctx.synchronize()
             return y
@@ -582,11 +611,16 @@ class SolveReport:
     breakdown: bool = False
     wall_time_seconds: float = 0.0
     final_true_residual: float = 0.0
+    inner_nonconverged: int = 0  # EXTENSION: tau-PCG block solves that stopped at maxit above tol
 
 
 def _report(rep: GmresReport, hist: np.ndarray) -> SolveReport:
+    if rep.inner_nonconverged:
+        import warnings
+        warnings.warn(f"gmres: {rep.inner_nonconverged} tau-PCG block solve(s) stopped at maxit above tol; "
+                      "the preconditioner was not applied exactly", RuntimeWarning, stacklevel=3)
     return SolveReport(rep.iterations, [float(v) for v in hist[: rep.history_len]], bool(rep.converged),
-                       bool(rep.breakdown), rep.wall_time_seconds, rep.final_true_residual)
+                       bool(rep.breakdown), rep.wall_time_seconds, rep.final_true_residual, rep.inner_nonconverged)
 
 
 class _CAI:
@@ -623,6 +657,7 @@ def gmres(apply_A, apply_M_inv, b, opts: Optional[GmresOptions] = None, x0=None,
             bp = _device_ptr(b, n)
             x0p = _device_ptr(x0, n) if x0 is not None else None
             x = torch.empty_like(b)
+            A.ctx.after_torch()
             _check(lib.fi_gmres(A.handle, Ph, bp, x0p, x.data_ptr(), ctypes.byref(o), ctypes.byref(rep), _dp(hist),
                                 cap))
             return x, _report(rep, hist)

@@ -28,12 +28,25 @@ def run(cfg, precond=True):
     t0 = time.time()
     A = O.SystemOperator(baseline_problem(O, cfg))
     P = O.BlockTriangularPreconditioner(A, cache=(cfg != 1))
-    Pfs = P if P.inner == "pcg" else None
-    mu = O.forward_solve(A, P=Pfs).mu if cfg != 1 else O.forward_solve(A, P=P).mu
-    mu_eps = O.add_gaussian_noise(mu, NOISE[cfg], SEED_BASE + cfg)
+    prec_file = os.path.join(HERE, f"oracle_config{cfg}.npz")
+    if not precond and os.path.exists(prec_file):
+        # the unpreconditioned solve runs on the same observation as the preconditioned golden
+        mu_eps = np.load(prec_file)["mu_eps"]
+    else:
+        Pfs = P if P.inner == "pcg" else None
+        mu = O.forward_solve(A, P=Pfs).mu if cfg != 1 else O.forward_solve(A, P=P).mu
+        mu_eps = O.add_gaussian_noise(mu, NOISE[cfg], SEED_BASE + cfg)
     z = O.build_rhs(A, mu_eps).z
     t1 = time.time()
-    x, rep = O.gmres(A.apply, P.apply if precond else None, z, tol=TOL[cfg], restart=RESTART,
+    calls = [0]
+
+    def apply_A(v):
+        calls[0] += 1
+        if calls[0] % 50 == 0:
+            print(f"  config {cfg}: {calls[0]} operator applies, {time.time() - t1:.0f}s", flush=True)
+        return A.apply(v)
+
+    x, rep = O.gmres(apply_A, P.apply if precond else None, z, tol=TOL[cfg], restart=RESTART,
                      maxit=0 if precond else 2000)
     t2 = time.time()
     f = x[-A.N:]
