@@ -152,15 +152,15 @@ __global__ void fft_cols_to_spec(ItArgs a, double* lamB) {
 //   T2  (C)  S1, divide by the tau eigenvalues, S1
 // p.delta.p of the new direction follows from z.delta.z + 2 beta z.delta.p_old + beta^2 p_old.delta.p_old.
 // Real data are packed two rows (two columns) per complex transform; the column pass of B works on the
-// L2/2 + 1 columns of the half spectrum.  The FFTs are radix-8 Stockham passes in registers, one group
-// of L/8 threads per transform, exchanging through padded shared memory.
+// L2/2 + 1 columns of the half spectrum.  The FFTs are radix-4 Stockham passes, one group
+// of L/4 threads per transform, exchanging through padded shared memory.
 constexpr int FT = 256;      // threads per CTA of the fused kernel
 constexpr int kRedMax = 4;   // scalars per grid reduction
 
 struct FusedCtl {
     unsigned* bar;                // monotone grid-barrier counter (zeroed before the launch)
     double* parts;                // 2 parities x G x kRedMax block partials
-    unsigned long long* trace;    // optional [10] per-phase time sums of CTA 0 (FI_ITER_TRACE=1)
+    unsigned long long* trace;    // optional [32] per-phase time sums of CTA 0 (FI_ITER_TRACE=1)
     unsigned long long* stats;    // [0] CG steps, [1] levels stopped at maxit, [2] max steps of a level, [3] applies
 };
 __device__ __forceinline__ unsigned long long gtime_ns() {
@@ -179,6 +179,16 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     return v;
 }
 
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
+
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 mul_i(double2 a, bool inv) {  // -i a (forward), +i a (inverse)
@@ -187,53 +197,21 @@ __device__ __forceinline__ double2 mul_i(double2 a, bool inv) {  // -i a (forwar
 // shared-memory index with one pad element per 8 (the radix-8 scatter of the first pass is conflict-free)
 __device__ __forceinline__ int pad8(int i) { return i + (i >> 3); }
 
-// in-register DFT of length 8 (decimation in frequency), forward or inverse (conjugate twiddles)
-__device__ __forceinline__ void dft8(double2 (&a)[8], bool inv) {
-    constexpr double r = 0.70710678118654752440;
-    double2 b[8];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        b[m] = cadd(a[m], a[m + 4]);
-        b[m + 4] = csub(a[m], a[m + 4]);
-    }
-    if (!inv) {
-        b[5] = make_double2(r * (b[5].x + b[5].y), r * (b[5].y - b[5].x));    // x (1 - i)/sqrt2
-        b[7] = make_double2(r * (b[7].y - b[7].x), -r * (b[7].x + b[7].y));   // x (-1 - i)/sqrt2
-    } else {
-        b[5] = make_double2(r * (b[5].x - b[5].y), r * (b[5].x + b[5].y));    // x (1 + i)/sqrt2
-        b[7] = make_double2(-r * (b[7].x + b[7].y), r * (b[7].x - b[7].y));  // x (-1 + i)/sqrt2
-    }
-    b[6] = mul_i(b[6], inv);
-    const double2 c0 = cadd(b[0], b[2]), c2 = csub(b[0], b[2]), c1 = cadd(b[1], b[3]), c3 = mul_i(csub(b[1], b[3]), inv);
-    const double2 c4 = cadd(b[4], b[6]), c6 = csub(b[4], b[6]), c5 = cadd(b[5], b[7]), c7 = mul_i(csub(b[5], b[7]), inv);
-    a[0] = cadd(c0, c1);
-    a[4] = csub(c0, c1);
-    a[2] = cadd(c2, c3);
-    a[6] = csub(c2, c3);
-    a[1] = cadd(c4, c5);
-    a[5] = csub(c4, c5);
-    a[3] = cadd(c6, c7);
-    a[7] = csub(c6, c7);
-}
-__device__ __forceinline__ double2 twv(const double2* tw, int t, int half, bool inv) {
-    double2 w = t < half ? tw[t] : make_double2(-tw[t - half].x, -tw[t - half].y);
-    if (inv) w.y = -w.y;
-    return w;
-}
 
-// Stockham FFT of length L = 2^lg by the nt threads (index t) of one group, between the group's two
-// padded shared buffers (index pad8(i)).  Input in src (natural order); returns the buffer holding the
-// output (natural order).  Every thread of the CTA must call it (it contains __syncthreads); groups
-// without a unit pass active = false.  Passes: one radix-2 or radix-4 pass if lg % 3 != 0, then radix-8.
-__device__ double2* fft_group(double2* src, double2* dst, int L, int lg, const double2* tw, bool inv, int t, int nt,
-                              bool active) {
-    const int half = L >> 1;
-    int p = 1;
-    const int rem = lg % 3;
-    if (rem == 1) {
+// Stockham FFT of length L = 2^LG by the L/4 threads (index t) of one group, between the group's two padded
+// shared buffers (index pad8(i)).  Input in src (natural order); the output lands in src when the number
+// of passes is even, else in dst (natural order).  Radix-4 passes (one radix-2 pass first when LG is odd),
+// one butterfly per thread; LG and the direction are template parameters so the index arithmetic folds
+// to constants.  tw: the full table exp(-2 pi i k / L), k < L.  Every thread of the CTA must call it (it
+// contains __syncthreads); groups without a unit pass active = false.  Not inlined: one copy per length
+// and direction serves every pass (instruction cache).
+template <int LG, bool INV>
+__device__ __noinline__ void fft_group(double2* src, double2* dst, const double2* tw, int t, bool active) {
+    constexpr int L = 1 << LG, Q = L >> 2;
+    if constexpr (LG & 1) {  // radix-2 pass: L/2 butterflies, two per thread
         if (active)
-            for (int j = t; j < half; j += nt) {
-                const double2 x0 = src[pad8(j)], x1 = src[pad8(j + half)];
+            for (int j = t; j < (L >> 1); j += Q) {
+                const double2 x0 = src[pad8(j)], x1 = src[pad8(j + (L >> 1))];
                 dst[pad8(2 * j)] = cadd(x0, x1);
                 dst[pad8(2 * j + 1)] = csub(x0, x1);
             }
@@ -241,51 +219,61 @@ __device__ double2* fft_group(double2* src, double2* dst, int L, int lg, const d
         double2* tt = src;
         src = dst;
         dst = tt;
-        p = 2;
-    } else if (rem == 2) {
-        const int q = L >> 2;
-        if (active)
-            for (int j = t; j < q; j += nt) {
-                const double2 a0 = src[pad8(j)], a1 = src[pad8(j + q)], a2 = src[pad8(j + 2 * q)], a3 = src[pad8(j + 3 * q)];
-                const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = mul_i(csub(a1, a3), inv);
-                dst[pad8(4 * j)] = cadd(s02, s13);
-                dst[pad8(4 * j + 1)] = cadd(d02, d13);
-                dst[pad8(4 * j + 2)] = csub(s02, s13);
-                dst[pad8(4 * j + 3)] = csub(d02, d13);
-            }
-        __syncthreads();
-        double2* tt = src;
-        src = dst;
-        dst = tt;
-        p = 4;
     }
-    const int q = L >> 3;
-    for (; p < L; p <<= 3) {
-        const int tstep = L / (8 * p);
-        if (active)
-            for (int j = t; j < q; j += nt) {
-                const int k = j & (p - 1);
-                double2 v[8];
 #pragma unroll
-                for (int m = 0; m < 8; ++m) v[m] = src[pad8(j + m * q)];
-                if (k) {
-#pragma unroll
-                    for (int m = 1; m < 8; ++m) {
-                        const double2 w = twv(tw, m * k * tstep, half, inv);
-                        v[m] = make_double2(v[m].x * w.x - v[m].y * w.y, v[m].x * w.y + v[m].y * w.x);
-                    }
+    for (int s = (LG & 1); s < LG; s += 2) {
+        const int p = 1 << s;
+        if (active && Q > 0) {
+            const int j = t;
+            const int k = j & (p - 1);
+            double2 a0 = src[pad8(j)], a1 = src[pad8(j + Q)], a2 = src[pad8(j + 2 * Q)], a3 = src[pad8(j + 3 * Q)];
+            if (p > 1) {
+                const int ts = k << (LG - s - 2);  // k L / (4 p)
+                double2 w1 = tw[ts], w2 = tw[2 * ts], w3 = tw[3 * ts];
+                if (INV) {
+                    w1.y = -w1.y;
+                    w2.y = -w2.y;
+                    w3.y = -w3.y;
                 }
-                dft8(v, inv);
-                const int o = (j - k) * 8 + k;
-#pragma unroll
-                for (int m = 0; m < 8; ++m) dst[pad8(o + m * p)] = v[m];
+                a1 = make_double2(a1.x * w1.x - a1.y * w1.y, a1.x * w1.y + a1.y * w1.x);
+                a2 = make_double2(a2.x * w2.x - a2.y * w2.y, a2.x * w2.y + a2.y * w2.x);
+                a3 = make_double2(a3.x * w3.x - a3.y * w3.y, a3.x * w3.y + a3.y * w3.x);
             }
+            const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = mul_i(csub(a1, a3), INV);
+            const int o = 4 * (j - k) + k;
+            dst[pad8(o)] = cadd(s02, s13);
+            dst[pad8(o + p)] = cadd(d02, d13);
+            dst[pad8(o + 2 * p)] = csub(s02, s13);
+            dst[pad8(o + 3 * p)] = csub(d02, d13);
+        }
         __syncthreads();
         double2* tt = src;
         src = dst;
         dst = tt;
     }
-    return src;
+}
+// runtime dispatch on the transform length; returns the buffer index (0 = src) holding the output
+__device__ __forceinline__ int fft_dispatch(double2* src, double2* dst, int lg, const double2* tw, bool inv, int t,
+                                            bool active) {
+#define FI_FFT_CASE(n)                                        \
+    case n:                                                   \
+        if (inv) fft_group<n, true>(src, dst, tw, t, active); \
+        else fft_group<n, false>(src, dst, tw, t, active);    \
+        break;
+    switch (lg) {
+        FI_FFT_CASE(2)
+        FI_FFT_CASE(3)
+        FI_FFT_CASE(4)
+        FI_FFT_CASE(5)
+        FI_FFT_CASE(6)
+        FI_FFT_CASE(7)
+        FI_FFT_CASE(8)
+        FI_FFT_CASE(9)
+        FI_FFT_CASE(10)
+        default: __trap();
+    }
+#undef FI_FFT_CASE
+    return ((lg + 1) / 2) & 1;
 }
 
 __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
@@ -297,7 +285,6 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     const int lane = tid & 31, warp = tid >> 5;
     const long long Np = a.Np;
     const int n1 = a.n1, n2 = a.n2, L1 = a.L1, L2 = a.L2, H2 = a.L2 / 2 + 1, ld2 = a.ld2;
-    unsigned target = 0;
     int rk = 0;
     unsigned long long tlast = 0;
     auto stamp = [&](int ph) {
@@ -307,7 +294,21 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             tlast = now;
         }
     };
+    // finer stamps inside the passes (slots 10..31, CTA 0 thread 0): SM cycles since the previous sub-stamp,
+    // summed in shared memory (a global read-modify-write per stamp would perturb the phases it measures)
+    __shared__ unsigned long long subc[32];
+    if (tid < 32) subc[tid] = 0;
+    long long tsub = 0;
+    auto sub = [&](int slot) {
+        if (ctl.trace && cta == 0 && tid == 0) {
+            const long long now = clock64();
+            if (tsub) subc[slot] += (unsigned long long)(now - tsub);
+            tsub = now;
+        }
+    };
+    unsigned target = 0;
     auto gsync = [&]() {
+        sub(30);  // (everything before the barrier that no other sub-stamp claimed)
         __syncthreads();
         if (tid == 0) {
             const unsigned long long t0 = ctl.trace && cta == 0 ? gtime_ns() : 0;
@@ -315,10 +316,10 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             __threadfence();
             atomicAdd(ctl.bar, 1u);
             unsigned n = 0;
-            // relaxed polls (an acquire load invalidates the SM's L1 on every iteration), one acquire
+            // spinning polls (a __nanosleep poller wakes late); relaxed polls (an acquire load invalidates
+            // the SM's L1 on every iteration), then one acquire
             while (ld_relaxed_u32(ctl.bar) < target) {
-                __nanosleep(32);
-                if (++n == (1u << 26)) __trap();
+                if (++n == (1u << 28)) __trap();
             }
             (void)ld_acquire_u32(ctl.bar);
             if (ctl.trace && cta == 0) {
@@ -327,8 +328,11 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             }
         }
         __syncthreads();
+        sub(31);  // the barrier
     };
     // deterministic grid sum of cnt scalars: block partials in fixed order, every CTA gets the same totals
+    // (measured: polling the partials themselves, NaN-armed, instead of a counter is slower — every CTA
+    // re-reading G slots costs more than one contended atomic)
     auto greduce = [&](double* v, int cnt) {
         for (int c = 0; c < cnt; ++c) {
             double x = v[c];
@@ -344,27 +348,39 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
         }
         gsync();
         if (warp == 0) {
+            double pv[5][kRedMax];
+#pragma unroll
+            for (int u = 0; u < 5; ++u)
+#pragma unroll
+                for (int c = 0; c < kRedMax; ++c) {
+                    const int k = lane + 32 * u;
+                    pv[u][c] = k < G && c < cnt ? __ldcg(pp + (size_t)k * kRedMax + c) : 0.0;
+                }
             for (int c = 0; c < cnt; ++c) {
                 double t = 0.0;
-                for (int k = lane; k < G; k += 32) t += __ldcg(pp + (size_t)k * kRedMax + c);
+#pragma unroll
+                for (int u = 0; u < 5; ++u) t += pv[u][c];
                 for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
                 if (lane == 0) bsum[c] = t;
             }
         }
         __syncthreads();
+        sub(29);
         ++rk;
         for (int c = 0; c < cnt; ++c) v[c] = bsum[c];
     };
     const double sc1 = sqrt(2.0 / (n1 + 1)) * -0.5, sc2 = sqrt(2.0 / (n2 + 1)) * -0.5;
-    double2* tws1 = sm;             // twiddle half tables in shared memory
-    double2* tws2 = sm + L1 / 2;
-    double2* gbuf = tws2 + L2 / 2;  // transform groups: two padded buffers each
-    for (int t = tid; t < L1 / 2; t += FT) tws1[t] = a.tw1[t];
-    for (int t = tid; t < L2 / 2; t += FT) tws2[t] = a.tw2[t];
+    double2* tws1 = sm;             // full twiddle tables exp(-2 pi i k / L), k < L, in shared memory
+    double2* tws2 = sm + L1;
+    double2* gbuf = tws2 + L2;      // transform groups: two padded buffers each
+    for (int t = tid; t < L1; t += FT)
+        tws1[t] = t < L1 / 2 ? a.tw1[t] : make_double2(-a.tw1[t - L1 / 2].x, -a.tw1[t - L1 / 2].y);
+    for (int t = tid; t < L2; t += FT)
+        tws2[t] = t < L2 / 2 ? a.tw2[t] : make_double2(-a.tw2[t - L2 / 2].x, -a.tw2[t - L2 / 2].y);
     __syncthreads();
     // group geometry of the row (length L2) and column (length L1) passes
-    const int ntR = max(L2 >> 3, 1), ngR = FT / ntR, gR = tid / ntR, tR = tid % ntR;
-    const int ntC = max(L1 >> 3, 1), ngC = FT / ntC, gC = tid / ntC, tC = tid % ntC;
+    const int ntR = max(L2 >> 2, 1), ngR = FT / ntR, gR = tid / ntR, tR = tid % ntR;
+    const int ntC = max(L1 >> 2, 1), ngC = FT / ntC, gC = tid / ntC, tC = tid % ntC;
     const int PLR = pad8(L2) + 1, PLC = pad8(L1) + 1;  // padded buffer lengths
     const int nuR = (n1 + 1) / 2, nuB = H2, nuT = (n2 + 1) / 2;  // units of the row, B-column, tau-column passes
     const int rdR = (nuR + G * ngR - 1) / (G * ngR), rdB = (nuB + G * ngC - 1) / (G * ngC),
@@ -372,13 +388,12 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
 
     // ---- group buffers and transforms.  Slot s of a pass owns the group buffers of group s; in round rd
     // it holds the unit cta + G (s + ng rd).  Element work (loads, stores, dot products) is spread over
-    // all FT threads of the CTA, the transforms run on the groups.  Element loops load everything a
-    // thread needs for UF (or 2) elements into registers before the first store, so the loads of a
-    // thread are in flight together (a generic shared-memory store would otherwise pin every later
-    // global load behind it).
+    // all FT threads of the CTA, the transforms run on the groups.  Every element loop issues all of a
+    // thread's loads before its first store, unconditionally at clamped (always valid) addresses with the
+    // unused values discarded by a select: the loads of a thread are in flight together instead of one
+    // L2 round trip per guarded iteration.
     auto rbuf = [&](int g, int w) { return gbuf + (size_t)g * 2 * PLR + (size_t)w * PLR; };
     auto cbuf = [&](int g, int w) { return gbuf + (size_t)g * 2 * PLC + (size_t)w * PLC; };
-    const int npR = (a.lg2 % 3 ? 1 : 0) + a.lg2 / 3, npC = (a.lg1 % 3 ? 1 : 0) + a.lg1 / 3;
     // active slots of this CTA in round rd (a prefix: the unit index grows with the slot)
     auto nact = [&](int nu, int ng, int rd) {
         const int first = cta + G * ng * rd;
@@ -386,15 +401,27 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     };
     auto fftR = [&](int w, bool inv, int rd) -> int {
         const bool act = cta + G * (gR + ngR * rd) < nuR;
-        fft_group(rbuf(gR, w), rbuf(gR, 1 - w), L2, a.lg2, tws2, inv, tR, ntR, act);
-        return w ^ (npR & 1);
+        return w ^ fft_dispatch(rbuf(gR, w), rbuf(gR, 1 - w), a.lg2, tws2, inv, tR, act);
     };
     auto fftC = [&](int w, bool inv, int rd, int nunits) -> int {
         const bool act = cta + G * (gC + ngC * rd) < nunits;
-        fft_group(cbuf(gC, w), cbuf(gC, 1 - w), L1, a.lg1, tws1, inv, tC, ntC, act);
-        return w ^ (npC & 1);
+        return w ^ fft_dispatch(cbuf(gC, w), cbuf(gC, 1 - w), a.lg1, tws1, inv, tC, act);
     };
-    constexpr int UF = 8;  // element-loop unroll: na * L / FT <= 8 always (na <= ng = 8 FT / L)
+    constexpr int UF = 4;  // element-loop unroll: na * L / FT <= 4 always (na <= ng = 4 FT / L)
+    // odd extension of a length-n sequence to L = 2(n + 1): position j holds sg * v[jj]
+    auto oext = [](int j, int n, int L, int& jj, double& sg) {
+        const bool lo = j >= 1 && j <= n, hi = j >= n + 2;
+        jj = lo ? j - 1 : (hi ? L - j - 1 : 0);
+        sg = lo ? 1.0 : (hi ? -1.0 : 0.0);
+    };
+    // row pair of slot s in round rd: clamped row indices and validity
+    auto rowpair = [&](int s, int rd, int& i0c, int& i1c, bool& ok0, bool& ok1) {
+        const int u = cta + G * (s + ngR * rd), i0 = 2 * u;
+        ok0 = u < nuR;
+        ok1 = ok0 && i0 + 1 < n1;
+        i0c = min(i0, n1 - 1);
+        i1c = min(i0 + 1, n1 - 1);
+    };
     // fill buffer 0 of the active row slots with the odd extensions of rows i0, i1 of src (stride sstride)
     auto fill_dst_rows = [&](const double* src, long long sstride, int rd) {
         const int lim = nact(nuR, ngR, rd) * L2;
@@ -402,43 +429,35 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
 #pragma unroll
         for (int q = 0; q < UF; ++q) {
             const int e = tid + q * FT;
-            v[q] = make_double2(0.0, 0.0);
-            if (e < lim) {
-                const int s = e / L2, j = e - s * L2, i0 = 2 * (cta + G * (s + ngR * rd));
-                const bool v1 = i0 + 1 < n1;
-                int jj = -1;
-                double sg = 1.0;
-                if (j >= 1 && j <= n2) jj = j - 1;
-                else if (j >= n2 + 2) {
-                    jj = L2 - j - 1;
-                    sg = -1.0;
-                }
-                if (jj >= 0) {
-                    v[q].x = sg * src[(long long)i0 * sstride + jj];
-                    if (v1) v[q].y = sg * src[(long long)(i0 + 1) * sstride + jj];
-                }
-            }
+            const bool ok = e < lim;
+            const int ec = ok ? e : 0, s = ec >> a.lg2, j = ec & (L2 - 1);
+            int i0c, i1c, jj;
+            bool ok0, ok1;
+            double sg;
+            rowpair(s, rd, i0c, i1c, ok0, ok1);
+            oext(j, n2, L2, jj, sg);
+            const double x0 = src[(long long)i0c * sstride + jj], x1 = src[(long long)i1c * sstride + jj];
+            v[q] = make_double2(ok && ok0 ? sg * x0 : 0.0, ok && ok1 ? sg * x1 : 0.0);
         }
 #pragma unroll
         for (int q = 0; q < UF; ++q) {
             const int e = tid + q * FT;
-            if (e < lim) {
-                const int s = e / L2;
-                rbuf(s, 0)[pad8(e - s * L2)] = v[q];
-            }
+            if (e < lim) rbuf(e >> a.lg2, 0)[pad8(e & (L2 - 1))] = v[q];
         }
         __syncthreads();
     };
-    // DST-I along the rows of the active row pairs (buffer 0 filled) into the same rows of Rr.  Two real
+    // DST-I along the rows of the active row pairs (buffer w0 filled) into the same rows of Rr.  Two real
     // odd sequences share one complex FFT: FFT(oe(a) + i oe(b)) = i A - B with A, B real: A = Im, B = -Re.
-    auto dst_rows_out = [&](int rd) {
-        const int w = fftR(0, false, rd);
-        const int lim = nact(nuR, ngR, rd) * n2;
-        for (int e = tid; e < lim; e += FT) {
-            const int s = e / n2, k = e - s * n2, i0 = 2 * (cta + G * (s + ngR * rd));
-            const double2 c = rbuf(s, w)[pad8(k + 1)];
-            a.Rr[(long long)i0 * n2 + k] = sc2 * c.y;
-            if (i0 + 1 < n1) a.Rr[(long long)(i0 + 1) * n2 + k] = -sc2 * c.x;
+    auto dst_rows_out = [&](int rd, int w0 = 0) {
+        const int w = fftR(w0, false, rd);
+        const int na = nact(nuR, ngR, rd);
+        for (int s = 0; s < na; ++s) {
+            const int i0 = 2 * (cta + G * (s + ngR * rd));
+            for (int k = tid; k < n2; k += FT) {
+                const double2 c = rbuf(s, w)[pad8(k + 1)];
+                a.Rr[(long long)i0 * n2 + k] = sc2 * c.y;
+                if (i0 + 1 < n1) a.Rr[(long long)(i0 + 1) * n2 + k] = -sc2 * c.x;
+            }
         }
         __syncthreads();
     };
@@ -446,24 +465,28 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     // spectra k = 0 .. L2/2 into rows i0, i1 of dst (row stride H2)
     auto f2_rows = [&](double2* dst, int w0, int rd) {
         const int w = fftR(w0, false, rd);
-        const int lim = nact(nuR, ngR, rd) * H2;
-        for (int e = tid; e < lim; e += FT) {
-            const int s = e / H2, k = e - s * H2, i0 = 2 * (cta + G * (s + ngR * rd));
-            const double2 P = rbuf(s, w)[pad8(k)], Qc = rbuf(s, w)[pad8((L2 - k) & (L2 - 1))];
-            const double2 Q = make_double2(Qc.x, -Qc.y);
-            dst[(long long)i0 * H2 + k] = make_double2(0.5 * (P.x + Q.x), 0.5 * (P.y + Q.y));
-            if (i0 + 1 < n1) dst[(long long)(i0 + 1) * H2 + k] = make_double2(0.5 * (P.y - Q.y), -0.5 * (P.x - Q.x));
+        const int na = nact(nuR, ngR, rd);
+        for (int s = 0; s < na; ++s) {
+            const int i0 = 2 * (cta + G * (s + ngR * rd));
+            for (int k = tid; k < H2; k += FT) {
+                const double2 P = rbuf(s, w)[pad8(k)], Qc = rbuf(s, w)[pad8((L2 - k) & (L2 - 1))];
+                const double2 Q = make_double2(Qc.x, -Qc.y);
+                dst[(long long)i0 * H2 + k] = make_double2(0.5 * (P.x + Q.x), 0.5 * (P.y + Q.y));
+                if (i0 + 1 < n1)
+                    dst[(long long)(i0 + 1) * H2 + k] = make_double2(0.5 * (P.y - Q.y), -0.5 * (P.x - Q.x));
+            }
         }
         __syncthreads();
     };
-    // element (row, column < n2) of the active row pairs: e in [0, na * 2 n2) -> padded index, or -1
-    auto row_elem = [&](int e, int rd, int& s, int& hi, int& j) -> long long {
-        s = e / (2 * n2);
-        const int rem = e - s * 2 * n2;
-        hi = rem >= n2;
-        j = rem - hi * n2;
-        const int ii = 2 * (cta + G * (s + ngR * rd)) + hi;
-        return ii < n1 ? (long long)ii * ld2 + j : -1;
+    // element idx in [0, 2 n2) of row pair s (row i0 + hi, column j < n2): clamped padded index, validity
+    auto row_elem = [&](int s, int idx, int rd, bool& ok, int& hi, int& j) -> long long {
+        const bool in = idx < 2 * n2;
+        const int ic = in ? idx : 0;
+        hi = ic >= n2;
+        j = ic - hi * n2;
+        const int u = cta + G * (s + ngR * rd), ii = 2 * u + hi;
+        ok = in && u < nuR && ii < n1;
+        return (long long)min(ii, n1 - 1) * ld2 + j;
     };
 
     // ---- the passes
@@ -478,98 +501,106 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             // block's 8 targets L is formed reading each y_m once (element pairs, 8 levels in flight);
             // per level the <= 7 recent terms are added
             const int nt8 = min(8, a.S - B0);
-            const int tot = nact(nuR, ngR, 0) > 0 ? ngR * rdR * n2 : 0;  // element pairs (2 rows per unit)
-            for (int e = tid; e < tot; e += FT) {
-                const int s = e / n2, j = e - s * n2, u = cta + G * s;
-                if (u >= nuR) continue;
-                const int i0 = 2 * u;
-                const bool v1 = i0 + 1 < n1;
-                const long long o0 = (long long)i0 * ld2 + j, o1 = v1 ? o0 + ld2 : o0;
-                double acc0[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, acc1[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-                for (int m0 = 0; m0 < B0; m0 += 8) {
-                    double y0[8], y1[8];
+            for (int s = 0; s < ngR * rdR; ++s)  // the CTA's units of every round; element pairs (rows i0, i1)
+                for (int j = tid; j < n2; j += FT) {
+                    const int u = cta + G * s;
+                    if (u >= nuR) continue;
+                    const int i0 = 2 * u;
+                    const bool v1 = i0 + 1 < n1;
+                    const long long o0 = (long long)i0 * ld2 + j, o1 = v1 ? o0 + ld2 : o0;
+                    double acc0[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                    double acc1[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                    for (int m0 = 0; m0 < B0; m0 += 8) {
+                        double y0[8], y1[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        y0[q] = a.y[(long long)(m0 + q) * Np + o0];
-                        y1[q] = a.y[(long long)(m0 + q) * Np + o1];
+                        for (int q = 0; q < 8; ++q) {
+                            y0[q] = a.y[(long long)(m0 + q) * Np + o0];
+                            y1[q] = a.y[(long long)(m0 + q) * Np + o1];
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+#pragma unroll
+                            for (int t8 = 0; t8 < 8; ++t8)
+                                if (t8 < nt8) {
+                                    const double ev = a.e[B0 + t8 - m0 - q];
+                                    acc0[t8] += ev * y0[q];
+                                    acc1[t8] += ev * y1[q];
+                                }
                     }
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-#pragma unroll
-                        for (int t8 = 0; t8 < 8; ++t8)
-                            if (t8 < nt8) {
-                                const double ev = a.e[B0 + t8 - m0 - q];
-                                acc0[t8] += ev * y0[q];
-                                acc1[t8] += ev * y1[q];
-                            }
+                    for (int t8 = 0; t8 < 8; ++t8) {
+                        a.hb[(long long)t8 * Np + o0] = acc0[t8];
+                        if (v1) a.hb[(long long)t8 * Np + o1] = acc1[t8];
+                    }
                 }
-#pragma unroll
-                for (int t8 = 0; t8 < 8; ++t8) {
-                    a.hb[(long long)t8 * Np + o0] = acc0[t8];
-                    if (v1) a.hb[(long long)t8 * Np + o1] = acc1[t8];
-                }
-            }
             __syncthreads();
         }
+        const bool tl = lv < a.S;
+        const long long lo = (long long)min(lv, a.S - 1) * Np;  // this level's rows of z, D1, 1/D2 (f-block: S-1)
         for (int rd = 0; rd < rdR; ++rd) {
-            const int lim = nact(nuR, ngR, rd) * 2 * n2;
-            for (int base = 0; base < lim; base += 2 * FT) {
-                double bq[2], x0q[2], xvq[2];
-                long long oq[2];
+            const int nae = nact(nuR, ngR, rd);
+            for (int sb = 0; sb < nae; ++sb)
+                for (int base = 0; base < 2 * n2; base += 2 * FT) {
+                    double bq[2], x0q[2], xvq[2];
+                    long long oq[2];
+                    bool okq[2];
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int e = base + tid + q * FT;
-                    int s, hi, j;
-                    oq[q] = e < lim ? row_elem(e, rd, s, hi, j) : -1;
-                    bq[q] = x0q[q] = xvq[q] = 0.0;
-                    const long long o = oq[q];
-                    if (o < 0) continue;
-                    if (lv < a.S) {
-                        double hist = B0 > 0 ? a.hb[(long long)jt * Np + o] : 0.0;
+                    for (int q = 0; q < 2; ++q) {
+                        int hi, j;
+                        const long long o = row_elem(sb, base + tid + q * FT, rd, okq[q], hi, j);
+                        oq[q] = o;
+                        // every load at a valid address; the selects below drop what this element does not use
+                        const double hbv = a.hb[(long long)jt * Np + o];
                         double yr[7];
 #pragma unroll
-                        for (int m = 0; m < 7; ++m) yr[m] = m < nrec ? a.y[(long long)(B0 + m) * Np + o] : 0.0;
-#pragma unroll
-                        for (int m = 0; m < 7; ++m)
-                            if (m < nrec) hist += a.e[lv - B0 - m] * yr[m];
-                        const long long oo = (long long)lv * Np + o;
-                        const double rhs = a.z_in[oo] - a.D1[oo] * hist;
-                        if (direct) xvq[q] = rhs / (a.e0 * a.D1[oo]);
-                        else bq[q] = rhs * a.d2inv[oo];
-                    } else {
-                        const double rhs = a.z_in[(long long)a.S * Np + o] - a.y[(long long)(a.S - 1) * Np + o];
-                        bq[q] = rhs * a.d2inv[(long long)(a.S - 1) * Np + o];
-                    }
-                    // initial guess of the time levels: the polynomial extrapolation through the previous kx
-                    // levels' solutions, x0 = sum_j (-1)^(j+1) C(kx, j) y_(lv-j)
-                    if (warm) {
+                        for (int m = 0; m < 7; ++m) yr[m] = a.y[(long long)(m < nrec ? B0 + m : 0) * Np + o];
+                        const double zv = a.z_in[(tl ? (long long)lv * Np : (long long)a.S * Np) + o];
+                        const double d1 = a.D1[lo + o], d2i = a.d2inv[lo + o];
+                        const double yprev = a.y[(long long)max(lv - 1, 0) * Np + o];
                         double yw[kWarmOrder];
 #pragma unroll
-                        for (int jj = 0; jj < kWarmOrder; ++jj)
-                            yw[jj] = jj < kx ? a.y[(long long)(lv - 1 - jj) * Np + o] : 0.0;
+                        for (int jj = 0; jj < kWarmOrder; ++jj) yw[jj] = a.y[(long long)max(lv - 1 - jj, 0) * Np + o];
+                        double b = 0.0, xv = 0.0, x0 = 0.0;
+                        if (tl) {
+                            double hist = B0 > 0 ? hbv : 0.0;
 #pragma unroll
-                        for (int jj = 0; jj < kWarmOrder; ++jj)
-                            if (jj < kx) x0q[q] += kWarmCoef[kx][jj + 1] * yw[jj];
+                            for (int m = 0; m < 7; ++m)
+                                if (m < nrec) hist += a.e[lv - B0 - m] * yr[m];
+                            const double rhs = zv - d1 * hist;
+                            if (direct) xv = rhs / (a.e0 * d1);
+                            else b = rhs * d2i;
+                        } else {
+                            b = (zv - yprev) * d2i;  // f-block: z_f - y_S (the last time level)
+                        }
+                        // initial guess of the time levels: the polynomial extrapolation through the previous
+                        // kx levels' solutions, x0 = sum_j (-1)^(j+1) C(kx, j) y_(lv-j)
+                        if (warm) {
+#pragma unroll
+                            for (int jj = 0; jj < kWarmOrder; ++jj)
+                                if (jj < kx) x0 += kWarmCoef[kx][jj + 1] * yw[jj];
+                        }
+                        bq[q] = okq[q] ? b : 0.0;
+                        x0q[q] = okq[q] ? x0 : 0.0;
+                        xvq[q] = xv;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        if (!okq[q]) continue;
+                        const long long o = oq[q];
+                        a.r[o] = bq[q];
+                        a.zz[o] = bq[q];
+                        a.p[o] = x0q[q];
+                        x[o] = xvq[q];
+                        bn += bq[q] * bq[q];
                     }
                 }
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const long long o = oq[q];
-                    if (o < 0) continue;
-                    a.r[o] = bq[q];
-                    a.zz[o] = bq[q];
-                    a.p[o] = x0q[q];
-                    x[o] = xvq[q];
-                    bn += bq[q] * bq[q];
-                }
-            }
             if (direct) continue;  // grid-uniform
             __syncthreads();
             if (warm) {
                 // (row i0, row i1) pairs of x0 (zero beyond n2) into buffer 0, then F2 -> Zh
                 const int limf = nact(nuR, ngR, rd) * L2;
                 for (int e = tid; e < limf; e += FT) {
-                    const int s = e / L2, j = e - s * L2, i0 = 2 * (cta + G * (s + ngR * rd));
+                    const int s = e >> a.lg2, j = e & (L2 - 1), i0 = 2 * (cta + G * (s + ngR * rd));
                     double2 v = make_double2(0.0, 0.0);
                     if (j < n2) {
                         v.x = a.p[(long long)i0 * ld2 + j];
@@ -584,6 +615,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                 dst_rows_out(rd);
             }
         }
+        sub(27);
         return bn;
     };
     // B2: columns k of the half spectrum: X = Zh + beta Xp (F2 of the new direction; stored to Xp when
@@ -596,60 +628,59 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
 #pragma unroll
             for (int q = 0; q < UF; ++q) {
                 const int e = tid + q * FT;
-                v[q] = make_double2(0.0, 0.0);
-                if (e < lim) {
-                    const int s = e / L1, j = e - s * L1, k = cta + G * (s + ngC * rd);
-                    if (j < n1) {
-                        const long long o = (long long)j * H2 + k;
-                        v[q] = a.Zh[o];
-                        if (beta != 0.0) {
-                            const double2 xp = a.Xp[o];
-                            v[q].x += beta * xp.x;
-                            v[q].y += beta * xp.y;
-                        }
-                    }
+                const bool ok = e < lim;
+                const int ec = ok ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
+                const int kc = min(cta + G * (s + ngC * rd), H2 - 1);
+                const long long o = (long long)min(j, n1 - 1) * H2 + kc;
+                double2 zv = a.Zh[o];
+                if (beta != 0.0) {
+                    const double2 xp = a.Xp[o];
+                    zv.x += beta * xp.x;
+                    zv.y += beta * xp.y;
                 }
+                v[q] = ok && j < n1 ? zv : make_double2(0.0, 0.0);
             }
 #pragma unroll
             for (int q = 0; q < UF; ++q) {
                 const int e = tid + q * FT;
                 if (e < lim) {
-                    const int s = e / L1, j = e - s * L1, k = cta + G * (s + ngC * rd);
+                    const int s = e >> a.lg1, j = e & (L1 - 1), k = cta + G * (s + ngC * rd);
                     if (keep && j < n1) a.Xp[(long long)j * H2 + k] = v[q];
                     cbuf(s, 0)[pad8(j)] = v[q];
                 }
             }
+            sub(23);
             __syncthreads();
             const int w = fftC(0, false, rd, nuB);
+            sub(24);
             double lam[UF];
 #pragma unroll
             for (int q = 0; q < UF; ++q) {
                 const int e = tid + q * FT;
-                lam[q] = 0.0;
-                if (e < lim) {
-                    const int s = e / L1, j = e - s * L1, k = cta + G * (s + ngC * rd);
-                    lam[q] = a.lamB[(long long)j * L2 + k];
-                }
+                const int ec = e < lim ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
+                lam[q] = a.lamB[(long long)j * L2 + min(cta + G * (s + ngC * rd), H2 - 1)];
             }
 #pragma unroll
             for (int q = 0; q < UF; ++q) {
                 const int e = tid + q * FT;
                 if (e < lim) {
-                    const int s = e / L1, j = e - s * L1, k = cta + G * (s + ngC * rd);
+                    const int s = e >> a.lg1, j = e & (L1 - 1), k = cta + G * (s + ngC * rd);
                     const double wk = (k == 0 || k == L2 / 2) ? 1.0 : 2.0;
                     double2* cell = cbuf(s, w) + pad8(j);
-                    const double2 c = *cell;
-                    pbp += wk * lam[q] * (c.x * c.x + c.y * c.y);
-                    *cell = make_double2(c.x * lam[q], c.y * lam[q]);
+                    const double2 cv = *cell;
+                    pbp += wk * lam[q] * (cv.x * cv.x + cv.y * cv.y);
+                    *cell = make_double2(cv.x * lam[q], cv.y * lam[q]);
                 }
             }
+            sub(25);
             __syncthreads();
             const int w2 = fftC(w, true, rd, nuB);
-            const int limo = nact(nuB, ngC, rd) * n1;
-            for (int e = tid; e < limo; e += FT) {
-                const int s = e / n1, j = e - s * n1, k = cta + G * (s + ngC * rd);
-                a.Yb[(long long)j * H2 + k] = cbuf(s, w2)[pad8(j)];
+            const int nao = nact(nuB, ngC, rd);
+            for (int s = 0; s < nao; ++s) {
+                const int k = cta + G * (s + ngC * rd);
+                for (int j = tid; j < n1; j += FT) a.Yb[(long long)j * H2 + k] = cbuf(s, w2)[pad8(j)];
             }
+            sub(26);
             __syncthreads();
         }
         return pbp;
@@ -658,6 +689,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     // delta p; x += alpha p; r -= alpha Ap; partial ||r||^2; S2(r) -> Rr
     auto passB3 = [&](int lv, double c, double alpha, double beta, bool cg) -> double {
         const long long lo = (long long)min(lv, a.S - 1) * Np;
+        const bool tl = lv < a.S;
         double* x = a.y + (long long)lv * Np;
         double part = 0.0;
         for (int rd = 0; rd < rdR; ++rd) {
@@ -667,72 +699,87 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             for (int q = 0; q < UF; ++q) {
                 // packed spectrum D = Y0 + i Y1 of the row pair from the two Hermitian half spectra
                 const int e = tid + q * FT;
-                v[q] = make_double2(0.0, 0.0);
-                if (e < lim) {
-                    const int s = e / L2, k = e - s * L2, i0 = 2 * (cta + G * (s + ngR * rd));
-                    const int kk = k <= L2 / 2 ? k : L2 - k;
-                    double2 y0 = a.Yb[(long long)i0 * H2 + kk];
-                    double2 y1 = i0 + 1 < n1 ? a.Yb[(long long)(i0 + 1) * H2 + kk] : make_double2(0.0, 0.0);
-                    if (kk == 0 || kk == L2 / 2) {
-                        y0.y = 0.0;
-                        y1.y = 0.0;
-                    }
-                    if (k > L2 / 2) {
-                        y0.y = -y0.y;
-                        y1.y = -y1.y;
-                    }
-                    v[q] = make_double2(y0.x - y1.y, y0.y + y1.x);
+                const bool ok = e < lim;
+                const int ec = ok ? e : 0, s = ec >> a.lg2, k = ec & (L2 - 1);
+                int i0c, i1c;
+                bool ok0, ok1;
+                rowpair(s, rd, i0c, i1c, ok0, ok1);
+                const int kk = k <= L2 / 2 ? k : L2 - k;
+                double2 y0 = a.Yb[(long long)i0c * H2 + kk];
+                double2 y1 = a.Yb[(long long)i1c * H2 + kk];
+                if (!ok1) y1 = make_double2(0.0, 0.0);
+                if (kk == 0 || kk == L2 / 2) {
+                    y0.y = 0.0;
+                    y1.y = 0.0;
                 }
+                if (k > L2 / 2) {
+                    y0.y = -y0.y;
+                    y1.y = -y1.y;
+                }
+                v[q] = make_double2(y0.x - y1.y, y0.y + y1.x);
             }
 #pragma unroll
             for (int q = 0; q < UF; ++q) {
                 const int e = tid + q * FT;
-                if (e < lim) {
-                    const int s = e / L2;
-                    rbuf(s, 0)[pad8(e - s * L2)] = v[q];
-                }
+                if (e < lim) rbuf(e >> a.lg2, 0)[pad8(e & (L2 - 1))] = v[q];
             }
+            sub(10);
             __syncthreads();
             const int w = fftR(0, true, rd);
-            const int lime = nact(nuR, ngR, rd) * 2 * n2;
-            for (int base = 0; base < lime; base += 2 * FT) {
-                double pq[2], zq[2], dq[2], xq[2], rq[2], bpq[2];
-                long long oq[2];
+            sub(11);
+            const int nae = nact(nuR, ngR, rd);
+            for (int sb = 0; sb < nae; ++sb) {
+                for (int base = 0; base < 2 * n2; base += 2 * FT) {
+                    double pq[2], zq[2], dq[2], xq[2], rq[2], bpq[2];
+                    long long oq[2];
+                    bool okq[2];
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int e = base + tid + q * FT;
-                    int s, hi, j;
-                    oq[q] = e < lime ? row_elem(e, rd, s, hi, j) : -1;
-                    const long long o = oq[q];
-                    pq[q] = zq[q] = dq[q] = xq[q] = rq[q] = bpq[q] = 0.0;
-                    if (o < 0) continue;
-                    const double2 yv = rbuf(s, w)[pad8(j)];
-                    bpq[q] = (hi ? yv.y : yv.x) * a.inv_LL;
-                    pq[q] = a.p[o];
-                    if (cg) zq[q] = a.zz[o];
-                    if (lv < a.S) dq[q] = a.e0 * a.D1[lo + o] * a.d2inv[lo + o];
-                    xq[q] = x[o];
-                    rq[q] = a.r[o];
-                }
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const long long o = oq[q];
-                    if (o < 0) continue;
-                    double pv = pq[q];
-                    if (cg) {
-                        pv = beta != 0.0 ? zq[q] + beta * pv : zq[q];
-                        a.p[o] = pv;
+                    for (int q = 0; q < 2; ++q) {
+                        int hi, j;
+                        const long long o = row_elem(sb, base + tid + q * FT, rd, okq[q], hi, j);
+                        oq[q] = o;
+                        const double2 yv = rbuf(sb, w)[pad8(j)];
+                        bpq[q] = (hi ? yv.y : yv.x) * a.inv_LL;
+                        pq[q] = a.p[o];
+                        zq[q] = a.zz[o];
+                        const double d1 = a.D1[lo + o], d2i = a.d2inv[lo + o];
+                        dq[q] = tl ? a.e0 * d1 * d2i : 0.0;
+                        xq[q] = x[o];
+                        rq[q] = a.r[o];
                     }
-                    const double ap = c * bpq[q] + dq[q] * pv;
-                    x[o] = xq[q] + alpha * pv;
-                    const double rv = rq[q] - alpha * ap;
-                    a.r[o] = rv;
-                    part += rv * rv;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int e = base + tid + q * FT;
+                        if (e >= 2 * n2) continue;
+                        double rv = 0.0;  // a row beyond n1 (odd n1) contributes zeros to the DST input
+                        if (okq[q]) {
+                            const long long o = oq[q];
+                            double pv = pq[q];
+                            if (cg) {
+                                pv = beta != 0.0 ? zq[q] + beta * pv : zq[q];
+                                a.p[o] = pv;
+                            }
+                            const double ap = c * bpq[q] + dq[q] * pv;
+                            x[o] = xq[q] + alpha * pv;
+                            rv = rq[q] - alpha * ap;
+                            a.r[o] = rv;
+                            part += rv * rv;
+                        }
+                        // the DST input of the new r straight from registers: odd extension of the row,
+                        // r_j at j + 1 and -r_j at L2 - 1 - j (row i0 in .x, row i1 in .y)
+                        const int hi = e >= n2, j = e - hi * n2;
+                        double* d0 = reinterpret_cast<double*>(rbuf(sb, 1 - w) + pad8(j + 1)) + hi;
+                        double* d1 = reinterpret_cast<double*>(rbuf(sb, 1 - w) + pad8(L2 - 1 - j)) + hi;
+                        *d0 = rv;
+                        *d1 = -rv;
+                    }
                 }
+                if (tid < 2) rbuf(sb, 1 - w)[pad8(tid == 0 ? 0 : n2 + 1)] = make_double2(0.0, 0.0);
             }
+            sub(12);
             __syncthreads();
-            fill_dst_rows(a.r, ld2, rd);
-            dst_rows_out(rd);
+            dst_rows_out(rd, 1 - w);
+            sub(13);
         }
         return part;
     };
@@ -740,14 +787,16 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     auto passFallback = [&](int lv) {
         double* x = a.y + (long long)lv * Np;
         for (int rd = 0; rd < rdR; ++rd) {
-            const int lime = nact(nuR, ngR, rd) * 2 * n2;
-            for (int e = tid; e < lime; e += FT) {
-                int s, hi, j;
-                const long long o = row_elem(e, rd, s, hi, j);
-                if (o < 0) continue;
-                a.r[o] = a.zz[o];
-                x[o] = 0.0;
-            }
+            const int nae = nact(nuR, ngR, rd);
+            for (int s = 0; s < nae; ++s)
+                for (int e = tid; e < 2 * n2; e += FT) {
+                    bool ok;
+                    int hi, j;
+                    const long long o = row_elem(s, e, rd, ok, hi, j);
+                    if (!ok) continue;
+                    a.r[o] = a.zz[o];
+                    x[o] = 0.0;
+                }
             __syncthreads();
             fill_dst_rows(a.r, ld2, rd);
             dst_rows_out(rd);
@@ -762,51 +811,40 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
 #pragma unroll
             for (int q = 0; q < UF; ++q) {
                 const int e = tid + q * FT;
-                v[q] = make_double2(0.0, 0.0);
-                if (e < lim) {
-                    const int s = e / L1, j = e - s * L1, k0 = 2 * (cta + G * (s + ngC * rd));
-                    int jj = -1;
-                    double sg = 1.0;
-                    if (j >= 1 && j <= n1) jj = j - 1;
-                    else if (j >= n1 + 2) {
-                        jj = L1 - j - 1;
-                        sg = -1.0;
-                    }
-                    if (jj >= 0) {
-                        v[q].x = sg * a.Rr[(long long)jj * n2 + k0];
-                        if (k0 + 1 < n2) v[q].y = sg * a.Rr[(long long)jj * n2 + k0 + 1];
-                    }
-                }
+                const bool ok = e < lim;
+                const int ec = ok ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
+                const int k0 = 2 * (cta + G * (s + ngC * rd));
+                const int k0c = min(k0, n2 - 1), k1c = min(k0 + 1, n2 - 1);
+                int jj;
+                double sg;
+                oext(j, n1, L1, jj, sg);
+                const double x0 = a.Rr[(long long)jj * n2 + k0c], x1 = a.Rr[(long long)jj * n2 + k1c];
+                v[q] = make_double2(ok ? sg * x0 : 0.0, ok && k0 + 1 < n2 ? sg * x1 : 0.0);
             }
 #pragma unroll
             for (int q = 0; q < UF; ++q) {
                 const int e = tid + q * FT;
-                if (e < lim) {
-                    const int s = e / L1;
-                    cbuf(s, 0)[pad8(e - s * L1)] = v[q];
-                }
+                if (e < lim) cbuf(e >> a.lg1, 0)[pad8(e & (L1 - 1))] = v[q];
             }
+            sub(14);
             __syncthreads();
             const int w = fftC(0, false, rd, nuT);
+            sub(15);
             double2 il[UF];
 #pragma unroll
             for (int q = 0; q < UF; ++q) {
                 const int e = tid + q * FT;
-                il[q] = make_double2(0.0, 0.0);
-                if (e < lim) {
-                    const int s = e / L1, j = e - s * L1, k0 = 2 * (cta + G * (s + ngC * rd));
-                    const int kk = (j >= 1 && j <= n1) ? j : (j >= n1 + 2 ? L1 - j : -1);
-                    if (kk > 0) {
-                        il[q].x = a.lamT[(long long)(kk - 1) * n2 + k0];
-                        if (k0 + 1 < n2) il[q].y = a.lamT[(long long)(kk - 1) * n2 + k0 + 1];
-                    }
-                }
+                const int ec = e < lim ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
+                const int k0 = 2 * (cta + G * (s + ngC * rd));
+                const int k0c = min(k0, n2 - 1), k1c = min(k0 + 1, n2 - 1);
+                const int kk = (j >= 1 && j <= n1) ? j : (j >= n1 + 2 ? L1 - j : 1);
+                il[q] = make_double2(a.lamT[(long long)(kk - 1) * n2 + k0c], a.lamT[(long long)(kk - 1) * n2 + k1c]);
             }
 #pragma unroll
             for (int q = 0; q < UF; ++q) {
                 const int e = tid + q * FT;
                 if (e < lim) {
-                    const int s = e / L1, j = e - s * L1, k0 = 2 * (cta + G * (s + ngC * rd));
+                    const int s = e >> a.lg1, j = e & (L1 - 1), k0 = 2 * (cta + G * (s + ngC * rd));
                     double x0 = 0.0, x1 = 0.0;
                     int kk = -1;
                     double sg = 1.0;
@@ -823,140 +861,175 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                     cbuf(s, 1 - w)[pad8(j)] = make_double2(x0, x1);
                 }
             }
+            sub(16);
             __syncthreads();
             const int w2 = fftC(1 - w, false, rd, nuT);
-            const int limo = nact(nuT, ngC, rd) * n1;
-            for (int e = tid; e < limo; e += FT) {
-                const int s = e / n1, j = e - s * n1, k0 = 2 * (cta + G * (s + ngC * rd));
-                const double2 cv = cbuf(s, w2)[pad8(j + 1)];
-                a.Rr[(long long)j * n2 + k0] = sc1 * cv.y;
-                if (k0 + 1 < n2) a.Rr[(long long)j * n2 + k0 + 1] = -sc1 * cv.x;
+            const int nao = nact(nuT, ngC, rd);
+            for (int s = 0; s < nao; ++s) {
+                const int k0 = 2 * (cta + G * (s + ngC * rd));
+                for (int j = tid; j < n1; j += FT) {
+                    const double2 cv = cbuf(s, w2)[pad8(j + 1)];
+                    a.Rr[(long long)j * n2 + k0] = sc1 * cv.y;
+                    if (k0 + 1 < n2) a.Rr[(long long)j * n2 + k0 + 1] = -sc1 * cv.x;
+                }
             }
+            sub(17);
             __syncthreads();
         }
     };
     // T3: zz = S2(Rr rows); partials r.z, z.delta.z, z.delta.p (p = the previous direction); F2(z) -> Zh
     auto passT3 = [&](int lv, double* part3) {
         const long long lo = (long long)min(lv, a.S - 1) * Np;
+        const bool tl = lv < a.S;
         part3[0] = part3[1] = part3[2] = 0.0;
         for (int rd = 0; rd < rdR; ++rd) {
             fill_dst_rows(a.Rr, n2, rd);
+            sub(18);
             const int w = fftR(0, false, rd);
+            sub(19);
             // z values into buffer 1 - w (pairs, zero beyond n2), zz stores and the dot-product partials
-            const int limz = nact(nuR, ngR, rd) * L2;
-            for (int e = tid; e < limz; e += FT) {
-                const int s = e / L2, k = e - s * L2, i0 = 2 * (cta + G * (s + ngR * rd));
-                double2 zv = make_double2(0.0, 0.0);
-                if (k < n2) {
-                    const double2 cv = rbuf(s, w)[pad8(k + 1)];
-                    zv = make_double2(sc2 * cv.y, i0 + 1 < n1 ? -sc2 * cv.x : 0.0);
+            const int nae = nact(nuR, ngR, rd);
+            for (int sb = 0; sb < nae; ++sb) {
+                for (int base = 0; base < 2 * n2; base += 2 * FT) {
+                    double zq[2], rq[2], pq[2], dq[2];
+                    long long oq[2];
+                    bool okq[2];
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        int hi, j;
+                        const long long o = row_elem(sb, base + tid + q * FT, rd, okq[q], hi, j);
+                        oq[q] = o;
+                        const double2 cv = rbuf(sb, w)[pad8(j + 1)];
+                        zq[q] = hi ? -sc2 * cv.x : sc2 * cv.y;
+                        rq[q] = a.r[o];
+                        pq[q] = a.p[o];
+                        const double d1 = a.D1[lo + o], d2i = a.d2inv[lo + o];
+                        dq[q] = tl ? a.e0 * d1 * d2i : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int e = base + tid + q * FT;
+                        if (e >= 2 * n2) continue;
+                        const double zv = okq[q] ? zq[q] : 0.0;
+                        if (okq[q]) {
+                            a.zz[oq[q]] = zv;
+                            part3[0] += rq[q] * zv;
+                            part3[1] += dq[q] * zv * zv;
+                            part3[2] += dq[q] * zv * pq[q];
+                        }
+                        const int hi = e >= n2, j = e - hi * n2;
+                        reinterpret_cast<double*>(rbuf(sb, 1 - w) + pad8(j))[hi] = zv;  // (z_i0, z_i1) pairs
+                    }
                 }
-                rbuf(s, 1 - w)[pad8(k)] = zv;
+                for (int k = n2 + tid; k < L2; k += FT) rbuf(sb, 1 - w)[pad8(k)] = make_double2(0.0, 0.0);
             }
+            sub(21);
             __syncthreads();
-            const int lime = nact(nuR, ngR, rd) * 2 * n2;
-            for (int base = 0; base < lime; base += 2 * FT) {
-                double zq[2], rq[2], pq[2], dq[2];
-                long long oq[2];
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int e = base + tid + q * FT;
-                    int s, hi, j;
-                    oq[q] = e < lime ? row_elem(e, rd, s, hi, j) : -1;
-                    const long long o = oq[q];
-                    zq[q] = rq[q] = pq[q] = dq[q] = 0.0;
-                    if (o < 0) continue;
-                    const double2 zv = rbuf(s, 1 - w)[pad8(j)];
-                    zq[q] = hi ? zv.y : zv.x;
-                    rq[q] = a.r[o];
-                    pq[q] = a.p[o];
-                    if (lv < a.S) dq[q] = a.e0 * a.D1[lo + o] * a.d2inv[lo + o];
-                }
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const long long o = oq[q];
-                    if (o < 0) continue;
-                    a.zz[o] = zq[q];
-                    part3[0] += rq[q] * zq[q];
-                    part3[1] += dq[q] * zq[q] * zq[q];
-                    part3[2] += dq[q] * zq[q] * pq[q];
-                }
-            }
             f2_rows(a.Zh, 1 - w, rd);
+            sub(22);
         }
     };
 
-    // a guess worse than zero (||b - M x0|| > ||b||: the input is not smooth in time) switches the warm
-    // start off for the rest of the apply (the decision is grid-uniform: it uses reduced values)
+    // The level / CG loop as a phase machine, so that every pass is inlined at exactly one place (the
+    // kernel's code stays small enough for the instruction cache).
+    enum { PH_SETUP, PH_B2, PH_B3, PH_FALLBACK, PH_T2, PH_T3 };
     bool warm_ok = true;
-    for (int lv = 0; lv < a.levels; ++lv) {
-        const bool direct = lv < a.S && a.direct[lv];
-        const int kx = min(lv, kWarmOrder);
-        bool warm = a.warm && warm_ok && lv >= 1 && lv < a.S && !direct;
-        for (int j = 1; j <= kx; ++j) warm = warm && !a.direct[lv - j];
-        double red[kRedMax];
-        red[0] = passR0(lv, direct, warm, kx);
-        greduce(red, 1);
-        const double bn2 = red[0];
-        stamp(0);
-        if (bn2 == 0.0 || direct) continue;
-        const double c = level_c(a, lv);
-        const double stop2 = a.tol * a.tol * bn2;
-        if (warm) {
-            // pre-step with alpha = 1 along p = x0: x = x0, r = b - M x0 (and the DST rows of r)
-            passB2(0.0, false);
-            gsync();
-            red[0] = passB3(lv, c, 1.0, 0.0, false);
-            greduce(red, 1);
-            const double rn0 = red[0];
-            stamp(1);
-            if (sqrt(rn0) <= a.tol * sqrt(bn2)) continue;  // the guess already solves the level
-            if (rn0 > bn2) {                                // a guess worse than 0: restart from x = 0, r = b
-                warm_ok = false;
-                passFallback(lv);
-                gsync();
-                stamp(1);
-            }
-        }
-        (void)stop2;
-        // ---- initial tau solve: zz = tau^{-1} r, p = zz, rz = r.zz
-        passT2(lv);
-        gsync();
-        stamp(2);
-        passT3(lv, red);
-        greduce(red, 3);
-        stamp(3);
-        double rz = red[0], pdp = red[1], beta = 0.0;
-        int it = 0;
-        bool conv = false;
-        while (true) {
-            red[0] = passB2(beta, true);
-            greduce(red, 1);
-            stamp(4);
-            const double alpha = rz / (c * a.inv_LL * red[0] + pdp);
-            red[0] = passB3(lv, c, alpha, beta, true);
-            greduce(red, 1);
-            stamp(5);
-            ++it;
-            conv = sqrt(red[0]) <= a.tol * sqrt(bn2);
-            if (conv || it >= a.maxit) break;
-            passT2(lv);
-            gsync();
-            stamp(2);
-            passT3(lv, red);
-            greduce(red, 3);
-            stamp(3);
-            beta = red[0] / rz;
-            rz = red[0];
-            pdp = red[1] + 2.0 * beta * red[2] + beta * beta * pdp;
-        }
-        if (ctl.stats && cta == 0 && tid == 0) {
+    int lv = 0, phase = PH_SETUP, it = 0, kx = 0;
+    bool direct = false, warm = false, pre = false, first_t3 = true;
+    double bn2 = 0.0, c = 0.0, rz = 0.0, pdp = 0.0, beta = 0.0, alpha = 0.0;
+    double red[kRedMax];
+    auto level_done = [&](bool cg, bool conv) {
+        if (cg && ctl.stats && cta == 0 && tid == 0) {
             ctl.stats[0] += (unsigned long long)it;
             if (!conv) ctl.stats[1] += 1;
             if ((unsigned long long)it > ctl.stats[2]) ctl.stats[2] = it;
         }
+        ++lv;
+        phase = PH_SETUP;
+    };
+    while (lv < a.levels) {
+        if (phase == PH_SETUP) {
+            // ---- level setup: rhs (forward substitution, krylov.cpp:55-68), b = rhs / D2, initial guess
+            direct = lv < a.S && a.direct[lv];
+            kx = min(lv, kWarmOrder);
+            warm = a.warm && warm_ok && lv >= 1 && lv < a.S && !direct;
+            for (int j = 1; j <= kx; ++j) warm = warm && !a.direct[lv - j];
+            red[0] = passR0(lv, direct, warm, kx);
+            greduce(red, 1);
+            bn2 = red[0];
+            stamp(0);
+            if (bn2 == 0.0 || direct) {
+                level_done(false, true);
+                continue;
+            }
+            c = level_c(a, lv);
+            it = 0;
+            first_t3 = true;
+            // warm start: a pre-step with alpha = 1 along p = x0 gives x = x0, r = b - M x0
+            pre = warm;
+            phase = warm ? PH_B2 : PH_T2;
+        } else if (phase == PH_B2) {
+            // B2 (the pre-step: X = F2(x0), nothing kept); then alpha = r.z / p.A p
+            red[0] = passB2(pre ? 0.0 : beta, !pre);
+            if (pre) {
+                gsync();
+            } else {
+                greduce(red, 1);
+                alpha = rz / (c * a.inv_LL * red[0] + pdp);
+            }
+            stamp(4);
+            phase = PH_B3;
+        } else if (phase == PH_B3) {
+            red[0] = pre ? passB3(lv, c, 1.0, 0.0, false) : passB3(lv, c, alpha, beta, true);
+            greduce(red, 1);
+            stamp(5);
+            const bool conv = sqrt(red[0]) <= a.tol * sqrt(bn2);
+            if (pre) {
+                pre = false;
+                if (conv) {  // the guess already solves the level
+                    level_done(true, true);
+                    continue;
+                }
+                phase = red[0] > bn2 ? PH_FALLBACK : PH_T2;  // a guess worse than 0: restart from x = 0, r = b
+            } else {
+                ++it;
+                if (conv || it >= a.maxit) {
+                    level_done(true, conv);
+                    continue;
+                }
+                phase = PH_T2;
+            }
+        } else if (phase == PH_FALLBACK) {
+            warm_ok = false;
+            passFallback(lv);
+            gsync();
+            stamp(1);
+            phase = PH_T2;
+        } else if (phase == PH_T2) {
+            passT2(lv);
+            gsync();
+            stamp(2);
+            phase = PH_T3;
+        } else {  // PH_T3: z = tau^{-1} r complete; r.z and the new direction's p.delta.p
+            passT3(lv, red);
+            greduce(red, 3);
+            stamp(3);
+            if (first_t3) {  // p = z
+                first_t3 = false;
+                beta = 0.0;
+                rz = red[0];
+                pdp = red[1];
+            } else {
+                beta = red[0] / rz;
+                rz = red[0];
+                pdp = red[1] + 2.0 * beta * red[2] + beta * beta * pdp;
+            }
+            phase = PH_B2;
+        }
     }
     if (ctl.stats && cta == 0 && tid == 0) ctl.stats[3] += 1;
+    if (ctl.trace && cta == 0 && tid == 0)
+        for (int i = 10; i < 32; ++i) ctl.trace[i] = subc[i];
 }
 
 int ilog2(int v) {
@@ -1130,8 +1203,8 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
     a.skip = skip;
     const int H2 = a.L2 / 2 + 1;
     const int plr = a.L2 + a.L2 / 8 + 1, plc = a.L1 + a.L1 / 8 + 1;
-    const int ngr = FT / std::max(a.L2 / 8, 1), ngc = FT / std::max(a.L1 / 8, 1);
-    const size_t smem = ((size_t)a.L1 / 2 + a.L2 / 2 + std::max((size_t)ngr * 2 * plr, (size_t)ngc * 2 * plc)) *
+    const int ngr = FT / std::max(a.L2 / 4, 1), ngc = FT / std::max(a.L1 / 4, 1);
+    const size_t smem = ((size_t)a.L1 + a.L2 + std::max((size_t)ngr * 2 * plr, (size_t)ngc * 2 * plc)) *
                         sizeof(double2);
     if (smem > 227 * 1024) throw Error(FI_E_RESOURCE, "tau_pcg_fused: shared memory");
     if (P->it_fgrid == 0) {
@@ -1141,7 +1214,7 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
         if (per_sm < 1) throw Error(FI_E_CUDA, "tau_pcg_fused cannot be resident");
         // one CTA per SM, or fewer when the passes have fewer units (small grids)
         const int units = std::max(std::max((a.n1 + 1) / 2, (a.n2 + 1) / 2), H2);
-        P->it_fgrid = std::min(ctx->sm_count, units);
+        P->it_fgrid = std::min(std::min(ctx->sm_count, units), 160);  // treduce polls <= 5 slots per lane
         P->it_fparts.alloc((size_t)2 * kRedMax * P->it_fgrid);
         P->it_fbar.alloc(1);
     } else {
@@ -1150,7 +1223,7 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
     static const bool tracing = std::getenv("FI_ITER_TRACE") != nullptr;
     DevBuf<unsigned long long> trace;
     if (tracing) {
-        trace.alloc(10);
+        trace.alloc(32);
         FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
     }
     FusedCtl ctl{P->it_fbar.p, P->it_fparts.p, tracing ? trace.p : nullptr, P->it_stats.p};
@@ -1160,13 +1233,16 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
                                         ctx->stream));
     FI_LAUNCHED(ctx);
     if (tracing) {
-        unsigned long long h[10];
+        unsigned long long h[32];
         FI_CUDA(cudaMemcpyAsync(h, trace.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
         std::fprintf(stderr,
                      "[tau_pcg_fused] ms: setup %.3f | pre-step %.3f | T2 %.3f | T3+red %.3f | B2+red %.3f | "
                      "B3+red %.3f | barrier wait (CTA 0) %.3f over %llu barriers\n",
                      h[0] * 1e-6, h[1] * 1e-6, h[2] * 1e-6, h[3] * 1e-6, h[4] * 1e-6, h[5] * 1e-6, h[8] * 1e-6, h[9]);
+        std::fprintf(stderr, "[tau_pcg_fused] sub-phases Mcycles (CTA 0):");
+        for (int i = 10; i < 32; ++i) std::fprintf(stderr, " %d:%.3f", i, h[i] * 1e-6);
+        std::fprintf(stderr, "\n");
     }
 }
 
