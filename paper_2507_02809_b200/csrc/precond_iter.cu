@@ -179,16 +179,6 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     return v;
 }
 
-__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
-    double v;
-    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
-    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
-}
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
-
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 mul_i(double2 a, bool inv) {  // -i a (forward), +i a (inverse)
@@ -381,7 +371,15 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     // group geometry of the row (length L2) and column (length L1) passes
     const int ntR = max(L2 >> 2, 1), ngR = FT / ntR, gR = tid / ntR, tR = tid % ntR;
     const int ntC = max(L1 >> 2, 1), ngC = FT / ntC, gC = tid / ntC, tC = tid % ntC;
+    const int ngR_ = ngR, ngC_ = ngC;
     const int PLR = pad8(L2) + 1, PLC = pad8(L1) + 1;  // padded buffer lengths
+    // the row pairs of a row pass are the same in every row pass: the CTA's rows of r, z, p, x and delta
+    // stay in shared memory for the whole level (x is also written to global memory: the later levels'
+    // history and the output need it)
+    enum { V_R, V_ZZ, V_P, V_X, V_DL, V_N };
+    const int VW = 2 * ld2;  // doubles per owned row pair and vector
+    double* vsm = reinterpret_cast<double*>(gbuf + max(ngR_ * 2 * PLR, ngC_ * 2 * PLC));
+    auto vrow = [&](int ou, int arr) { return vsm + ((size_t)ou * V_N + arr) * VW; };
     const int nuR = (n1 + 1) / 2, nuB = H2, nuT = (n2 + 1) / 2;  // units of the row, B-column, tau-column passes
     const int rdR = (nuR + G * ngR - 1) / (G * ngR), rdB = (nuB + G * ngC - 1) / (G * ngC),
               rdT = (nuT + G * ngC - 1) / (G * ngC);
@@ -443,6 +441,19 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
         for (int q = 0; q < UF; ++q) {
             const int e = tid + q * FT;
             if (e < lim) rbuf(e >> a.lg2, 0)[pad8(e & (L2 - 1))] = v[q];
+        }
+        __syncthreads();
+    };
+    // the same from the CTA's own rows in shared memory (vector arr)
+    auto fill_dst_rows_smem = [&](int arr, int rd) {
+        const int lim = nact(nuR, ngR, rd) * L2;
+        for (int e = tid; e < lim; e += FT) {
+            const int s = e >> a.lg2, j = e & (L2 - 1);
+            const double* v = vrow(s + ngR * rd, arr);
+            int jj;
+            double sg;
+            oext(j, n2, L2, jj, sg);
+            rbuf(s, 0)[pad8(j)] = make_double2(sg * v[jj], sg * v[ld2 + jj]);
         }
         __syncthreads();
     };
@@ -541,7 +552,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             const int nae = nact(nuR, ngR, rd);
             for (int sb = 0; sb < nae; ++sb)
                 for (int base = 0; base < 2 * n2; base += 2 * FT) {
-                    double bq[2], x0q[2], xvq[2];
+                    double bq[2], x0q[2], xvq[2], dlq[2];
                     long long oq[2];
                     bool okq[2];
 #pragma unroll
@@ -582,15 +593,21 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                         bq[q] = okq[q] ? b : 0.0;
                         x0q[q] = okq[q] ? x0 : 0.0;
                         xvq[q] = xv;
+                        dlq[q] = tl ? a.e0 * d1 * d2i : 0.0;
                     }
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
+                        const int e = base + tid + q * FT;
+                        if (e >= 2 * n2) continue;
+                        const int hi = e >= n2, li = hi * ld2 + (e - hi * n2), ou = sb + ngR * rd;
+                        // (an element beyond n1 stores zeros: the DST fills read whole row pairs)
+                        vrow(ou, V_R)[li] = bq[q];
+                        vrow(ou, V_ZZ)[li] = bq[q];
+                        vrow(ou, V_P)[li] = x0q[q];
+                        vrow(ou, V_X)[li] = okq[q] ? xvq[q] : 0.0;
+                        vrow(ou, V_DL)[li] = okq[q] ? dlq[q] : 0.0;
                         if (!okq[q]) continue;
-                        const long long o = oq[q];
-                        a.r[o] = bq[q];
-                        a.zz[o] = bq[q];
-                        a.p[o] = x0q[q];
-                        x[o] = xvq[q];
+                        x[oq[q]] = xvq[q];
                         bn += bq[q] * bq[q];
                     }
                 }
@@ -600,18 +617,14 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                 // (row i0, row i1) pairs of x0 (zero beyond n2) into buffer 0, then F2 -> Zh
                 const int limf = nact(nuR, ngR, rd) * L2;
                 for (int e = tid; e < limf; e += FT) {
-                    const int s = e >> a.lg2, j = e & (L2 - 1), i0 = 2 * (cta + G * (s + ngR * rd));
-                    double2 v = make_double2(0.0, 0.0);
-                    if (j < n2) {
-                        v.x = a.p[(long long)i0 * ld2 + j];
-                        if (i0 + 1 < n1) v.y = a.p[(long long)(i0 + 1) * ld2 + j];
-                    }
-                    rbuf(s, 0)[pad8(j)] = v;
+                    const int s = e >> a.lg2, j = e & (L2 - 1);
+                    const double* p0 = vrow(s + ngR * rd, V_P);
+                    rbuf(s, 0)[pad8(j)] = j < n2 ? make_double2(p0[j], p0[ld2 + j]) : make_double2(0.0, 0.0);
                 }
                 __syncthreads();
                 f2_rows(a.Zh, 0, rd);
             } else {
-                fill_dst_rows(a.r, ld2, rd);
+                fill_dst_rows_smem(V_R, rd);
                 dst_rows_out(rd);
             }
         }
@@ -689,7 +702,6 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     // delta p; x += alpha p; r -= alpha Ap; partial ||r||^2; S2(r) -> Rr
     auto passB3 = [&](int lv, double c, double alpha, double beta, bool cg) -> double {
         const long long lo = (long long)min(lv, a.S - 1) * Np;
-        const bool tl = lv < a.S;
         double* x = a.y + (long long)lv * Np;
         double part = 0.0;
         for (int rd = 0; rd < rdR; ++rd) {
@@ -740,34 +752,36 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                         oq[q] = o;
                         const double2 yv = rbuf(sb, w)[pad8(j)];
                         bpq[q] = (hi ? yv.y : yv.x) * a.inv_LL;
-                        pq[q] = a.p[o];
-                        zq[q] = a.zz[o];
-                        const double d1 = a.D1[lo + o], d2i = a.d2inv[lo + o];
-                        dq[q] = tl ? a.e0 * d1 * d2i : 0.0;
-                        xq[q] = x[o];
-                        rq[q] = a.r[o];
+                        const int li = hi * ld2 + j, ou = sb + ngR * rd;
+                        pq[q] = vrow(ou, V_P)[li];
+                        zq[q] = vrow(ou, V_ZZ)[li];
+                        dq[q] = vrow(ou, V_DL)[li];
+                        xq[q] = vrow(ou, V_X)[li];
+                        rq[q] = vrow(ou, V_R)[li];
                     }
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         const int e = base + tid + q * FT;
                         if (e >= 2 * n2) continue;
                         double rv = 0.0;  // a row beyond n1 (odd n1) contributes zeros to the DST input
+                        const int hi = e >= n2, j = e - hi * n2, li = hi * ld2 + j, ou = sb + ngR * rd;
                         if (okq[q]) {
                             const long long o = oq[q];
                             double pv = pq[q];
                             if (cg) {
                                 pv = beta != 0.0 ? zq[q] + beta * pv : zq[q];
-                                a.p[o] = pv;
+                                vrow(ou, V_P)[li] = pv;
                             }
                             const double ap = c * bpq[q] + dq[q] * pv;
-                            x[o] = xq[q] + alpha * pv;
+                            const double xv = xq[q] + alpha * pv;
+                            vrow(ou, V_X)[li] = xv;
+                            x[o] = xv;
                             rv = rq[q] - alpha * ap;
-                            a.r[o] = rv;
+                            vrow(ou, V_R)[li] = rv;
                             part += rv * rv;
                         }
                         // the DST input of the new r straight from registers: odd extension of the row,
                         // r_j at j + 1 and -r_j at L2 - 1 - j (row i0 in .x, row i1 in .y)
-                        const int hi = e >= n2, j = e - hi * n2;
                         double* d0 = reinterpret_cast<double*>(rbuf(sb, 1 - w) + pad8(j + 1)) + hi;
                         double* d1 = reinterpret_cast<double*>(rbuf(sb, 1 - w) + pad8(L2 - 1 - j)) + hi;
                         *d0 = rv;
@@ -793,12 +807,13 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                     bool ok;
                     int hi, j;
                     const long long o = row_elem(s, e, rd, ok, hi, j);
-                    if (!ok) continue;
-                    a.r[o] = a.zz[o];
-                    x[o] = 0.0;
+                    const int li = hi * ld2 + j, ou = s + ngR * rd;
+                    vrow(ou, V_R)[li] = vrow(ou, V_ZZ)[li];
+                    vrow(ou, V_X)[li] = 0.0;
+                    if (ok) x[o] = 0.0;
                 }
             __syncthreads();
-            fill_dst_rows(a.r, ld2, rd);
+            fill_dst_rows_smem(V_R, rd);
             dst_rows_out(rd);
         }
     };
@@ -879,8 +894,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     };
     // T3: zz = S2(Rr rows); partials r.z, z.delta.z, z.delta.p (p = the previous direction); F2(z) -> Zh
     auto passT3 = [&](int lv, double* part3) {
-        const long long lo = (long long)min(lv, a.S - 1) * Np;
-        const bool tl = lv < a.S;
+        (void)lv;
         part3[0] = part3[1] = part3[2] = 0.0;
         for (int rd = 0; rd < rdR; ++rd) {
             fill_dst_rows(a.Rr, n2, rd);
@@ -892,19 +906,17 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             for (int sb = 0; sb < nae; ++sb) {
                 for (int base = 0; base < 2 * n2; base += 2 * FT) {
                     double zq[2], rq[2], pq[2], dq[2];
-                    long long oq[2];
                     bool okq[2];
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         int hi, j;
-                        const long long o = row_elem(sb, base + tid + q * FT, rd, okq[q], hi, j);
-                        oq[q] = o;
+                        (void)row_elem(sb, base + tid + q * FT, rd, okq[q], hi, j);
                         const double2 cv = rbuf(sb, w)[pad8(j + 1)];
                         zq[q] = hi ? -sc2 * cv.x : sc2 * cv.y;
-                        rq[q] = a.r[o];
-                        pq[q] = a.p[o];
-                        const double d1 = a.D1[lo + o], d2i = a.d2inv[lo + o];
-                        dq[q] = tl ? a.e0 * d1 * d2i : 0.0;
+                        const int li = hi * ld2 + j, ou = sb + ngR * rd;
+                        rq[q] = vrow(ou, V_R)[li];
+                        pq[q] = vrow(ou, V_P)[li];
+                        dq[q] = vrow(ou, V_DL)[li];
                     }
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
@@ -912,7 +924,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                         if (e >= 2 * n2) continue;
                         const double zv = okq[q] ? zq[q] : 0.0;
                         if (okq[q]) {
-                            a.zz[oq[q]] = zv;
+                            vrow(sb + ngR * rd, V_ZZ)[(e >= n2) * ld2 + e - (e >= n2) * n2] = zv;
                             part3[0] += rq[q] * zv;
                             part3[1] += dq[q] * zv * zv;
                             part3[2] += dq[q] * zv * pq[q];
@@ -1204,8 +1216,11 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
     const int H2 = a.L2 / 2 + 1;
     const int plr = a.L2 + a.L2 / 8 + 1, plc = a.L1 + a.L1 / 8 + 1;
     const int ngr = FT / std::max(a.L2 / 4, 1), ngc = FT / std::max(a.L1 / 4, 1);
+    const int nown = 1 + ((a.n1 + 1) / 2 - 1) / std::min(std::min(ctx->sm_count, std::max(std::max((a.n1 + 1) / 2,
+                                                         (a.n2 + 1) / 2), H2)), 160);  // row pairs per CTA
     const size_t smem = ((size_t)a.L1 + a.L2 + std::max((size_t)ngr * 2 * plr, (size_t)ngc * 2 * plc)) *
-                        sizeof(double2);
+                            sizeof(double2) +
+                        (size_t)nown * 5 * 2 * a.ld2 * sizeof(double);
     if (smem > 227 * 1024) throw Error(FI_E_RESOURCE, "tau_pcg_fused: shared memory");
     if (P->it_fgrid == 0) {
         ensure_smem_attr((const void*)tau_pcg_fused, smem);
@@ -1214,7 +1229,7 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
         if (per_sm < 1) throw Error(FI_E_CUDA, "tau_pcg_fused cannot be resident");
         // one CTA per SM, or fewer when the passes have fewer units (small grids)
         const int units = std::max(std::max((a.n1 + 1) / 2, (a.n2 + 1) / 2), H2);
-        P->it_fgrid = std::min(std::min(ctx->sm_count, units), 160);  // treduce polls <= 5 slots per lane
+        P->it_fgrid = std::min(std::min(ctx->sm_count, units), 160);  // greduce reads <= 5 partials per lane
         P->it_fparts.alloc((size_t)2 * kRedMax * P->it_fgrid);
         P->it_fbar.alloc(1);
     } else {
