@@ -224,29 +224,42 @@ def cpu_reference_sample(cfg: int, iters: int, threads: int, nlev: int = 12):
             P.pcg.iterations = []
             k = min(nlev, S)
             Y = np.zeros((k, N))
-            t_lev = []
+            t_solve, t_hist_l = [], []
             for s in range(1, k + 1):
                 t0 = time.perf_counter()
                 rhs = z[(s - 1) * N: s * N].copy()
                 if s > 1:
                     rhs -= D1[s - 1] * (e[s - 1:0:-1] @ Y[: s - 1])
+                t1 = time.perf_counter()
                 Y[s - 1] = P.solve_block(s, rhs, [Y[s - 1 - j] for j in range(1, min(O.WARM_ORDER, s - 1) + 1)])
-                t_lev.append(time.perf_counter() - t0)
-            steady = float(np.mean(t_lev[O.WARM_ORDER:])) if k > O.WARM_ORDER else float(np.mean(t_lev))
+                t_solve.append(time.perf_counter() - t1)
+                t_hist_l.append(t1 - t0)
+            its = list(P.pcg.iterations[:k])
+            # per-level solve time = a + b * (CG steps): least squares over the sampled levels
+            A_ls = np.stack([np.ones(k), np.array(its, dtype=float)], axis=1)
+            (a_fix, b_step), *_ = np.linalg.lstsq(A_ls, np.array(t_solve), rcond=None)
+            if not (b_step > 0 and a_fix >= 0):
+                b_step = float(np.sum(t_solve)) / float(np.sum(np.array(its) + 1))
+                a_fix = b_step
+            # the oracle's own CG step counts of every level on this input (tests/golden/gen_pcg_steps.py)
+            try:
+                steps = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_pcg_steps.json")))[str(cfg)]
+                counts = steps["steps_per_level"]
+                src = "per-level CG step counts of the oracle's full apply (tests/golden/oracle_pcg_steps.json)"
+            except Exception:
+                counts = its + [its[-1]] * (S + 1 - k)
+                src = "the last sampled level's CG step count for the unsampled levels"
             # the history sum at full depth (S - 1 previous levels), scaled linearly in s
             Yh = rng.uniform(-1, 1, (S - 1, N))
             t0 = time.perf_counter()
             _ = e[S - 1:0:-1] @ Yh
             t_hist = time.perf_counter() - t0
             del Yh
-            t0 = time.perf_counter()
-            P.solve_block(S + 1, z[S * N:] - Y[k - 1])
-            t_f = time.perf_counter() - t0
-            t_P = sum(t_lev) + (S - k) * steady + sum(t_hist * s / S for s in range(k + 1, S + 1)) + t_f
-            its = P.pcg.iterations
-            how = (f"P: the first {k} of {S} time levels of the tau-PCG substitution timed (CG steps "
-                   f"{its[:k]}), the rest at the warm-start steady state ({steady * 1e3:.1f} ms/level) plus "
-                   f"the history sum at its true length, f-block timed")
+            t_P = sum(a_fix + b_step * c for c in counts) + sum(t_hist * s / S for s in range(2, S + 1))
+            how = (f"P: the first {k} of {S} time levels of the tau-PCG substitution timed level by level "
+                   f"(CG steps {its}; per level {a_fix * 1e3:.1f} ms + {b_step * 1e3:.2f} ms per CG step, least "
+                   f"squares), extrapolated to all {S + 1} levels with {src} ({sum(counts)} steps) plus the L1 "
+                   f"history sum at its true length")
         # one MGS step at k = iters/2 (k+1 dots + axpys over the (S+1)N vector, krylov.cpp:127-132)
         kk = max(1, iters // 2)
         w = v.copy()

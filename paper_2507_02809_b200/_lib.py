@@ -8,7 +8,7 @@ import os
 import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libfracinv_b200.so")
+LIB_PATH = os.environ.get("FI_LIB_PATH") or os.path.join(PKG, "libfracinv_b200.so")  # FI_LIB_PATH: A/B builds
 HEADER = os.path.join(os.path.dirname(PKG), "include", "fracinv_b200.h")
 
 FI_OK, FI_E_DIM, FI_E_RESOURCE, FI_E_SINGULAR, FI_E_DOMAIN, FI_E_CUDA, FI_E_NOCONV, FI_E_CONFIG = range(8)
@@ -123,6 +123,8 @@ def load():
             "(the B200 path has no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in _SIGS.items():
+        if os.environ.get("FI_LIB_PATH") and not hasattr(lib, name):
+            continue  # an A/B build of an older ABI
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
