@@ -1,6 +1,7 @@
 // C-ABI entry points (include/fracinv_b200.h).  Every call converts library exceptions
 // into status codes; the message and SingularBlockError time index are kept per host
 // thread (fi_last_error, fi_last_error_time_index).
+#include <atomic>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -106,6 +107,8 @@ fi_precond* build_precond(fi_system* sys, long long block_cap, int mode = -1, do
         throw fib::Error(FI_E_DOMAIN, "tau-PCG preconditioner needs fi_system_desc.omega");
     fi_precond* P = new fi_precond();
     P->sys = sys;
+    static std::atomic<unsigned long long> next_uid{1};
+    P->uid = next_uid++;
     try {
         if (mode == 1) fib::precond_build_iterative(P, tol, maxit);
         else fib::precond_build(P);
@@ -562,8 +565,17 @@ int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x
         sys->engine->set_fused(split && P ? &Fz : nullptr);
         std::vector<double> hist;
         if (P && P->mode == 1) FI_CUDA(cudaMemsetAsync(P->it_stats.p, 0, P->it_stats.bytes(), ctx->stream));
-        sys->engine->solve(A, P ? &M : nullptr, b.p, x0_dev ? x0.p : nullptr, x.p, opts->tol, maxit, opts->restart,
-                           report, hist);
+        // device-driven (one CUDA graph per solve, one host synchronisation) unless the restart cycle's
+        // basis does not fit or full GMRES was asked for (its basis grows on demand: host-driven loop)
+        static const bool device_env = !(std::getenv("FI_GMRES_DEVICE") && std::atoi(std::getenv("FI_GMRES_DEVICE")) == 0);
+        const std::vector<long long> key = {(long long)(P ? P->uid : 0), P ? P->refine : -1, split ? 1 : 0,
+                                            (long long)(P ? P->mode : -1)};
+        const bool done = device_env && sys->engine->solve_device(A, P ? &M : nullptr, b.p, x0_dev ? x0.p : nullptr,
+                                                                  x.p, opts->tol, maxit, opts->restart, key, report,
+                                                                  hist);
+        if (!done)
+            sys->engine->solve(A, P ? &M : nullptr, b.p, x0_dev ? x0.p : nullptr, x.p, opts->tol, maxit,
+                               opts->restart, report, hist);
         sys->engine->set_fused(nullptr);
         report->inner_nonconverged = 0;
         if (P && P->mode == 1) {

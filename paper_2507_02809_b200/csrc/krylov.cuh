@@ -9,21 +9,27 @@
 
 namespace fib {
 
-// Device-resident Arnoldi/Givens state (one per solve).
+// Device-resident Arnoldi/Givens state (one per solve).  The pointer fields come first (the host
+// rewrites them alone when the workspace grows during a solve).
 struct GmresState {
-    double* h;      // current Hessenberg column (cycle + 2)
-    double* c;      // second-pass corrections (cycle + 2)
+    double* h;      // current Hessenberg column (capacity + 1)
+    double* c;      // second-pass corrections
     double* cs;     // Givens cosines
     double* sn;     // Givens sines
     double* g;      // rotated right-hand side
     double* ycoef;  // back-substitution result
-    double* R;      // rotated columns, column k at R + k * ldR
-    int ldR;
+    double* R;      // rotated columns, packed: column k (k + 1 entries) at k (k + 1) / 2
     double bnorm, tol, breakdown_tol;
     double pre_norm2, hnorm2;
     int done, reorth, vnext_ok, iters, kc, converged, breakdown;
+    int k;      // device-driven solve: Arnoldi step within the cycle
+    int steps;  // device-driven solve: steps of this cycle, min(restart, maxit - iterations)
+    int flags;  // device-driven solve: bit 0 zero right-hand side, bit 1 converged at the start
+    int ncycles, nresid;  // device-driven solve: executions of the cycle body and of the restart residual
+    double beta, bnorm_true, final_rn2;
     double scal[4];  // scratch norms read back by the host
 };
+constexpr int kStatePointers = 7;
 
 inline double* scal_dev(GmresState* st_dev) {
     return reinterpret_cast<double*>(reinterpret_cast<char*>(st_dev) + offsetof(GmresState, scal));
@@ -44,19 +50,33 @@ public:
     GmresEngine(const GmresEngine&) = delete;
     GmresEngine& operator=(const GmresEngine&) = delete;
     long long n() const { return n_; }
-    // Reference semantics of gmres() (krylov.cpp:72-209) + restart extension (DESIGN.md §5).
     // optional: w = M^{-1} A v in one operation (used for the Arnoldi step instead of A then M)
     void set_fused(const Op* f) { fused_ = f; }
     // measurement hook (bench roofline): average time of one MGS round w -= c x; h = y.w over
-    // device vectors of length n(), L2 flushed (a write larger than L2) before every timed round
+    // device vectors of length n(), L2 flushed (a read larger than L2) before every timed round
     double time_mgs_round(double* w, const double* x, const double* y, int reps);
+    // Reference semantics of gmres() (krylov.cpp:72-209) + restart extension (DESIGN.md §5).
+    // Host-driven: the host enqueues every Arnoldi step, two steps ahead of the device's convergence
+    // flag; the Krylov basis grows on demand (full GMRES allocates as it goes, like the reference).
     void solve(const Op& A, const Op* M, const double* b, const double* x0, double* x, double tol, int maxit,
                int restart, fi_gmres_report* rep, std::vector<double>& history);
+    // Device-driven: the whole solve is one CUDA graph (conditional WHILE nodes for the restart cycles
+    // and the Arnoldi steps, an IF node for the restart residual); the host launches it and synchronises
+    // once.  The operators must be capturable (stream-ordered, no host synchronisation).  Returns false
+    // (nothing done) when the cycle's basis does not fit in device memory; use solve() then.
+    // key: what the captured graph depends on besides this engine's own buffers (the caller's object ids
+    // and settings); a different key re-captures.
+    bool solve_device(const Op& A, const Op* M, const double* b, const double* x0, double* x, double tol, int maxit,
+                      int restart, const std::vector<long long>& key, fi_gmres_report* rep,
+                      std::vector<double>& history);
 
 private:
-    void reduce(double* w, const double* x, const double* coef, const double* y, int mode, int k, int slot,
-                double* out, const int* gate_on, const int* done);
+    void reduce(double* w, const double* x, const double* coef, const double* y, int mode, int slot,
+                const int* done);
     double norm2(const double* v, int slot);
+    void mgs_step(int k, int maxit, bool graph, unsigned long long cond);
+    void reserve(int vectors, bool keep);  // basis and coefficient arrays for `vectors` basis vectors
+    void bind_state_pointers();
 
     template <class T>
     static void ensure(DevBuf<T>& b, size_t count) {
@@ -64,18 +84,24 @@ private:
     }
 
     fi_ctx* ctx_;
-    long long n_;
-    int grid_;
+    long long n_, ldv_;
+    int grid_, mgs_grid_ = 0;
+    int cap_ = 0;  // basis capacity (vectors)
     GmresState* st_ = nullptr;
-    DevBuf<double> partials_;
-    DevBuf<unsigned> ticket_;
-    DevBuf<double> V_, w_, t1_, t2_, hist_, arr_, ycoef_;
+    DevBuf<double> partials_, mparts_;
+    DevBuf<unsigned> ticket_, mbar_;
+    DevBuf<double> V_, w_, t1_, t2_, vcur_, hist_, h_, c_, cs_, sn_, g_, R_, ycoef_;
     DevBuf<GmresState> st_buf_;
     static constexpr int kLook = 2;  // Arnoldi steps kept queued ahead of the host's convergence check
     const Op* fused_ = nullptr;
     int* done_host_ = nullptr;       // pinned, host-mapped copy of the device `done` flag
     int* done_hmap_ = nullptr;       // its device alias
     cudaEvent_t iter_ev_[kLook] = {};
+    // device-driven solve: the captured graph and what it was captured for
+    cudaGraphExec_t gexec_ = nullptr;
+    cudaGraph_t graph_ = nullptr;
+    std::vector<long long> gkey_;
+    long long glaunch_[4] = {};  // kernel/memcpy launches captured in the top graph, a cycle, a step, a residual
 };
 
 }  // namespace fib

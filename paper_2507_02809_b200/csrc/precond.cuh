@@ -10,6 +10,7 @@ struct HodlrData;
 
 struct fi_precond {
     fi_system* sys = nullptr;
+    unsigned long long uid = 0;  // unique per preconditioner built (keys the captured GMRES graph)
     int nb = 0;        // 64-row blocks per level (Np / 64)
     long long T = 0;   // lower-triangular 64x64 tiles per level: nb (nb + 1) / 2
     int G = 0;         // persistent CTAs of the apply kernel
