@@ -137,6 +137,11 @@ int fi_precond_apply_host(fi_precond* P, const double* z_host, double* y_host);
  * above their tolerance, out[2] most CG steps of one block solve, out[3] preconditioner applies.  All zero
  * for dense blocks.  Synchronises the context's stream; reset != 0 zeroes the counters after reading. */
 int fi_precond_stats(fi_precond* P, long long out[4], int reset);
+/* The build's a-posteriori check of HODLR-compressed inverses (fi_precond_form == 2), worst over levels and
+ * 4 probe vectors x: out[0] forward error |W x - H x| / |W x| against the uncompressed inverse W, out[1]
+ * normwise backward error |M y - x| / (|M| |y| + |x|) of y = H x in the block matrix M itself.  A level that
+ * fails either bound (1e-12, 1e-13) rebuilds the preconditioner with packed tiles; zeros otherwise. */
+int fi_precond_build_check(const fi_precond* P, double out[2]);
 /* Device memory held by the preconditioner's per-level inverses (bytes). */
 long long fi_precond_bytes(const fi_precond* P);
 /* refine == 0 (default for dense blocks): one FP64 sweep over the polished inverses (built to the

@@ -91,6 +91,7 @@ _SIGS = {
     "fi_precond_apply_timed": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, ctypes.c_int, c_double_p]),
     "fi_precond_bytes": (ctypes.c_longlong, [c_void_p]),
     "fi_precond_stats": (ctypes.c_int, [c_void_p, ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]),
+    "fi_precond_build_check": (ctypes.c_int, [c_void_p, ctypes.POINTER(ctypes.c_double)]),
     "fi_precond_set_refine": (ctypes.c_int, [c_void_p, ctypes.c_int]),
     "fi_precond_create_ex": (ctypes.c_int, [c_void_p, ctypes.c_longlong, ctypes.c_int, ctypes.c_double, ctypes.c_int,
                                              ctypes.POINTER(c_void_p)]),

@@ -432,6 +432,14 @@ int fi_precond_apply_host(fi_precond* P, const double* z_host, double* y_host) {
     });
 }
 
+int fi_precond_build_check(const fi_precond* P, double out[2]) {
+    return guard([&] {
+        require(P && out, FI_E_DOMAIN, "fi_precond_build_check: NULL argument");
+        out[0] = P->hodlr_check_fwd;
+        out[1] = P->hodlr_check_bwd;
+    });
+}
+
 int fi_precond_stats(fi_precond* P, long long out[4], int reset) {
     return guard([&] {
         require(P && out, FI_E_DOMAIN, "fi_precond_stats: NULL argument");

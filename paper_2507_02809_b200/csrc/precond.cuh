@@ -17,6 +17,7 @@ struct fi_precond {
     int levels = 0;    // S + 1
     int refine = 1;    // one iterative-refinement sweep per apply (0 by default once the inverses are polished)
     fib::HodlrData* hodlr = nullptr;  // dense blocks in HODLR form (precond_hodlr.cu), else packed tiles
+    double hodlr_check_fwd = 0.0, hodlr_check_bwd = 0.0;  // the build's a-posteriori HODLR check (worst level)
     fib::DevBuf<double> H;      // [level][tile][64*64]: packed symmetric inverses
     fib::DevBuf<float> Hf;      // FP32 copy for the refinement sweep
     fib::DevBuf<double> rbuf, dbuf;  // refinement residual and correction
@@ -78,7 +79,8 @@ void hodlr_destroy(HodlrData* h);
 size_t hodlr_bytes(const HodlrData* h);
 size_t hodlr_work_doubles(const Layout& L, int nbt);
 void hodlr_compress(fi_ctx* ctx, HodlrData* h, const Layout& L, const double* W, int nbt, int l0, double* work);
-double hodlr_check(fi_ctx* ctx, HodlrData* h, const Layout& L, const double* W, int nbt, int l0, double* work);
+double hodlr_check(fi_ctx* ctx, HodlrData* h, const Layout& L, const double* W, int nbt, int l0, double* work,
+                   const OperatorView& op, const double* diag, const double* bscale, double* backward);
 void hodlr_sweep(fi_ctx* ctx, HodlrData* h, const fi_system* sys, const double* d2inv, const double* z, double* y,
                  int levels, const int* skip);
 // merged sweep: forward substitution + one refinement step in one persistent kernel (K2)

@@ -19,6 +19,9 @@ namespace {
 
 constexpr int TB = 64;            // tile edge
 constexpr int TILE = TB * TB;     // doubles per tile
+// HODLR acceptance: the normwise backward error |M y - x| / (|M| |y| + |x|) of y = H_hodlr x in the block
+// matrix itself (an LU solve reaches ~1e-16; the rank-32 truncation is accepted up to this)
+constexpr double kHodlrBackwardTol = 1e-13;
 
 __device__ __forceinline__ void tile_coords(long long t, int& bi, int& bj) {
     // lower-triangular row-major order: t = bi (bi + 1) / 2 + bj, bj <= bi
@@ -316,6 +319,7 @@ void precond_build(fi_precond* P) {
     // One pass over all levels; the HODLR pass checks every batch a posteriori (probe vector,
     // |H x - H_hodlr x| <= 1e-12 |H x|) and, if the rank does not suffice, the build restarts with
     // packed tiles.
+    double check_fwd = 0.0, check_bwd = 0.0;
     auto build_pass = [&](bool hodlr) -> bool {
         DevBuf<double> hwork;
         if (hodlr) {
@@ -367,15 +371,24 @@ void precond_build(fi_precond* P) {
                 throw Error(FI_E_SINGULAR,
                             "precond_build: singular block at time level " + std::to_string(first_singular),
                             first_singular);
-            if (hodlr && hodlr_check(ctx, P->hodlr, L, W.p, nbt, (int)l0, hwork.p) > 1e-12) {
-                hodlr_destroy(P->hodlr);
-                P->hodlr = nullptr;
-                return false;
+            if (hodlr) {
+                double bwd = 0.0;
+                const double fwd = hodlr_check(ctx, P->hodlr, L, W.p, nbt, (int)l0, hwork.p, op, diag_d.p,
+                                               bscale_d.p, &bwd);
+                check_fwd = std::max(check_fwd, fwd);
+                check_bwd = std::max(check_bwd, bwd);
+                if (!(fwd <= 1e-12) || !(bwd <= kHodlrBackwardTol)) {
+                    hodlr_destroy(P->hodlr);
+                    P->hodlr = nullptr;
+                    return false;
+                }
             }
         }
         return true;
     };
     if (!(use_hodlr && build_pass(true))) build_pass(false);
+    P->hodlr_check_fwd = check_fwd;
+    P->hodlr_check_bwd = check_bwd;
 }
 
 }  // namespace fib

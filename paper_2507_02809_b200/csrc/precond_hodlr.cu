@@ -604,11 +604,14 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
 // fixed pseudo-random x; acc[level] += (|y_dense - y_hodlr|^2, |y_dense|^2).  Rank 32 is ample for
 // the 1D BASELINE blocks; where it is not (the build checks every batch), the preconditioner falls
 // back to packed tiles.
-__device__ __forceinline__ double probe(long long r, int n2, int ld2) {
-    return (int)(r % ld2) >= n2 ? 0.0 : omega(7, r, 3);
+// deterministic probe vectors q = 0 .. NPROBE-1 (zero on the pad rows)
+constexpr int NPROBE = 4;
+__device__ __forceinline__ double probe(long long r, int n2, int ld2, int q) {
+    return (int)(r % ld2) >= n2 ? 0.0 : omega(7 + q, r, 3);
 }
+// grid (Np / HR, nbt, NPROBE): the node projections V^T x / Q^T x of the compressed blocks
 __global__ void hodlr_check_proj(const double2* hd, long long Np, int n2, int ld2, Tree tr, double* pj) {
-    const int c = blockIdx.x, lvb = blockIdx.y, t = threadIdx.x;
+    const int c = blockIdx.x, lvb = blockIdx.y, q = blockIdx.z, t = threadIdx.x;
     const int i = t >> 3, p = t & 7;
     const long long r = (long long)c * HR + i;
     const int b = (int)(r / TB);
@@ -617,17 +620,19 @@ __global__ void hodlr_check_proj(const double2* hd, long long Np, int n2, int ld
     if (node < 0) return;
     const int side = tr.rb_side[d * tr.nb + b];
     const double2* o = hd + ((long long)lvb * (Np / HR) + c) * (RK / 2) * 256;
-    const double xv = probe(r, n2, ld2);
-    double* dst = pj + (((long long)lvb * tr.nnodes + node) * 2 + side) * RK;
+    const double xv = probe(r, n2, ld2, q);
+    double* dst = pj + ((((long long)lvb * NPROBE + q) * tr.nnodes + node) * 2 + side) * RK;
     for (int k2 = 0; k2 < RK / 2; ++k2) {
         const double2 v = o[hd_index(i, p, k2)];
         atomicAdd(dst + 2 * k2, v.x * xv);
         atomicAdd(dst + 2 * k2 + 1, v.y * xv);
     }
 }
+// y = H_hodlr x (written to ybuf) and the forward error against the uncompressed inverse W:
+// acc[(lvb, q)] += (|W x - y|^2, |W x|^2)
 __global__ void hodlr_check_apply(const double* W, const double2* hd, long long Np, int n2, int ld2, Tree tr,
-                                  const double* pj, double* acc) {
-    const int c = blockIdx.x, lvb = blockIdx.y, t = threadIdx.x;
+                                  const double* pj, double* acc, double* ybuf) {
+    const int c = blockIdx.x, lvb = blockIdx.y, q = blockIdx.z, t = threadIdx.x;
     const int i = t >> 3, p = t & 7;
     const long long r = (long long)c * HR + i;
     const int b = (int)(r / TB);
@@ -639,11 +644,11 @@ __global__ void hodlr_check_apply(const double* W, const double2* hd, long long 
         for (int k2 = 0; k2 < RK / 2; ++k2) {
             const double2 v = o[hd_index(i, p, k2)];
             const long long c0 = (long long)b * TB + 32 * p + 2 * k2;
-            yh += v.x * probe(c0, n2, ld2) + v.y * probe(c0 + 1, n2, ld2);
+            yh += v.x * probe(c0, n2, ld2, q) + v.y * probe(c0 + 1, n2, ld2, q);
         }
     } else if (p - 1 <= tr.D && tr.rb_node[(p - 1) * tr.nb + b] >= 0) {
         const int d = p - 1, node = tr.rb_node[d * tr.nb + b], side = tr.rb_side[d * tr.nb + b];
-        const double* tv = pj + (((long long)lvb * tr.nnodes + node) * 2 + (1 - side)) * RK;
+        const double* tv = pj + ((((long long)lvb * NPROBE + q) * tr.nnodes + node) * 2 + (1 - side)) * RK;
         for (int k2 = 0; k2 < RK / 2; ++k2) {
             const double2 v = o[hd_index(i, p, k2)];
             yh += v.x * tv[2 * k2] + v.y * tv[2 * k2 + 1];
@@ -651,14 +656,55 @@ __global__ void hodlr_check_apply(const double* W, const double2* hd, long long 
     }
     if (!prow)
         for (long long col = p; col < Np; col += HPART)
-            if ((int)(col % ld2) < n2) yd += Wb[r * Np + col] * probe(col, n2, ld2);
+            if ((int)(col % ld2) < n2) yd += Wb[r * Np + col] * probe(col, n2, ld2, q);
     for (int off = 1; off < HPART; off <<= 1) {
         yh += __shfl_xor_sync(0xffffffffu, yh, off);
         yd += __shfl_xor_sync(0xffffffffu, yd, off);
     }
+    if (p == 0) {
+        ybuf[((long long)lvb * NPROBE + q) * Np + r] = prow ? 0.0 : yh;
+        if (!prow) {
+            atomicAdd(acc + 2 * (lvb * NPROBE + q), (yd - yh) * (yd - yh));
+            atomicAdd(acc + 2 * (lvb * NPROBE + q) + 1, yd * yd);
+        }
+    }
+}
+// The independent check: the residual of y = H_hodlr x in the block system itself,
+// M_L y - x with M_L = bscale_L B + diag(e0 D1 / D2) (the matrix the inverse was built from, gj_fill), and
+// the row sums of |M_L| (an upper bound of its 2-norm).  racc[(lvb, q)] += (|M y - x|^2, |y|^2, |x|^2);
+// mnorm[lvb] = max row sum (atomicMax on the bits of a non-negative double).
+__global__ void hodlr_check_residual(OperatorView op, const double* ybuf, const double* diag, const double* bscale,
+                                     int l0, double* racc, unsigned long long* mnorm) {
+    const long long Np = op.Np;
+    const int c = blockIdx.x, lvb = blockIdx.y, q = blockIdx.z, t = threadIdx.x;
+    const int i = t >> 3, p = t & 7;
+    const long long r = (long long)c * HR + i;
+    const int L = l0 + lvb;
+    const int n1 = op.n1, n2 = op.n2, ld2 = op.ld2;
+    const int r1 = (int)(r / ld2), r2 = (int)(r % ld2);
+    const bool prow = r2 >= n2;
+    const double scale = bscale[L];
+    const double* y = ybuf + ((long long)lvb * NPROBE + q) * Np;
+    double my = 0.0, rowabs = 0.0;
+    if (!prow)
+        for (long long col = p; col < Np; col += HPART) {
+            const int c1 = (int)(col / ld2), c2 = (int)(col % ld2);
+            if (c2 >= n2) continue;
+            double m = scale * op.gen[(long long)(r1 - c1 + n1 - 1) * op.gen_stride + (r2 - c2) + ld2];
+            if (col == r && L < op.S) m += diag[(long long)L * Np + r];
+            my += m * y[col];
+            rowabs += fabs(m);
+        }
+    for (int off = 1; off < HPART; off <<= 1) {
+        my += __shfl_xor_sync(0xffffffffu, my, off);
+        rowabs += __shfl_xor_sync(0xffffffffu, rowabs, off);
+    }
     if (p == 0 && !prow) {
-        atomicAdd(acc + 2 * lvb, (yd - yh) * (yd - yh));
-        atomicAdd(acc + 2 * lvb + 1, yd * yd);
+        const double xv = probe(r, n2, ld2, q), res = my - xv;
+        atomicAdd(racc + 3 * (lvb * NPROBE + q), res * res);
+        atomicAdd(racc + 3 * (lvb * NPROBE + q) + 1, y[r] * y[r]);
+        atomicAdd(racc + 3 * (lvb * NPROBE + q) + 2, xv * xv);
+        if (q == 0) atomicMax(mnorm + lvb, (unsigned long long)__double_as_longlong(rowabs));
     }
 }
 
@@ -769,27 +815,49 @@ void hodlr_compress(fi_ctx* ctx, HodlrData* h, const Layout& L, const double* W,
     FI_LAUNCHED(ctx);
 }
 
-size_t hodlr_work_doubles(const Layout& L, int nbt) { return (size_t)nbt * (DMAX + 1) * L.Np * RK; }
+size_t hodlr_work_doubles(const Layout& L, int nbt) {
+    // the compression's work, and the check's (projections, accumulators, the probe products)
+    return std::max((size_t)nbt * (DMAX + 1) * L.Np * RK,
+                    (size_t)nbt * NPROBE * (2 * (L.Np / TB) * 2 * RK + L.Np + 6) + nbt + 16);
+}
 
-// Largest relative error |H x - H_hodlr x| / |H x| over the batch's levels (probe vector x).
-double hodlr_check(fi_ctx* ctx, HodlrData* h, const Layout& L, const double* W, int nbt, int l0, double* work) {
+// A-posteriori check of the compressed inverses of a batch, NPROBE probe vectors x per level:
+//  * forward error |W x - H_hodlr x| / |W x| against the uncompressed inverse W (the truncation error);
+//  * normwise backward error |M y - x| / (|M| |y| + |x|) of y = H_hodlr x in the block matrix M itself
+//    (independent of W: it also catches an inaccurate W).
+// Returns the worst forward error; *backward receives the worst backward error.
+double hodlr_check(fi_ctx* ctx, HodlrData* h, const Layout& L, const double* W, int nbt, int l0, double* work,
+                   const OperatorView& op, const double* diag, const double* bscale, double* backward) {
     const long long Np = L.Np;
     const Tree tr = h->tree();
     const double2* hd = h->hd.p + (size_t)l0 * (Np / HR) * (RK / 2) * 256;
-    double* pj = work;                                          // nbt x nnodes x 2 x RK
-    double* acc = work + (size_t)nbt * h->nnodes * 2 * RK;      // nbt x 2
-    FI_CUDA(cudaMemsetAsync(work, 0, ((size_t)nbt * h->nnodes * 2 * RK + 2 * nbt) * sizeof(double), ctx->stream));
-    hodlr_check_proj<<<dim3((unsigned)(Np / HR), (unsigned)nbt), 256, 0, ctx->stream>>>(hd, Np, L.n2, L.ld2, tr, pj);
+    const size_t npj = (size_t)nbt * NPROBE * h->nnodes * 2 * RK;
+    double* pj = work;                                            // nbt x NPROBE x nnodes x 2 x RK
+    double* acc = pj + npj;                                       // nbt x NPROBE x 2
+    double* racc = acc + (size_t)2 * nbt * NPROBE;                // nbt x NPROBE x 3
+    unsigned long long* mnorm = reinterpret_cast<unsigned long long*>(racc + (size_t)3 * nbt * NPROBE);  // nbt
+    double* ybuf = racc + (size_t)3 * nbt * NPROBE + nbt;         // nbt x NPROBE x Np
+    FI_CUDA(cudaMemsetAsync(work, 0, (npj + (size_t)6 * nbt * NPROBE + nbt) * sizeof(double), ctx->stream));
+    const dim3 grid((unsigned)(Np / HR), (unsigned)nbt, NPROBE);
+    hodlr_check_proj<<<grid, 256, 0, ctx->stream>>>(hd, Np, L.n2, L.ld2, tr, pj);
     FI_LAUNCHED(ctx);
-    hodlr_check_apply<<<dim3((unsigned)(Np / HR), (unsigned)nbt), 256, 0, ctx->stream>>>(W, hd, Np, L.n2, L.ld2, tr,
-                                                                                        pj, acc);
+    hodlr_check_apply<<<grid, 256, 0, ctx->stream>>>(W, hd, Np, L.n2, L.ld2, tr, pj, acc, ybuf);
     FI_LAUNCHED(ctx);
-    std::vector<double> hacc((size_t)2 * nbt);
+    hodlr_check_residual<<<grid, 256, 0, ctx->stream>>>(op, ybuf, diag, bscale, l0, racc, mnorm);
+    FI_LAUNCHED(ctx);
+    std::vector<double> hacc((size_t)5 * nbt * NPROBE + nbt);
     FI_CUDA(cudaMemcpyAsync(hacc.data(), acc, hacc.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     FI_CUDA(cudaStreamSynchronize(ctx->stream));
-    double worst = 0.0;
-    for (int q = 0; q < nbt; ++q)
-        worst = std::max(worst, hacc[(size_t)2 * q + 1] > 0 ? std::sqrt(hacc[(size_t)2 * q] / hacc[(size_t)2 * q + 1]) : 0.0);
+    double worst = 0.0, worst_b = 0.0;
+    const double* ra = hacc.data() + (size_t)2 * nbt * NPROBE;
+    const double* mn = ra + (size_t)3 * nbt * NPROBE;
+    for (int lq = 0; lq < nbt * NPROBE; ++lq) {
+        if (hacc[(size_t)2 * lq + 1] > 0) worst = std::max(worst, std::sqrt(hacc[(size_t)2 * lq] / hacc[(size_t)2 * lq + 1]));
+        const double mnorm_l = mn[lq / NPROBE];
+        const double den = mnorm_l * std::sqrt(ra[(size_t)3 * lq + 1]) + std::sqrt(ra[(size_t)3 * lq + 2]);
+        if (den > 0) worst_b = std::max(worst_b, std::sqrt(ra[(size_t)3 * lq]) / den);
+    }
+    if (backward) *backward = worst_b;
     return worst;
 }
 

@@ -491,6 +491,12 @@ class BlockTriangularPreconditioner:
     def device_bytes(self) -> int:
         return int(lib.fi_precond_bytes(self.handle))
 
+    def build_check(self) -> dict:
+        """The build's a-posteriori check of HODLR-compressed inverses (fi_precond_build_check)."""
+        out = (ctypes.c_double * 2)()
+        _check(lib.fi_precond_build_check(self.handle, out))
+        return {"forward": out[0], "backward": out[1]}
+
     def stats(self, reset: bool = False) -> dict:
         """tau-PCG inner-solve counters since the last reset (fi_precond_stats; zeros for dense blocks)."""
         out = (ctypes.c_longlong * 4)()

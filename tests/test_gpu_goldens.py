@@ -59,3 +59,16 @@ def test_split_apply_matches_operator_then_precond(cfg):
     assert r1.iterations == r2.iterations
     assert np.allclose(r1.residual_history, r2.residual_history, rtol=1e-6, atol=1e-15)
     assert _rel(x1, x2) <= 1e-10
+
+
+def test_full_gmres_reference_defaults_grow_the_basis():
+    """maxit = 0, restart = 0 are the reference's defaults (krylov.hpp:54-57): full GMRES with maxit = n.
+    For config 1 (n = 2.1M) a basis of n + 1 vectors up front would be 35 TB; the basis grows on demand
+    and the solve converges in the same iterations as GMRES(50) (fewer than 50 steps)."""
+    g = np.load(os.path.join(GOLDEN, "oracle_config1.npz"))
+    A = F.SystemOperator(baseline_problem(F, 1))
+    P = F.BlockTriangularPreconditioner(A)
+    z = F.build_rhs(A, g["mu_eps"]).z
+    x, rep = F.gmres(A, P, z, F.GmresOptions(TOL[1], 0, 0))
+    assert rep.converged and abs(rep.iterations - int(g["iterations"])) <= 1
+    assert _rel(x[-A.N:], g["f"]) <= 1e-8
