@@ -21,6 +21,10 @@
 
 #include "precond.cuh"
 
+#ifndef FI_FFT_R8
+#define FI_FFT_R8 1  // radix-8 transform groups (L/8 threads); 0: radix-4 (L/4 threads), measured 7-9% slower
+#endif
+
 namespace fib {
 namespace {
 
@@ -195,6 +199,99 @@ __device__ __forceinline__ int pad8(int i) { return i + (i >> 3); }
 // to constants.  tw: the full table exp(-2 pi i k / L), k < L.  Every thread of the CTA must call it (it
 // contains __syncthreads); groups without a unit pass active = false.  Not inlined: one copy per length
 // and direction serves every pass (instruction cache).
+#if FI_FFT_R8
+// radix-8 variant: L/8 threads per transform, one radix-2 or radix-4 pass first when LG % 3 != 0
+__device__ __forceinline__ void dft8(double2 (&v)[8], bool inv) {
+    constexpr double r = 0.70710678118654752440;
+    double2 b[8];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        b[m] = cadd(v[m], v[m + 4]);
+        b[m + 4] = csub(v[m], v[m + 4]);
+    }
+    if (!inv) {
+        b[5] = make_double2(r * (b[5].x + b[5].y), r * (b[5].y - b[5].x));
+        b[7] = make_double2(r * (b[7].y - b[7].x), -r * (b[7].x + b[7].y));
+    } else {
+        b[5] = make_double2(r * (b[5].x - b[5].y), r * (b[5].x + b[5].y));
+        b[7] = make_double2(-r * (b[7].x + b[7].y), r * (b[7].x - b[7].y));
+    }
+    b[6] = mul_i(b[6], inv);
+    const double2 c0 = cadd(b[0], b[2]), c2 = csub(b[0], b[2]), c1 = cadd(b[1], b[3]), c3 = mul_i(csub(b[1], b[3]), inv);
+    const double2 c4 = cadd(b[4], b[6]), c6 = csub(b[4], b[6]), c5 = cadd(b[5], b[7]), c7 = mul_i(csub(b[5], b[7]), inv);
+    v[0] = cadd(c0, c1);
+    v[4] = csub(c0, c1);
+    v[2] = cadd(c2, c3);
+    v[6] = csub(c2, c3);
+    v[1] = cadd(c4, c5);
+    v[5] = csub(c4, c5);
+    v[3] = cadd(c6, c7);
+    v[7] = csub(c6, c7);
+}
+template <int LG, bool INV>
+__device__ __noinline__ void fft_group(double2* src, double2* dst, const double2* tw, int t, bool active) {
+    constexpr int L = 1 << LG, NT = (L >> 3) > 0 ? (L >> 3) : 1, REM = LG % 3;
+    int p = 1;
+    if constexpr (REM == 1) {
+        if (active)
+            for (int j = t; j < (L >> 1); j += NT) {
+                const double2 x0 = src[pad8(j)], x1 = src[pad8(j + (L >> 1))];
+                dst[pad8(2 * j)] = cadd(x0, x1);
+                dst[pad8(2 * j + 1)] = csub(x0, x1);
+            }
+        __syncthreads();
+        double2* tt = src;
+        src = dst;
+        dst = tt;
+        p = 2;
+    } else if constexpr (REM == 2) {
+        constexpr int Q = L >> 2;
+        if (active)
+            for (int j = t; j < Q; j += NT) {
+                const double2 a0 = src[pad8(j)], a1 = src[pad8(j + Q)], a2 = src[pad8(j + 2 * Q)], a3 = src[pad8(j + 3 * Q)];
+                const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = mul_i(csub(a1, a3), INV);
+                dst[pad8(4 * j)] = cadd(s02, s13);
+                dst[pad8(4 * j + 1)] = cadd(d02, d13);
+                dst[pad8(4 * j + 2)] = csub(s02, s13);
+                dst[pad8(4 * j + 3)] = csub(d02, d13);
+            }
+        __syncthreads();
+        double2* tt = src;
+        src = dst;
+        dst = tt;
+        p = 4;
+    }
+    constexpr int Q8 = L >> 3;
+#pragma unroll
+    for (int s = REM; s < LG; s += 3) {
+        p = 1 << s;
+        if (active && Q8 > 0) {
+            const int j = t, k = j & (p - 1);
+            double2 v[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) v[m] = src[pad8(j + m * Q8)];
+            if (p > 1) {
+                const int ts = k << (LG - s - 3);  // k L / (8 p)
+#pragma unroll
+                for (int m = 1; m < 8; ++m) {
+                    double2 w = tw[m * ts];
+                    if (INV) w.y = -w.y;
+                    v[m] = make_double2(v[m].x * w.x - v[m].y * w.y, v[m].x * w.y + v[m].y * w.x);
+                }
+            }
+            dft8(v, INV);
+            const int o = 8 * (j - k) + k;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) dst[pad8(o + m * p)] = v[m];
+        }
+        __syncthreads();
+        double2* tt = src;
+        src = dst;
+        dst = tt;
+    }
+}
+constexpr int kFftRadix = 8;
+#else
 template <int LG, bool INV>
 __device__ __noinline__ void fft_group(double2* src, double2* dst, const double2* tw, int t, bool active) {
     constexpr int L = 1 << LG, Q = L >> 2;
@@ -242,6 +339,8 @@ __device__ __noinline__ void fft_group(double2* src, double2* dst, const double2
         dst = tt;
     }
 }
+constexpr int kFftRadix = 4;
+#endif
 // runtime dispatch on the transform length; returns the buffer index (0 = src) holding the output
 __device__ __forceinline__ int fft_dispatch(double2* src, double2* dst, int lg, const double2* tw, bool inv, int t,
                                             bool active) {
@@ -263,7 +362,7 @@ __device__ __forceinline__ int fft_dispatch(double2* src, double2* dst, int lg, 
         default: __trap();
     }
 #undef FI_FFT_CASE
-    return ((lg + 1) / 2) & 1;
+    return kFftRadix == 4 ? ((lg + 1) / 2) & 1 : ((lg / 3) + (lg % 3 ? 1 : 0)) & 1;
 }
 
 __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
@@ -369,8 +468,8 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
         tws2[t] = t < L2 / 2 ? a.tw2[t] : make_double2(-a.tw2[t - L2 / 2].x, -a.tw2[t - L2 / 2].y);
     __syncthreads();
     // group geometry of the row (length L2) and column (length L1) passes
-    const int ntR = max(L2 >> 2, 1), ngR = FT / ntR, gR = tid / ntR, tR = tid % ntR;
-    const int ntC = max(L1 >> 2, 1), ngC = FT / ntC, gC = tid / ntC, tC = tid % ntC;
+    const int ntR = max(kFftRadix == 4 ? L2 >> 2 : L2 >> 3, 1), ngR = FT / ntR, gR = tid / ntR, tR = tid % ntR;
+    const int ntC = max(kFftRadix == 4 ? L1 >> 2 : L1 >> 3, 1), ngC = FT / ntC, gC = tid / ntC, tC = tid % ntC;
     const int ngR_ = ngR, ngC_ = ngC;
     const int PLR = pad8(L2) + 1, PLC = pad8(L1) + 1;  // padded buffer lengths
     // the row pairs of a row pass are the same in every row pass: the CTA's rows of r, z, p, x and delta
@@ -405,7 +504,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
         const bool act = cta + G * (gC + ngC * rd) < nunits;
         return w ^ fft_dispatch(cbuf(gC, w), cbuf(gC, 1 - w), a.lg1, tws1, inv, tC, act);
     };
-    constexpr int UF = 4;  // element-loop unroll: na * L / FT <= 4 always (na <= ng = 4 FT / L)
+    constexpr int UF = 4;  // element-loop unroll: the loads of UF elements per thread are in flight together
     // odd extension of a length-n sequence to L = 2(n + 1): position j holds sg * v[jj]
     auto oext = [](int j, int n, int L, int& jj, double& sg) {
         const bool lo = j >= 1 && j <= n, hi = j >= n + 2;
@@ -423,24 +522,26 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     // fill buffer 0 of the active row slots with the odd extensions of rows i0, i1 of src (stride sstride)
     auto fill_dst_rows = [&](const double* src, long long sstride, int rd) {
         const int lim = nact(nuR, ngR, rd) * L2;
-        double2 v[UF];
+        for (int base = 0; base < lim; base += UF * FT) {
+            double2 v[UF];
 #pragma unroll
-        for (int q = 0; q < UF; ++q) {
-            const int e = tid + q * FT;
-            const bool ok = e < lim;
-            const int ec = ok ? e : 0, s = ec >> a.lg2, j = ec & (L2 - 1);
-            int i0c, i1c, jj;
-            bool ok0, ok1;
-            double sg;
-            rowpair(s, rd, i0c, i1c, ok0, ok1);
-            oext(j, n2, L2, jj, sg);
-            const double x0 = src[(long long)i0c * sstride + jj], x1 = src[(long long)i1c * sstride + jj];
-            v[q] = make_double2(ok && ok0 ? sg * x0 : 0.0, ok && ok1 ? sg * x1 : 0.0);
-        }
+            for (int q = 0; q < UF; ++q) {
+                const int e = base + tid + q * FT;
+                const bool ok = e < lim;
+                const int ec = ok ? e : 0, s = ec >> a.lg2, j = ec & (L2 - 1);
+                int i0c, i1c, jj;
+                bool ok0, ok1;
+                double sg;
+                rowpair(s, rd, i0c, i1c, ok0, ok1);
+                oext(j, n2, L2, jj, sg);
+                const double x0 = src[(long long)i0c * sstride + jj], x1 = src[(long long)i1c * sstride + jj];
+                v[q] = make_double2(ok && ok0 ? sg * x0 : 0.0, ok && ok1 ? sg * x1 : 0.0);
+            }
 #pragma unroll
-        for (int q = 0; q < UF; ++q) {
-            const int e = tid + q * FT;
-            if (e < lim) rbuf(e >> a.lg2, 0)[pad8(e & (L2 - 1))] = v[q];
+            for (int q = 0; q < UF; ++q) {
+                const int e = base + tid + q * FT;
+                if (e < lim) rbuf(e >> a.lg2, 0)[pad8(e & (L2 - 1))] = v[q];
+            }
         }
         __syncthreads();
     };
@@ -637,52 +738,56 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
         double pbp = 0.0;
         for (int rd = 0; rd < rdB; ++rd) {
             const int lim = nact(nuB, ngC, rd) * L1;
-            double2 v[UF];
+            for (int base = 0; base < lim; base += UF * FT) {
+                double2 v[UF];
 #pragma unroll
-            for (int q = 0; q < UF; ++q) {
-                const int e = tid + q * FT;
-                const bool ok = e < lim;
-                const int ec = ok ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
-                const int kc = min(cta + G * (s + ngC * rd), H2 - 1);
-                const long long o = (long long)min(j, n1 - 1) * H2 + kc;
-                double2 zv = a.Zh[o];
-                if (beta != 0.0) {
-                    const double2 xp = a.Xp[o];
-                    zv.x += beta * xp.x;
-                    zv.y += beta * xp.y;
+                for (int q = 0; q < UF; ++q) {
+                    const int e = base + tid + q * FT;
+                    const bool ok = e < lim;
+                    const int ec = ok ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
+                    const int kc = min(cta + G * (s + ngC * rd), H2 - 1);
+                    const long long o = (long long)min(j, n1 - 1) * H2 + kc;
+                    double2 zv = a.Zh[o];
+                    if (beta != 0.0) {
+                        const double2 xp = a.Xp[o];
+                        zv.x += beta * xp.x;
+                        zv.y += beta * xp.y;
+                    }
+                    v[q] = ok && j < n1 ? zv : make_double2(0.0, 0.0);
                 }
-                v[q] = ok && j < n1 ? zv : make_double2(0.0, 0.0);
-            }
 #pragma unroll
-            for (int q = 0; q < UF; ++q) {
-                const int e = tid + q * FT;
-                if (e < lim) {
-                    const int s = e >> a.lg1, j = e & (L1 - 1), k = cta + G * (s + ngC * rd);
-                    if (keep && j < n1) a.Xp[(long long)j * H2 + k] = v[q];
-                    cbuf(s, 0)[pad8(j)] = v[q];
+                for (int q = 0; q < UF; ++q) {
+                    const int e = base + tid + q * FT;
+                    if (e < lim) {
+                        const int s = e >> a.lg1, j = e & (L1 - 1), k = cta + G * (s + ngC * rd);
+                        if (keep && j < n1) a.Xp[(long long)j * H2 + k] = v[q];
+                        cbuf(s, 0)[pad8(j)] = v[q];
+                    }
                 }
             }
             sub(23);
             __syncthreads();
             const int w = fftC(0, false, rd, nuB);
             sub(24);
-            double lam[UF];
+            for (int base = 0; base < lim; base += UF * FT) {
+                double lam[UF];
 #pragma unroll
-            for (int q = 0; q < UF; ++q) {
-                const int e = tid + q * FT;
-                const int ec = e < lim ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
-                lam[q] = a.lamB[(long long)j * L2 + min(cta + G * (s + ngC * rd), H2 - 1)];
-            }
+                for (int q = 0; q < UF; ++q) {
+                    const int e = base + tid + q * FT;
+                    const int ec = e < lim ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
+                    lam[q] = a.lamB[(long long)j * L2 + min(cta + G * (s + ngC * rd), H2 - 1)];
+                }
 #pragma unroll
-            for (int q = 0; q < UF; ++q) {
-                const int e = tid + q * FT;
-                if (e < lim) {
-                    const int s = e >> a.lg1, j = e & (L1 - 1), k = cta + G * (s + ngC * rd);
-                    const double wk = (k == 0 || k == L2 / 2) ? 1.0 : 2.0;
-                    double2* cell = cbuf(s, w) + pad8(j);
-                    const double2 cv = *cell;
-                    pbp += wk * lam[q] * (cv.x * cv.x + cv.y * cv.y);
-                    *cell = make_double2(cv.x * lam[q], cv.y * lam[q]);
+                for (int q = 0; q < UF; ++q) {
+                    const int e = base + tid + q * FT;
+                    if (e < lim) {
+                        const int s = e >> a.lg1, j = e & (L1 - 1), k = cta + G * (s + ngC * rd);
+                        const double wk = (k == 0 || k == L2 / 2) ? 1.0 : 2.0;
+                        double2* cell = cbuf(s, w) + pad8(j);
+                        const double2 cv = *cell;
+                        pbp += wk * lam[q] * (cv.x * cv.x + cv.y * cv.y);
+                        *cell = make_double2(cv.x * lam[q], cv.y * lam[q]);
+                    }
                 }
             }
             sub(25);
@@ -706,34 +811,36 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
         double part = 0.0;
         for (int rd = 0; rd < rdR; ++rd) {
             const int lim = nact(nuR, ngR, rd) * L2;
-            double2 v[UF];
+            for (int base = 0; base < lim; base += UF * FT) {
+                double2 v[UF];
 #pragma unroll
-            for (int q = 0; q < UF; ++q) {
-                // packed spectrum D = Y0 + i Y1 of the row pair from the two Hermitian half spectra
-                const int e = tid + q * FT;
-                const bool ok = e < lim;
-                const int ec = ok ? e : 0, s = ec >> a.lg2, k = ec & (L2 - 1);
-                int i0c, i1c;
-                bool ok0, ok1;
-                rowpair(s, rd, i0c, i1c, ok0, ok1);
-                const int kk = k <= L2 / 2 ? k : L2 - k;
-                double2 y0 = a.Yb[(long long)i0c * H2 + kk];
-                double2 y1 = a.Yb[(long long)i1c * H2 + kk];
-                if (!ok1) y1 = make_double2(0.0, 0.0);
-                if (kk == 0 || kk == L2 / 2) {
-                    y0.y = 0.0;
-                    y1.y = 0.0;
+                for (int q = 0; q < UF; ++q) {
+                    // packed spectrum D = Y0 + i Y1 of the row pair from the two Hermitian half spectra
+                    const int e = base + tid + q * FT;
+                    const bool ok = e < lim;
+                    const int ec = ok ? e : 0, s = ec >> a.lg2, k = ec & (L2 - 1);
+                    int i0c, i1c;
+                    bool ok0, ok1;
+                    rowpair(s, rd, i0c, i1c, ok0, ok1);
+                    const int kk = k <= L2 / 2 ? k : L2 - k;
+                    double2 y0 = a.Yb[(long long)i0c * H2 + kk];
+                    double2 y1 = a.Yb[(long long)i1c * H2 + kk];
+                    if (!ok1) y1 = make_double2(0.0, 0.0);
+                    if (kk == 0 || kk == L2 / 2) {
+                        y0.y = 0.0;
+                        y1.y = 0.0;
+                    }
+                    if (k > L2 / 2) {
+                        y0.y = -y0.y;
+                        y1.y = -y1.y;
+                    }
+                    v[q] = make_double2(y0.x - y1.y, y0.y + y1.x);
                 }
-                if (k > L2 / 2) {
-                    y0.y = -y0.y;
-                    y1.y = -y1.y;
-                }
-                v[q] = make_double2(y0.x - y1.y, y0.y + y1.x);
-            }
 #pragma unroll
-            for (int q = 0; q < UF; ++q) {
-                const int e = tid + q * FT;
-                if (e < lim) rbuf(e >> a.lg2, 0)[pad8(e & (L2 - 1))] = v[q];
+                for (int q = 0; q < UF; ++q) {
+                    const int e = base + tid + q * FT;
+                    if (e < lim) rbuf(e >> a.lg2, 0)[pad8(e & (L2 - 1))] = v[q];
+                }
             }
             sub(10);
             __syncthreads();
@@ -822,58 +929,62 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
         const double c = level_c(a, lv), dmean = level_dmean(a, lv);
         for (int rd = 0; rd < rdT; ++rd) {
             const int lim = nact(nuT, ngC, rd) * L1;
-            double2 v[UF];
+            for (int base = 0; base < lim; base += UF * FT) {
+                double2 v[UF];
 #pragma unroll
-            for (int q = 0; q < UF; ++q) {
-                const int e = tid + q * FT;
-                const bool ok = e < lim;
-                const int ec = ok ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
-                const int k0 = 2 * (cta + G * (s + ngC * rd));
-                const int k0c = min(k0, n2 - 1), k1c = min(k0 + 1, n2 - 1);
-                int jj;
-                double sg;
-                oext(j, n1, L1, jj, sg);
-                const double x0 = a.Rr[(long long)jj * n2 + k0c], x1 = a.Rr[(long long)jj * n2 + k1c];
-                v[q] = make_double2(ok ? sg * x0 : 0.0, ok && k0 + 1 < n2 ? sg * x1 : 0.0);
-            }
+                for (int q = 0; q < UF; ++q) {
+                    const int e = base + tid + q * FT;
+                    const bool ok = e < lim;
+                    const int ec = ok ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
+                    const int k0 = 2 * (cta + G * (s + ngC * rd));
+                    const int k0c = min(k0, n2 - 1), k1c = min(k0 + 1, n2 - 1);
+                    int jj;
+                    double sg;
+                    oext(j, n1, L1, jj, sg);
+                    const double x0 = a.Rr[(long long)jj * n2 + k0c], x1 = a.Rr[(long long)jj * n2 + k1c];
+                    v[q] = make_double2(ok ? sg * x0 : 0.0, ok && k0 + 1 < n2 ? sg * x1 : 0.0);
+                }
 #pragma unroll
-            for (int q = 0; q < UF; ++q) {
-                const int e = tid + q * FT;
-                if (e < lim) cbuf(e >> a.lg1, 0)[pad8(e & (L1 - 1))] = v[q];
+                for (int q = 0; q < UF; ++q) {
+                    const int e = base + tid + q * FT;
+                    if (e < lim) cbuf(e >> a.lg1, 0)[pad8(e & (L1 - 1))] = v[q];
+                }
             }
             sub(14);
             __syncthreads();
             const int w = fftC(0, false, rd, nuT);
             sub(15);
-            double2 il[UF];
+            for (int base = 0; base < lim; base += UF * FT) {
+                double2 il[UF];
 #pragma unroll
-            for (int q = 0; q < UF; ++q) {
-                const int e = tid + q * FT;
-                const int ec = e < lim ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
-                const int k0 = 2 * (cta + G * (s + ngC * rd));
-                const int k0c = min(k0, n2 - 1), k1c = min(k0 + 1, n2 - 1);
-                const int kk = (j >= 1 && j <= n1) ? j : (j >= n1 + 2 ? L1 - j : 1);
-                il[q] = make_double2(a.lamT[(long long)(kk - 1) * n2 + k0c], a.lamT[(long long)(kk - 1) * n2 + k1c]);
-            }
+                for (int q = 0; q < UF; ++q) {
+                    const int e = base + tid + q * FT;
+                    const int ec = e < lim ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
+                    const int k0 = 2 * (cta + G * (s + ngC * rd));
+                    const int k0c = min(k0, n2 - 1), k1c = min(k0 + 1, n2 - 1);
+                    const int kk = (j >= 1 && j <= n1) ? j : (j >= n1 + 2 ? L1 - j : 1);
+                    il[q] = make_double2(a.lamT[(long long)(kk - 1) * n2 + k0c], a.lamT[(long long)(kk - 1) * n2 + k1c]);
+                }
 #pragma unroll
-            for (int q = 0; q < UF; ++q) {
-                const int e = tid + q * FT;
-                if (e < lim) {
-                    const int s = e >> a.lg1, j = e & (L1 - 1), k0 = 2 * (cta + G * (s + ngC * rd));
-                    double x0 = 0.0, x1 = 0.0;
-                    int kk = -1;
-                    double sg = 1.0;
-                    if (j >= 1 && j <= n1) kk = j;
-                    else if (j >= n1 + 2) {
-                        kk = L1 - j;
-                        sg = -1.0;
+                for (int q = 0; q < UF; ++q) {
+                    const int e = base + tid + q * FT;
+                    if (e < lim) {
+                        const int s = e >> a.lg1, j = e & (L1 - 1), k0 = 2 * (cta + G * (s + ngC * rd));
+                        double x0 = 0.0, x1 = 0.0;
+                        int kk = -1;
+                        double sg = 1.0;
+                        if (j >= 1 && j <= n1) kk = j;
+                        else if (j >= n1 + 2) {
+                            kk = L1 - j;
+                            sg = -1.0;
+                        }
+                        if (kk > 0) {
+                            const double2 cv = cbuf(s, w)[pad8(kk)];
+                            x0 = sg * (sc1 * cv.y) / (c * il[q].x + dmean);
+                            if (k0 + 1 < n2) x1 = sg * (-sc1 * cv.x) / (c * il[q].y + dmean);
+                        }
+                        cbuf(s, 1 - w)[pad8(j)] = make_double2(x0, x1);
                     }
-                    if (kk > 0) {
-                        const double2 cv = cbuf(s, w)[pad8(kk)];
-                        x0 = sg * (sc1 * cv.y) / (c * il[q].x + dmean);
-                        if (k0 + 1 < n2) x1 = sg * (-sc1 * cv.x) / (c * il[q].y + dmean);
-                    }
-                    cbuf(s, 1 - w)[pad8(j)] = make_double2(x0, x1);
                 }
             }
             sub(16);
@@ -1215,7 +1326,7 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
     a.skip = skip;
     const int H2 = a.L2 / 2 + 1;
     const int plr = a.L2 + a.L2 / 8 + 1, plc = a.L1 + a.L1 / 8 + 1;
-    const int ngr = FT / std::max(a.L2 / 4, 1), ngc = FT / std::max(a.L1 / 4, 1);
+    const int ngr = FT / std::max(a.L2 / kFftRadix, 1), ngc = FT / std::max(a.L1 / kFftRadix, 1);
     const int nown = 1 + ((a.n1 + 1) / 2 - 1) / std::min(std::min(ctx->sm_count, std::max(std::max((a.n1 + 1) / 2,
                                                          (a.n2 + 1) / 2), H2)), 160);  // row pairs per CTA
     const size_t smem = ((size_t)a.L1 + a.L2 + std::max((size_t)ngr * 2 * plr, (size_t)ngc * 2 * plc)) *
