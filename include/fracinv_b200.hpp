@@ -10,6 +10,7 @@
 // the reference's stacked layout (block s at (s-1)*N, f last).
 #pragma once
 
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <functional>
@@ -44,6 +45,11 @@ class ConfigError : public std::runtime_error {
 public:
     using std::runtime_error::runtime_error;
 };
+// EXTENSION: a tau-PCG block solve stopped at maxit above its tolerance (FI_E_NOCONV)
+class NoConvergenceError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
 class CudaError : public std::runtime_error {
 public:
     using std::runtime_error::runtime_error;
@@ -58,6 +64,7 @@ inline void check(int rc) {
         case FI_E_SINGULAR: throw SingularBlockError(msg, fi_last_error_time_index());
         case FI_E_DOMAIN: throw std::domain_error(msg);
         case FI_E_CONFIG: throw ConfigError(msg);
+        case FI_E_NOCONV: throw NoConvergenceError(msg);
         default: throw CudaError(msg);
     }
 }
@@ -252,6 +259,19 @@ public:
         return y;
     }
     void apply_device(const double* z_dev, double* y_dev) const { check(fi_precond_apply(h_, z_dev, y_dev)); }
+    // tau-PCG inner-solve counters since the last reset: CG steps, block solves stopped at maxit, most steps
+    // of one block solve, applies (fi_precond_stats)
+    std::array<long long, 4> stats(bool reset = false) const {
+        std::array<long long, 4> out{};
+        check(fi_precond_stats(h_, out.data(), reset ? 1 : 0));
+        return out;
+    }
+    // the build's HODLR check: forward error vs the uncompressed inverse, backward error in the block matrix
+    std::array<double, 2> build_check() const {
+        std::array<double, 2> out{};
+        check(fi_precond_build_check(h_, out.data()));
+        return out;
+    }
 
 private:
     const SystemOperator* A_;
@@ -291,6 +311,7 @@ struct SolveReport {
     bool breakdown = false;
     double wall_time_seconds = 0.0;
     double final_true_residual = 0.0;
+    int inner_nonconverged = 0;  // EXTENSION: tau-PCG block solves that stopped at maxit above tol
 };
 
 inline std::pair<std::vector<double>, SolveReport> gmres(const SystemOperator& A,
@@ -311,6 +332,7 @@ inline std::pair<std::vector<double>, SolveReport> gmres(const SystemOperator& A
     rep.breakdown = r.breakdown != 0;
     rep.wall_time_seconds = r.wall_time_seconds;
     rep.final_true_residual = r.final_true_residual;
+    rep.inner_nonconverged = r.inner_nonconverged;
     rep.residual_history.assign(hist.begin(), hist.begin() + std::min(r.history_len, cap));
     return {std::move(x), std::move(rep)};
 }
