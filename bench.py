@@ -477,12 +477,14 @@ def run_ours(args):
     op_flops = 2.0 * N * N * (S + 1)
     op_tflops = op_flops / (ms_op * 1e-3) / 1e12
     fp64_peak, fp64_src = load_fp64_peak()
-    mw, mx, my = (torch.from_numpy(np.random.default_rng(k).uniform(-1, 1, n)).to(b_dev.device) for k in (5, 6, 7))
-    assert lib.fi_mgs_round_timed(ctx.handle, n, mw.data_ptr(), mx.data_ptr(), my.data_ptr(), reps,
-                                  ctypes.byref(ms)) == 0
+    # K3/K4: one Arnoldi step's MGS + Givens kernel at k = iterations / 2 (mgs_step_kernel), L2 flushed before each
+    k_mgs = max(1, rep.iterations // 2)
+    reorth = ctypes.c_int()
+    assert lib.fi_mgs_step_timed(ctx.handle, n, k_mgs, reps, ctypes.byref(ms), ctypes.byref(reorth)) == 0, last_error()
     ms_mgs = ms.value
-    del mw, mx, my, y
-
+    # algorithmic bytes of MGS step k: 8 n (3 (k + 1) + 3), doubled when the second pass runs
+    mgs_bytes = 8 * n * (3 * (k_mgs + 1) + 3) * (2 if reorth.value else 1)
+    del y
     # max over ranks for times, sum over ranks for the work done (replicas)
     ms_total_max, iters_all = replica_aggregate(ms_total, total_iters, b_dev.device)
     ms_e2e_max, e_iters_all = replica_aggregate(ms_e2e, e_iters, b_dev.device)
@@ -558,11 +560,14 @@ def run_ours(args):
                                   "achieved": round(op_tflops, 3), "peak": fp64_peak, "unit": "TFLOP/s",
                                   "frac": round(op_tflops / fp64_peak, 4), "flops_per_launch": op_flops,
                                   "ms_per_launch": round(ms_op, 4), "peak_source": fp64_src},
-            "roofline_arnoldi": {"bound": "hbm", "kernel": "reduce_kernel (K3: one MGS round, fused axpy + dot)",
-                                 "achieved": round(32.0 * n / (ms_mgs * 1e-3) / 1e9, 1), "peak": hbm_peak,
-                                 "unit": "GB/s", "frac": round(32.0 * n / (ms_mgs * 1e-3) / 1e9 / hbm_peak, 4),
-                                 "bytes_per_launch": 32 * n, "ms_per_launch": round(ms_mgs, 5),
-                                 "note": "w read + written, v_(i-1) and v_i read; L2 flushed before each timed round"},
+            "roofline_arnoldi": {"bound": "hbm", "kernel": "mgs_step_kernel (K3/K4: the MGS rounds, second pass, "
+                                                          "h_(k+1), v_(k+1) and the Givens update of one Arnoldi step)",
+                                 "achieved": round(mgs_bytes / (ms_mgs * 1e-3) / 1e9, 1), "peak": hbm_peak,
+                                 "unit": "GB/s", "frac": round(mgs_bytes / (ms_mgs * 1e-3) / 1e9 / hbm_peak, 4),
+                                 "bytes_per_launch": mgs_bytes, "ms_per_launch": round(ms_mgs, 5), "k": k_mgs,
+                                 "second_pass": bool(reorth.value),
+                                 "note": "algorithmic bytes 8 n (3 (k + 1) + 3) (SURVEY 8(d)); the kernel moves "
+                                         "8 n (7 + 4 k) (w read and written every round); L2 flushed before each"},
             "configs": configs,
             "clocks": clocks,
         }

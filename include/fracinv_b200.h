@@ -192,6 +192,10 @@ int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x
  * fused axpy + dot of krylov.cpp:127-132) over device vectors of length n, L2 flushed before each. */
 int fi_mgs_round_timed(fi_ctx* ctx, long long n, double* w_dev, const double* x_dev, const double* y_dev, int reps,
                        double* ms_avg);
+/* Measurement hook (bench roofline of K3/K4): average time of one Arnoldi step's MGS + Givens kernel
+ * (mgs_step_kernel) at step k over pseudo-random vectors of length n, L2 flushed before each; *reorth
+ * (may be NULL) tells whether the conditional second pass ran. */
+int fi_mgs_step_timed(fi_ctx* ctx, long long n, int k, int reps, double* ms_avg, int* reorth);
 /* Dense realisation (spectra.cpp:14-45, verification only): kind 0 = SystemA, 1 = PreconditionerP,
  * 2 = ForwardAhat; row-major dim x dim into device memory M_dev (dim = (S+1)N, or S N for Ahat);
  * FI_E_RESOURCE above cap (<= 0: 4096).  Bit-for-bit the reference's entries. */

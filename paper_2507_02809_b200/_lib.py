@@ -70,6 +70,8 @@ _SIGS = {
     "fi_symbol_coeffs_md": (ctypes.c_int, [ctypes.c_double, ctypes.c_int, c_int_p, ctypes.c_longlong, c_double_p]),
     "fi_mgs_round_timed": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
+    "fi_mgs_step_timed": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
     "fi_assemble_dense": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p]),
     "fi_system_set_split_apply": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "fi_symbol_coeffs_md_dev": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int, c_int_p, ctypes.c_longlong,

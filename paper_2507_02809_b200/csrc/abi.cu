@@ -608,6 +608,15 @@ int fi_mgs_round_timed(fi_ctx* ctx, long long n, double* w_dev, const double* x_
     });
 }
 
+int fi_mgs_step_timed(fi_ctx* ctx, long long n, int k, int reps, double* ms_avg, int* reorth) {
+    return guard([&] {
+        require(ctx && ms_avg && n > 0 && k >= 0 && reps > 0, FI_E_DOMAIN, "fi_mgs_step_timed: bad argument");
+        bind(ctx);
+        fib::GmresEngine eng(ctx, n);
+        *ms_avg = eng.time_mgs_step(k, reps, reorth);
+    });
+}
+
 int fi_assemble_dense(fi_system* sys, int kind, long long cap, double* M_dev) {
     return guard([&] {
         require(sys && M_dev, FI_E_DOMAIN, "fi_assemble_dense: NULL argument");

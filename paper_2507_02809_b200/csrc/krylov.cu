@@ -291,7 +291,9 @@ __global__ void __launch_bounds__(MT) mgs_step_kernel(MgsArgs a) {
     round(V + (long long)k * ldv, coef, nullptr, dummy, post2);
     double nn2 = post2;
     // conditional second pass (krylov.cpp:134-140)
-    if (sqrt(post2) < sqrt(pre2) * 0.70710678118654752) {
+    const bool reorth = sqrt(post2) < sqrt(pre2) * 0.70710678118654752;
+    if (writer) st->reorth = reorth ? 1 : 0;
+    if (reorth) {
         round(nullptr, 0.0, V, coef, dummy);
         if (writer) st->c[0] = coef;
         for (int i = 1; i <= k; ++i) {
@@ -549,6 +551,66 @@ double GmresEngine::time_mgs_round(double* w, const double* x, const double* y, 
         FI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         if (r > 0) total += ms;  // (round 0: warm-up)
     }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return total / reps;
+}
+
+__global__ void fill_random_kernel(double* p, long long n, unsigned long long seed) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long x = (unsigned long long)i * 0x9E3779B97F4A7C15ull + seed * 0xBF58476D1CE4E5B9ull;
+        x ^= x >> 30;
+        x *= 0xBF58476D1CE4E5B9ull;
+        x ^= x >> 27;
+        x *= 0x94D049BB133111EBull;
+        x ^= x >> 31;
+        p[i] = (double)(x >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    }
+}
+
+double GmresEngine::time_mgs_step(int k, int reps, int* reorth) {
+    reserve(k + 2, false);
+    ensure(w_, (size_t)n_);
+    ensure(hist_, 8);
+    DevBuf<double> flush((size_t)48 << 20), sink(1);  // 384 MB: larger than L2
+    FI_CUDA(cudaMemsetAsync(flush.p, 0, flush.bytes(), ctx_->stream));
+    fill_random_kernel<<<ctx_->sm_count * 4, 256, 0, ctx_->stream>>>(V_.p, (long long)(k + 1) * ldv_, 11);
+    FI_LAUNCHED(ctx_);
+    GmresState hs{};
+    hs.h = h_.p;
+    hs.c = c_.p;
+    hs.cs = cs_.p;
+    hs.sn = sn_.p;
+    hs.g = g_.p;
+    hs.ycoef = ycoef_.p;
+    hs.R = R_.p;
+    hs.bnorm = 1.0;
+    hs.tol = 0.0;
+    hs.breakdown_tol = 0.0;
+    std::vector<double> zeros((size_t)k + 2, 0.0);
+    FI_CUDA(cudaMemcpyAsync(cs_.p, zeros.data(), zeros.size() * sizeof(double), cudaMemcpyHostToDevice, ctx_->stream));
+    FI_CUDA(cudaMemcpyAsync(sn_.p, zeros.data(), zeros.size() * sizeof(double), cudaMemcpyHostToDevice, ctx_->stream));
+    cudaEvent_t e0, e1;
+    FI_CUDA(cudaEventCreate(&e0));
+    FI_CUDA(cudaEventCreate(&e1));
+    float total = 0.f;
+    for (int r = 0; r <= reps; ++r) {
+        fill_random_kernel<<<ctx_->sm_count * 4, 256, 0, ctx_->stream>>>(w_.p, n_, 17 + r);
+        FI_LAUNCHED(ctx_);
+        FI_CUDA(cudaMemcpyAsync(st_, &hs, sizeof(GmresState), cudaMemcpyHostToDevice, ctx_->stream));
+        flush_read_kernel<<<ctx_->sm_count * 8, 256, 0, ctx_->stream>>>(reinterpret_cast<const double2*>(flush.p),
+                                                                        (long long)(flush.n / 2), sink.p);
+        FI_CUDA(cudaEventRecord(e0, ctx_->stream));
+        mgs_step(k, 1 << 30, false, 0);
+        FI_CUDA(cudaEventRecord(e1, ctx_->stream));
+        FI_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        FI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        if (r > 0) total += ms;  // (round 0: warm-up)
+    }
+    GmresState out{};
+    FI_CUDA(cudaMemcpy(&out, st_, sizeof(GmresState), cudaMemcpyDeviceToHost));
+    if (reorth) *reorth = out.reorth;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return total / reps;

@@ -55,6 +55,9 @@ public:
     // measurement hook (bench roofline): average time of one MGS round w -= c x; h = y.w over
     // device vectors of length n(), L2 flushed (a read larger than L2) before every timed round
     double time_mgs_round(double* w, const double* x, const double* y, int reps);
+    // measurement hook (bench roofline of K3/K4): average time of one mgs_step_kernel at Arnoldi step k on
+    // pseudo-random vectors, L2 flushed before each; *reorth: whether the second pass ran
+    double time_mgs_step(int k, int reps, int* reorth);
     // Reference semantics of gmres() (krylov.cpp:72-209) + restart extension.
     // Host-driven: the host enqueues every Arnoldi step, two steps ahead of the device's convergence
     // flag; the Krylov basis grows on demand (full GMRES allocates as it goes, like the reference).

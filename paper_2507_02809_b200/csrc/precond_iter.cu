@@ -646,6 +646,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                     }
                 }
             __syncthreads();
+            sub(20);  // the block-start history
         }
         const bool tl = lv < a.S;
         const long long lo = (long long)min(lv, a.S - 1) * Np;  // this level's rows of z, D1, 1/D2 (f-block: S-1)
@@ -713,6 +714,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                     }
                 }
             if (direct) continue;  // grid-uniform
+            sub(28);  // the element setup
             __syncthreads();
             if (warm) {
                 // (row i0, row i1) pairs of x0 (zero beyond n2) into buffer 0, then F2 -> Zh
