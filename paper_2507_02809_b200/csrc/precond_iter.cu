@@ -479,6 +479,9 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     const int VW = 2 * ld2;  // doubles per owned row pair and vector
     double* vsm = reinterpret_cast<double*>(gbuf + max(ngR_ * 2 * PLR, ngC_ * 2 * PLC));
     auto vrow = [&](int ou, int arr) { return vsm + ((size_t)ou * V_N + arr) * VW; };
+    // the column passes' eigenvalues, loaded with the pass's input (before the first transform) and read
+    // after it: 2 x ngC x L1 doubles after the row-owned vectors
+    double* lsm = vsm + (size_t)((((n1 + 1) / 2) + G - 1) / G) * V_N * VW;
     const int nuR = (n1 + 1) / 2, nuB = H2, nuT = (n2 + 1) / 2;  // units of the row, B-column, tau-column passes
     const int rdR = (nuR + G * ngR - 1) / (G * ngR), rdB = (nuB + G * ngC - 1) / (G * ngC),
               rdT = (nuT + G * ngC - 1) / (G * ngC);
@@ -742,6 +745,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             const int lim = nact(nuB, ngC, rd) * L1;
             for (int base = 0; base < lim; base += UF * FT) {
                 double2 v[UF];
+                double lamq[UF];
 #pragma unroll
                 for (int q = 0; q < UF; ++q) {
                     const int e = base + tid + q * FT;
@@ -756,6 +760,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                         zv.y += beta * xp.y;
                     }
                     v[q] = ok && j < n1 ? zv : make_double2(0.0, 0.0);
+                    lamq[q] = a.lamB[(long long)j * L2 + kc];
                 }
 #pragma unroll
                 for (int q = 0; q < UF; ++q) {
@@ -764,6 +769,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                         const int s = e >> a.lg1, j = e & (L1 - 1), k = cta + G * (s + ngC * rd);
                         if (keep && j < n1) a.Xp[(long long)j * H2 + k] = v[q];
                         cbuf(s, 0)[pad8(j)] = v[q];
+                        lsm[(size_t)s * L1 + j] = lamq[q];
                     }
                 }
             }
@@ -771,26 +777,13 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             __syncthreads();
             const int w = fftC(0, false, rd, nuB);
             sub(24);
-            for (int base = 0; base < lim; base += UF * FT) {
-                double lam[UF];
-#pragma unroll
-                for (int q = 0; q < UF; ++q) {
-                    const int e = base + tid + q * FT;
-                    const int ec = e < lim ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
-                    lam[q] = a.lamB[(long long)j * L2 + min(cta + G * (s + ngC * rd), H2 - 1)];
-                }
-#pragma unroll
-                for (int q = 0; q < UF; ++q) {
-                    const int e = base + tid + q * FT;
-                    if (e < lim) {
-                        const int s = e >> a.lg1, j = e & (L1 - 1), k = cta + G * (s + ngC * rd);
-                        const double wk = (k == 0 || k == L2 / 2) ? 1.0 : 2.0;
-                        double2* cell = cbuf(s, w) + pad8(j);
-                        const double2 cv = *cell;
-                        pbp += wk * lam[q] * (cv.x * cv.x + cv.y * cv.y);
-                        *cell = make_double2(cv.x * lam[q], cv.y * lam[q]);
-                    }
-                }
+            for (int e = tid; e < lim; e += FT) {
+                const int s = e >> a.lg1, j = e & (L1 - 1), k = cta + G * (s + ngC * rd);
+                const double wk = (k == 0 || k == L2 / 2) ? 1.0 : 2.0, lam = lsm[(size_t)s * L1 + j];
+                double2* cell = cbuf(s, w) + pad8(j);
+                const double2 cv = *cell;
+                pbp += wk * lam * (cv.x * cv.x + cv.y * cv.y);
+                *cell = make_double2(cv.x * lam, cv.y * lam);
             }
             sub(25);
             __syncthreads();
@@ -932,7 +925,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
         for (int rd = 0; rd < rdT; ++rd) {
             const int lim = nact(nuT, ngC, rd) * L1;
             for (int base = 0; base < lim; base += UF * FT) {
-                double2 v[UF];
+                double2 v[UF], ilq[UF];
 #pragma unroll
                 for (int q = 0; q < UF; ++q) {
                     const int e = base + tid + q * FT;
@@ -945,49 +938,39 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                     oext(j, n1, L1, jj, sg);
                     const double x0 = a.Rr[(long long)jj * n2 + k0c], x1 = a.Rr[(long long)jj * n2 + k1c];
                     v[q] = make_double2(ok ? sg * x0 : 0.0, ok && k0 + 1 < n2 ? sg * x1 : 0.0);
+                    const int kk = (j >= 1 && j <= n1) ? j : (j >= n1 + 2 ? L1 - j : 1);
+                    ilq[q] = make_double2(a.lamT[(long long)(kk - 1) * n2 + k0c], a.lamT[(long long)(kk - 1) * n2 + k1c]);
                 }
 #pragma unroll
                 for (int q = 0; q < UF; ++q) {
                     const int e = base + tid + q * FT;
-                    if (e < lim) cbuf(e >> a.lg1, 0)[pad8(e & (L1 - 1))] = v[q];
+                    if (e < lim) {
+                        cbuf(e >> a.lg1, 0)[pad8(e & (L1 - 1))] = v[q];
+                        reinterpret_cast<double2*>(lsm)[e] = ilq[q];
+                    }
                 }
             }
             sub(14);
             __syncthreads();
             const int w = fftC(0, false, rd, nuT);
             sub(15);
-            for (int base = 0; base < lim; base += UF * FT) {
-                double2 il[UF];
-#pragma unroll
-                for (int q = 0; q < UF; ++q) {
-                    const int e = base + tid + q * FT;
-                    const int ec = e < lim ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
-                    const int k0 = 2 * (cta + G * (s + ngC * rd));
-                    const int k0c = min(k0, n2 - 1), k1c = min(k0 + 1, n2 - 1);
-                    const int kk = (j >= 1 && j <= n1) ? j : (j >= n1 + 2 ? L1 - j : 1);
-                    il[q] = make_double2(a.lamT[(long long)(kk - 1) * n2 + k0c], a.lamT[(long long)(kk - 1) * n2 + k1c]);
+            for (int e = tid; e < lim; e += FT) {
+                const int s = e >> a.lg1, j = e & (L1 - 1), k0 = 2 * (cta + G * (s + ngC * rd));
+                const double2 il = reinterpret_cast<const double2*>(lsm)[e];
+                double x0 = 0.0, x1 = 0.0;
+                int kk = -1;
+                double sg = 1.0;
+                if (j >= 1 && j <= n1) kk = j;
+                else if (j >= n1 + 2) {
+                    kk = L1 - j;
+                    sg = -1.0;
                 }
-#pragma unroll
-                for (int q = 0; q < UF; ++q) {
-                    const int e = base + tid + q * FT;
-                    if (e < lim) {
-                        const int s = e >> a.lg1, j = e & (L1 - 1), k0 = 2 * (cta + G * (s + ngC * rd));
-                        double x0 = 0.0, x1 = 0.0;
-                        int kk = -1;
-                        double sg = 1.0;
-                        if (j >= 1 && j <= n1) kk = j;
-                        else if (j >= n1 + 2) {
-                            kk = L1 - j;
-                            sg = -1.0;
-                        }
-                        if (kk > 0) {
-                            const double2 cv = cbuf(s, w)[pad8(kk)];
-                            x0 = sg * (sc1 * cv.y) / (c * il[q].x + dmean);
-                            if (k0 + 1 < n2) x1 = sg * (-sc1 * cv.x) / (c * il[q].y + dmean);
-                        }
-                        cbuf(s, 1 - w)[pad8(j)] = make_double2(x0, x1);
-                    }
+                if (kk > 0) {
+                    const double2 cv = cbuf(s, w)[pad8(kk)];
+                    x0 = sg * (sc1 * cv.y) / (c * il.x + dmean);
+                    if (k0 + 1 < n2) x1 = sg * (-sc1 * cv.x) / (c * il.y + dmean);
                 }
+                cbuf(s, 1 - w)[pad8(j)] = make_double2(x0, x1);
             }
             sub(16);
             __syncthreads();
@@ -1333,7 +1316,7 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
                                                          (a.n2 + 1) / 2), H2)), 160);  // row pairs per CTA
     const size_t smem = ((size_t)a.L1 + a.L2 + std::max((size_t)ngr * 2 * plr, (size_t)ngc * 2 * plc)) *
                             sizeof(double2) +
-                        (size_t)nown * 5 * 2 * a.ld2 * sizeof(double);
+                        (size_t)nown * 5 * 2 * a.ld2 * sizeof(double) + (size_t)2 * ngc * a.L1 * sizeof(double);
     if (smem > 227 * 1024) throw Error(FI_E_RESOURCE, "tau_pcg_fused: shared memory");
     if (P->it_fgrid == 0) {
         ensure_smem_attr((const void*)tau_pcg_fused, smem);
