@@ -483,8 +483,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     // after it: 2 x ngC x L1 doubles after the row-owned vectors
     double* lsm = vsm + (size_t)((((n1 + 1) / 2) + G - 1) / G) * V_N * VW;
     const int nuR = (n1 + 1) / 2, nuB = H2, nuT = (n2 + 1) / 2;  // units of the row, B-column, tau-column passes
-    const int rdR = (nuR + G * ngR - 1) / (G * ngR), rdB = (nuB + G * ngC - 1) / (G * ngC),
-              rdT = (nuT + G * ngC - 1) / (G * ngC);
+    const int rdR = (nuR + G * ngR - 1) / (G * ngR), rdT = (nuT + G * ngC - 1) / (G * ngC);
 
     // ---- group buffers and transforms.  Slot s of a pass owns the group buffers of group s; in round rd
     // it holds the unit cta + G (s + ng rd).  Element work (loads, stores, dot products) is spread over
@@ -737,21 +736,32 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
         sub(27);
         return bn;
     };
+    // The B column pass: a CTA takes CU adjacent columns per round, one transform group each, and the
+    // element loops interleave the lanes across them, so a warp's loads and stores cover whole 32-byte
+    // sectors of adjacent columns instead of one 16-byte value per row (a column pass reads and writes
+    // with the stride of a full row).  (The tau column pass keeps one column pair per CTA: with two per
+    // CTA on half the SMs its transforms were slower than the sectors it saved.)
+    constexpr int CU = 2;  // (the lane interleave below is e & 1, e >> 1)
+    const int rdB2 = (nuB + G * CU - 1) / (G * CU);
+    auto cunit = [&](int s, int rd) { return (cta + G * rd) * CU + s; };
+    auto fftCU = [&](int w, bool inv, int rd, int nunits) -> int {
+        const bool act = gC < CU && cunit(gC, rd) < nunits;
+        return w ^ fft_dispatch(cbuf(gC, w), cbuf(gC, 1 - w), a.lg1, tws1, inv, tC, act);
+    };
     // B2: columns k of the half spectrum: X = Zh + beta Xp (F2 of the new direction; stored to Xp when
     // keep), column FFT, x lambda_B, partial p.Bp (Parseval), inverse column FFT -> Yb
     auto passB2 = [&](double beta, bool keep) -> double {
         double pbp = 0.0;
-        for (int rd = 0; rd < rdB; ++rd) {
-            const int lim = nact(nuB, ngC, rd) * L1;
+        for (int rd = 0; rd < rdB2; ++rd) {
+            if (cunit(0, rd) >= nuB) continue;  // no unit this round (CTA-uniform: no barrier to match)
+            const int lim = CU * L1;
             for (int base = 0; base < lim; base += UF * FT) {
                 double2 v[UF];
                 double lamq[UF];
 #pragma unroll
                 for (int q = 0; q < UF; ++q) {
-                    const int e = base + tid + q * FT;
-                    const bool ok = e < lim;
-                    const int ec = ok ? e : 0, s = ec >> a.lg1, j = ec & (L1 - 1);
-                    const int kc = min(cta + G * (s + ngC * rd), H2 - 1);
+                    const int e = base + tid + q * FT, sl = e & (CU - 1), j = e >> 1;
+                    const int k = cunit(sl, rd), kc = min(k, H2 - 1);
                     const long long o = (long long)min(j, n1 - 1) * H2 + kc;
                     double2 zv = a.Zh[o];
                     if (beta != 0.0) {
@@ -759,39 +769,38 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                         zv.x += beta * xp.x;
                         zv.y += beta * xp.y;
                     }
-                    v[q] = ok && j < n1 ? zv : make_double2(0.0, 0.0);
-                    lamq[q] = a.lamB[(long long)j * L2 + kc];
+                    v[q] = e < lim && k < nuB && j < n1 ? zv : make_double2(0.0, 0.0);
+                    lamq[q] = a.lamB[(long long)min(j, L1 - 1) * L2 + kc];
                 }
 #pragma unroll
                 for (int q = 0; q < UF; ++q) {
-                    const int e = base + tid + q * FT;
+                    const int e = base + tid + q * FT, sl = e & (CU - 1), j = e >> 1, k = cunit(sl, rd);
                     if (e < lim) {
-                        const int s = e >> a.lg1, j = e & (L1 - 1), k = cta + G * (s + ngC * rd);
-                        if (keep && j < n1) a.Xp[(long long)j * H2 + k] = v[q];
-                        cbuf(s, 0)[pad8(j)] = v[q];
-                        lsm[(size_t)s * L1 + j] = lamq[q];
+                        if (keep && j < n1 && k < nuB) a.Xp[(long long)j * H2 + k] = v[q];
+                        cbuf(sl, 0)[pad8(j)] = v[q];
+                        lsm[(size_t)sl * L1 + j] = lamq[q];
                     }
                 }
             }
             sub(23);
             __syncthreads();
-            const int w = fftC(0, false, rd, nuB);
+            const int w = fftCU(0, false, rd, nuB);
             sub(24);
             for (int e = tid; e < lim; e += FT) {
-                const int s = e >> a.lg1, j = e & (L1 - 1), k = cta + G * (s + ngC * rd);
-                const double wk = (k == 0 || k == L2 / 2) ? 1.0 : 2.0, lam = lsm[(size_t)s * L1 + j];
-                double2* cell = cbuf(s, w) + pad8(j);
+                const int sl = e >> a.lg1, j = e & (L1 - 1), k = cunit(sl, rd);
+                if (k >= nuB) continue;
+                const double wk = (k == 0 || k == L2 / 2) ? 1.0 : 2.0, lam = lsm[(size_t)sl * L1 + j];
+                double2* cell = cbuf(sl, w) + pad8(j);
                 const double2 cv = *cell;
                 pbp += wk * lam * (cv.x * cv.x + cv.y * cv.y);
                 *cell = make_double2(cv.x * lam, cv.y * lam);
             }
             sub(25);
             __syncthreads();
-            const int w2 = fftC(w, true, rd, nuB);
-            const int nao = nact(nuB, ngC, rd);
-            for (int s = 0; s < nao; ++s) {
-                const int k = cta + G * (s + ngC * rd);
-                for (int j = tid; j < n1; j += FT) a.Yb[(long long)j * H2 + k] = cbuf(s, w2)[pad8(j)];
+            const int w2 = fftCU(w, true, rd, nuB);
+            for (int e = tid; e < CU * n1; e += FT) {
+                const int sl = e & (CU - 1), j = e >> 1, k = cunit(sl, rd);
+                if (k < nuB) a.Yb[(long long)j * H2 + k] = cbuf(sl, w2)[pad8(j)];
             }
             sub(26);
             __syncthreads();
