@@ -72,3 +72,29 @@ def test_full_gmres_reference_defaults_grow_the_basis():
     x, rep = F.gmres(A, P, z, F.GmresOptions(TOL[1], 0, 0))
     assert rep.converged and abs(rep.iterations - int(g["iterations"])) <= 1
     assert _rel(x[-A.N:], g["f"]) <= 1e-8
+
+
+def test_unpreconditioned_config4_matches_oracle_golden():
+    """BASELINE configs[4] is solved twice; this is the unpreconditioned GMRES(50) solve (max 2000
+    iterations, tol 1e-8): no preconditioner = the reference's empty apply_M_inv (krylov.cpp:81-83), the
+    loop of krylov.cpp:123-186 with the restart extension.  Golden: the oracle's run on the
+    same observation (tests/golden/oracle_config4_unprec.npz, gen_oracle_solutions.py 4u)."""
+    path = os.path.join(GOLDEN, "oracle_config4_unprec.npz")
+    if not os.path.exists(path):
+        pytest.skip("oracle golden for the unpreconditioned config-4 solve not generated")
+    g = np.load(path)
+    A = F.SystemOperator(baseline_problem(F, 4))
+    z = F.build_rhs(A, g["mu_eps"]).z
+    x, rep = F.gmres(A, None, z, F.GmresOptions(TOL[4], 2000, RESTART))
+    f = x[-A.N:]
+    h, ho = np.asarray(rep.residual_history), np.asarray(g["history"])
+    print(f"config4 unpreconditioned: {rep.iterations} iterations (oracle {int(g['iterations'])}), converged "
+          f"{rep.converged} (oracle {bool(g['converged'])}), f parity {_rel(f, g['f']):.3e}, last history "
+          f"{h[-1]:.6e} (oracle {ho[-1]:.6e}), final true residual {rep.final_true_residual:.6e} "
+          f"(oracle {float(g['final_true_residual']):.6e})")
+    assert rep.converged == bool(g["converged"])
+    assert abs(rep.iterations - int(g["iterations"])) <= 1
+    assert _rel(f, g["f"]) <= 1e-8
+    k = min(len(h), len(ho))
+    assert np.allclose(h[:k], ho[:k], rtol=1e-4, atol=1e-14)
+    assert abs(rep.final_true_residual - float(g["final_true_residual"])) <= 1e-4 * float(g["final_true_residual"])
