@@ -206,6 +206,15 @@ int fi_assemble_dense(fi_system* sys, int kind, long long cap, double* M_dev);
  * identity, cf. Eisenstat's trick); on = 0: A v by K1, then P^{-1} (the reference's order of
  * operations, krylov.cpp:123-126).  Environment FI_SPLIT_APPLY=0 forces 0. */
 int fi_system_set_split_apply(fi_system* sys, int on);
+/* Realisation of the operator apply (fi_system_apply*, and A inside fi_gmres): FI_APPLY_DMMA = K1, the
+ * dense FP64 DMMA contraction K U with K generated per tile (the 1D default); FI_APPLY_FFT = K1f, the
+ * reference's own algorithm (circulant-embedded FFT Toeplitz products, toeplitz.cpp:68-114) as batched
+ * 2D transforms with K1's time convolution fused beside them (2D grids with n_i + 1 a power of two);
+ * FI_APPLY_AUTO (default) = FFT where supported, else DMMA.  FI_E_DOMAIN for FFT on another layout.
+ * Environment FI_APPLY=dmma|fft sets the mode at creation.  get: the realisation in use. */
+enum { FI_APPLY_AUTO = 0, FI_APPLY_DMMA = 1, FI_APPLY_FFT = 2 };
+int fi_system_set_apply_mode(fi_system* sys, int mode);
+int fi_system_get_apply_mode(const fi_system* sys);
 int fi_gmres_host(fi_system* sys, fi_precond* P, const double* b_host, const double* x0_host, double* x_host,
                   const fi_gmres_opts* opts, fi_gmres_report* report, double* history_host, int history_cap);
 

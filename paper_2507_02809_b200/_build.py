@@ -13,7 +13,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libfracinv_b200.so")
-SOURCES = ["toeplitz_apply.cu", "precond_build.cu", "precond_polish.cu", "precond_apply.cu", "precond_sweep_ir.cu", "precond_hodlr.cu", "precond_iter.cu", "krylov.cu", "abi.cu", "setup_host.cpp", "symbol_dev.cu", "spectra_dev.cu"]
+SOURCES = ["toeplitz_apply.cu", "toeplitz_fft.cu", "precond_build.cu", "precond_polish.cu", "precond_apply.cu", "precond_sweep_ir.cu", "precond_hodlr.cu", "precond_iter.cu", "krylov.cu", "abi.cu", "setup_host.cpp", "symbol_dev.cu", "spectra_dev.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include")]
 

@@ -74,6 +74,8 @@ _SIGS = {
                                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
     "fi_assemble_dense": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, ctypes.c_void_p]),
     "fi_system_set_split_apply": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "fi_system_set_apply_mode": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "fi_system_get_apply_mode": (ctypes.c_int, [ctypes.c_void_p]),
     "fi_symbol_coeffs_md_dev": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double, ctypes.c_int, c_int_p, ctypes.c_longlong,
                                                c_double_p]),
     "fi_add_gaussian_noise": (ctypes.c_int,

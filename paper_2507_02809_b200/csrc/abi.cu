@@ -285,6 +285,13 @@ int fi_system_create(fi_ctx* ctx, const fi_system_desc* desc, fi_system** out) {
             sys->ubuf.alloc((size_t)L.nI());
             sys->zbuf.alloc((size_t)L.nI());
             FI_CUDA(cudaMemset(sys->ubuf.p, 0, sys->ubuf.bytes()));
+            // operator realisation: FI_APPLY=dmma|fft overrides the default (AUTO: K1f where supported)
+            sys->fft_ok = fib::fft_apply_supported(L);
+            if (const char* m = std::getenv("FI_APPLY")) {
+                if (std::string(m) == "dmma") sys->apply_mode = FI_APPLY_DMMA;
+                else if (std::string(m) == "fft") sys->apply_mode = FI_APPLY_FFT;
+            }
+            if (sys->use_fft()) fib::fft_apply_prepare(sys);
         } catch (...) {
             delete sys;
             throw;
@@ -312,7 +319,7 @@ int fi_system_apply(fi_system* sys, const double* y_dev, double* z_dev) {
         bind(sys->ctx);
         fi_ctx* ctx = sys->ctx;
         fib::pack_vector(ctx, sys->L, y_dev, sys->ubuf.p);
-        fib::toeplitz_apply(ctx, sys->view(), sys->ubuf.p, sys->zbuf.p, nullptr);
+        fib::system_apply(ctx, sys, sys->ubuf.p, sys->zbuf.p, nullptr);
         fib::unpack_vector(ctx, sys->L, sys->zbuf.p, z_dev);
     });
 }
@@ -326,7 +333,7 @@ int fi_system_apply_host(fi_system* sys, const double* y_host, double* z_host) {
         fib::DevBuf<double> y((size_t)sys->L.nRef()), z((size_t)sys->L.nRef());
         FI_CUDA(cudaMemcpyAsync(y.p, y_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
         fib::pack_vector(ctx, sys->L, y.p, sys->ubuf.p);
-        fib::toeplitz_apply(ctx, sys->view(), sys->ubuf.p, sys->zbuf.p, nullptr);
+        fib::system_apply(ctx, sys, sys->ubuf.p, sys->zbuf.p, nullptr);
         fib::unpack_vector(ctx, sys->L, sys->zbuf.p, z.p);
         FI_CUDA(cudaMemcpyAsync(z_host, z.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
         FI_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -339,9 +346,9 @@ int fi_system_apply_timed(fi_system* sys, const double* y_dev, double* z_dev, in
         bind(sys->ctx);
         fi_ctx* ctx = sys->ctx;
         fib::pack_vector(ctx, sys->L, y_dev, sys->ubuf.p);
-        fib::toeplitz_apply(ctx, sys->view(), sys->ubuf.p, sys->zbuf.p, nullptr);  // warm-up
+        fib::system_apply(ctx, sys, sys->ubuf.p, sys->zbuf.p, nullptr);  // warm-up
         FI_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
-        for (int r = 0; r < reps; ++r) fib::toeplitz_apply(ctx, sys->view(), sys->ubuf.p, sys->zbuf.p, nullptr);
+        for (int r = 0; r < reps; ++r) fib::system_apply(ctx, sys, sys->ubuf.p, sys->zbuf.p, nullptr);
         FI_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
         FI_CUDA(cudaEventSynchronize(ctx->ev1));
         float ms = 0.f;
@@ -548,9 +555,8 @@ int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x
             if (x0.n < (size_t)n) x0.alloc((size_t)n);
             fib::pack_vector(ctx, L, x0_dev, x0.p);
         }
-        const fib::OperatorView view = sys->view();
-        fib::Op A = [ctx, view](const double* in, double* out, const int* skip) {
-            fib::toeplitz_apply(ctx, view, in, out, skip);
+        fib::Op A = [ctx, sys](const double* in, double* out, const int* skip) {
+            fib::system_apply(ctx, sys, in, out, skip);
         };
         fib::Op M = [ctx, P](const double* in, double* out, const int* skip) {
             fib::precond_apply(ctx, P, in, out, P->sys->L.S + 1, skip);
@@ -576,7 +582,7 @@ int fi_gmres(fi_system* sys, fi_precond* P, const double* b_dev, const double* x
         // device-driven (one CUDA graph per solve, one host synchronisation) unless the restart cycle's
         // basis does not fit or full GMRES was asked for (its basis grows on demand: host-driven loop)
         static const bool device_env = !(std::getenv("FI_GMRES_DEVICE") && std::atoi(std::getenv("FI_GMRES_DEVICE")) == 0);
-        const std::vector<long long> key = {(long long)(P ? P->uid : 0), P ? P->refine : -1, split ? 1 : 0,
+        const std::vector<long long> key = {(long long)(P ? P->uid : 0), P ? P->refine : -1, split ? 1 : 0, sys->use_fft() ? 1 : 0,
                                             (long long)(P ? P->mode : -1)};
         const bool done = device_env && sys->engine->solve_device(A, P ? &M : nullptr, b.p, x0_dev ? x0.p : nullptr,
                                                                   x.p, opts->tol, maxit, opts->restart, key, report,
@@ -623,6 +629,24 @@ int fi_assemble_dense(fi_system* sys, int kind, long long cap, double* M_dev) {
         bind(sys->ctx);
         fib::assemble_dense(sys->ctx, sys, kind, cap <= 0 ? 4096 : cap, M_dev);
     });
+}
+
+int fi_system_set_apply_mode(fi_system* sys, int mode) {
+    return guard([&] {
+        require(sys, FI_E_DOMAIN, "fi_system_set_apply_mode: NULL system");
+        require(mode == FI_APPLY_AUTO || mode == FI_APPLY_DMMA || mode == FI_APPLY_FFT, FI_E_DOMAIN,
+                "fi_system_set_apply_mode: unknown mode");
+        require(mode != FI_APPLY_FFT || sys->fft_ok, FI_E_DOMAIN,
+                "fi_system_set_apply_mode: the FFT apply needs a 2D grid with n_i + 1 a power of two");
+        bind(sys->ctx);
+        sys->apply_mode = mode;
+        if (sys->use_fft()) fib::fft_apply_prepare(sys);
+    });
+}
+
+int fi_system_get_apply_mode(const fi_system* sys) {
+    if (!sys) return -1;
+    return sys->use_fft() ? FI_APPLY_FFT : FI_APPLY_DMMA;
 }
 
 int fi_system_set_split_apply(fi_system* sys, int on) {

@@ -44,6 +44,8 @@ struct fi_precond {
     fib::DevBuf<unsigned long long> it_stats;    // CG steps, levels stopped at maxit, max steps, applies
     fib::DevBuf<int> it_direct_d;
     int it_fgrid = 0;                            // fused kernel: cooperative grid size
+    int it_cu = 2;                               // fused kernel: B column-pass columns per CTA
+    bool it_occ_checked = false;
     fib::DevBuf<double> it_fparts;               // fused kernel: 2 x grid block partials
     fib::DevBuf<unsigned> it_fbar;               // fused kernel: grid-barrier counter
     ~fi_precond();

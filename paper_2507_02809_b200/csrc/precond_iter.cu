@@ -19,11 +19,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include "fft_dev.cuh"
 #include "precond.cuh"
-
-#ifndef FI_FFT_R8
-#define FI_FFT_R8 1  // radix-8 transform groups (L/8 threads); 0: radix-4 (L/4 threads), measured 7-9% slower
-#endif
 
 namespace fib {
 namespace {
@@ -65,6 +62,7 @@ struct ItArgs {
     double* Rr;   // n1 x n2 real DST work
     const int* skip;
     int warm;    // extrapolated initial guesses for the time levels (FI_TAU_WARM, default 1)
+    int cu, cus; // B column pass: adjacent columns per CTA and round (a power of two <= the groups), log2
 };
 
 __device__ __forceinline__ bool skipped(const ItArgs& a) { return a.skip && *a.skip; }
@@ -181,188 +179,6 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
     return v;
-}
-
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 mul_i(double2 a, bool inv) {  // -i a (forward), +i a (inverse)
-    return inv ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
-}
-// shared-memory index with one pad element per 8 (the radix-8 scatter of the first pass is conflict-free)
-__device__ __forceinline__ int pad8(int i) { return i + (i >> 3); }
-
-
-// Stockham FFT of length L = 2^LG by the L/4 threads (index t) of one group, between the group's two padded
-// shared buffers (index pad8(i)).  Input in src (natural order); the output lands in src when the number
-// of passes is even, else in dst (natural order).  Radix-4 passes (one radix-2 pass first when LG is odd),
-// one butterfly per thread; LG and the direction are template parameters so the index arithmetic folds
-// to constants.  tw: the full table exp(-2 pi i k / L), k < L.  Every thread of the CTA must call it (it
-// contains __syncthreads); groups without a unit pass active = false.  Not inlined: one copy per length
-// and direction serves every pass (instruction cache).
-#if FI_FFT_R8
-// radix-8 variant: L/8 threads per transform, one radix-2 or radix-4 pass first when LG % 3 != 0
-__device__ __forceinline__ void dft8(double2 (&v)[8], bool inv) {
-    constexpr double r = 0.70710678118654752440;
-    double2 b[8];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        b[m] = cadd(v[m], v[m + 4]);
-        b[m + 4] = csub(v[m], v[m + 4]);
-    }
-    if (!inv) {
-        b[5] = make_double2(r * (b[5].x + b[5].y), r * (b[5].y - b[5].x));
-        b[7] = make_double2(r * (b[7].y - b[7].x), -r * (b[7].x + b[7].y));
-    } else {
-        b[5] = make_double2(r * (b[5].x - b[5].y), r * (b[5].x + b[5].y));
-        b[7] = make_double2(-r * (b[7].x + b[7].y), r * (b[7].x - b[7].y));
-    }
-    b[6] = mul_i(b[6], inv);
-    const double2 c0 = cadd(b[0], b[2]), c2 = csub(b[0], b[2]), c1 = cadd(b[1], b[3]), c3 = mul_i(csub(b[1], b[3]), inv);
-    const double2 c4 = cadd(b[4], b[6]), c6 = csub(b[4], b[6]), c5 = cadd(b[5], b[7]), c7 = mul_i(csub(b[5], b[7]), inv);
-    v[0] = cadd(c0, c1);
-    v[4] = csub(c0, c1);
-    v[2] = cadd(c2, c3);
-    v[6] = csub(c2, c3);
-    v[1] = cadd(c4, c5);
-    v[5] = csub(c4, c5);
-    v[3] = cadd(c6, c7);
-    v[7] = csub(c6, c7);
-}
-template <int LG, bool INV>
-__device__ __noinline__ void fft_group(double2* src, double2* dst, const double2* tw, int t, bool active) {
-    constexpr int L = 1 << LG, NT = (L >> 3) > 0 ? (L >> 3) : 1, REM = LG % 3;
-    int p = 1;
-    if constexpr (REM == 1) {
-        if (active)
-            for (int j = t; j < (L >> 1); j += NT) {
-                const double2 x0 = src[pad8(j)], x1 = src[pad8(j + (L >> 1))];
-                dst[pad8(2 * j)] = cadd(x0, x1);
-                dst[pad8(2 * j + 1)] = csub(x0, x1);
-            }
-        __syncthreads();
-        double2* tt = src;
-        src = dst;
-        dst = tt;
-        p = 2;
-    } else if constexpr (REM == 2) {
-        constexpr int Q = L >> 2;
-        if (active)
-            for (int j = t; j < Q; j += NT) {
-                const double2 a0 = src[pad8(j)], a1 = src[pad8(j + Q)], a2 = src[pad8(j + 2 * Q)], a3 = src[pad8(j + 3 * Q)];
-                const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = mul_i(csub(a1, a3), INV);
-                dst[pad8(4 * j)] = cadd(s02, s13);
-                dst[pad8(4 * j + 1)] = cadd(d02, d13);
-                dst[pad8(4 * j + 2)] = csub(s02, s13);
-                dst[pad8(4 * j + 3)] = csub(d02, d13);
-            }
-        __syncthreads();
-        double2* tt = src;
-        src = dst;
-        dst = tt;
-        p = 4;
-    }
-    constexpr int Q8 = L >> 3;
-#pragma unroll
-    for (int s = REM; s < LG; s += 3) {
-        p = 1 << s;
-        if (active && Q8 > 0) {
-            const int j = t, k = j & (p - 1);
-            double2 v[8];
-#pragma unroll
-            for (int m = 0; m < 8; ++m) v[m] = src[pad8(j + m * Q8)];
-            if (p > 1) {
-                const int ts = k << (LG - s - 3);  // k L / (8 p)
-#pragma unroll
-                for (int m = 1; m < 8; ++m) {
-                    double2 w = tw[m * ts];
-                    if (INV) w.y = -w.y;
-                    v[m] = make_double2(v[m].x * w.x - v[m].y * w.y, v[m].x * w.y + v[m].y * w.x);
-                }
-            }
-            dft8(v, INV);
-            const int o = 8 * (j - k) + k;
-#pragma unroll
-            for (int m = 0; m < 8; ++m) dst[pad8(o + m * p)] = v[m];
-        }
-        __syncthreads();
-        double2* tt = src;
-        src = dst;
-        dst = tt;
-    }
-}
-constexpr int kFftRadix = 8;
-#else
-template <int LG, bool INV>
-__device__ __noinline__ void fft_group(double2* src, double2* dst, const double2* tw, int t, bool active) {
-    constexpr int L = 1 << LG, Q = L >> 2;
-    if constexpr (LG & 1) {  // radix-2 pass: L/2 butterflies, two per thread
-        if (active)
-            for (int j = t; j < (L >> 1); j += Q) {
-                const double2 x0 = src[pad8(j)], x1 = src[pad8(j + (L >> 1))];
-                dst[pad8(2 * j)] = cadd(x0, x1);
-                dst[pad8(2 * j + 1)] = csub(x0, x1);
-            }
-        __syncthreads();
-        double2* tt = src;
-        src = dst;
-        dst = tt;
-    }
-#pragma unroll
-    for (int s = (LG & 1); s < LG; s += 2) {
-        const int p = 1 << s;
-        if (active && Q > 0) {
-            const int j = t;
-            const int k = j & (p - 1);
-            double2 a0 = src[pad8(j)], a1 = src[pad8(j + Q)], a2 = src[pad8(j + 2 * Q)], a3 = src[pad8(j + 3 * Q)];
-            if (p > 1) {
-                const int ts = k << (LG - s - 2);  // k L / (4 p)
-                double2 w1 = tw[ts], w2 = tw[2 * ts], w3 = tw[3 * ts];
-                if (INV) {
-                    w1.y = -w1.y;
-                    w2.y = -w2.y;
-                    w3.y = -w3.y;
-                }
-                a1 = make_double2(a1.x * w1.x - a1.y * w1.y, a1.x * w1.y + a1.y * w1.x);
-                a2 = make_double2(a2.x * w2.x - a2.y * w2.y, a2.x * w2.y + a2.y * w2.x);
-                a3 = make_double2(a3.x * w3.x - a3.y * w3.y, a3.x * w3.y + a3.y * w3.x);
-            }
-            const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = mul_i(csub(a1, a3), INV);
-            const int o = 4 * (j - k) + k;
-            dst[pad8(o)] = cadd(s02, s13);
-            dst[pad8(o + p)] = cadd(d02, d13);
-            dst[pad8(o + 2 * p)] = csub(s02, s13);
-            dst[pad8(o + 3 * p)] = csub(d02, d13);
-        }
-        __syncthreads();
-        double2* tt = src;
-        src = dst;
-        dst = tt;
-    }
-}
-constexpr int kFftRadix = 4;
-#endif
-// runtime dispatch on the transform length; returns the buffer index (0 = src) holding the output
-__device__ __forceinline__ int fft_dispatch(double2* src, double2* dst, int lg, const double2* tw, bool inv, int t,
-                                            bool active) {
-#define FI_FFT_CASE(n)                                        \
-    case n:                                                   \
-        if (inv) fft_group<n, true>(src, dst, tw, t, active); \
-        else fft_group<n, false>(src, dst, tw, t, active);    \
-        break;
-    switch (lg) {
-        FI_FFT_CASE(2)
-        FI_FFT_CASE(3)
-        FI_FFT_CASE(4)
-        FI_FFT_CASE(5)
-        FI_FFT_CASE(6)
-        FI_FFT_CASE(7)
-        FI_FFT_CASE(8)
-        FI_FFT_CASE(9)
-        FI_FFT_CASE(10)
-        default: __trap();
-    }
-#undef FI_FFT_CASE
-    return kFftRadix == 4 ? ((lg + 1) / 2) & 1 : ((lg / 3) + (lg % 3 ? 1 : 0)) & 1;
 }
 
 __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
@@ -741,7 +557,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     // sectors of adjacent columns instead of one 16-byte value per row (a column pass reads and writes
     // with the stride of a full row).  (The tau column pass keeps one column pair per CTA: with two per
     // CTA on half the SMs its transforms were slower than the sectors it saved.)
-    constexpr int CU = 2;  // (the lane interleave below is e & 1, e >> 1)
+    const int CU = a.cu, CUS = a.cus;  // (the lane interleave below is e & (CU - 1), e >> CUS)
     const int rdB2 = (nuB + G * CU - 1) / (G * CU);
     auto cunit = [&](int s, int rd) { return (cta + G * rd) * CU + s; };
     auto fftCU = [&](int w, bool inv, int rd, int nunits) -> int {
@@ -760,7 +576,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                 double lamq[UF];
 #pragma unroll
                 for (int q = 0; q < UF; ++q) {
-                    const int e = base + tid + q * FT, sl = e & (CU - 1), j = e >> 1;
+                    const int e = base + tid + q * FT, sl = e & (CU - 1), j = e >> CUS;
                     const int k = cunit(sl, rd), kc = min(k, H2 - 1);
                     const long long o = (long long)min(j, n1 - 1) * H2 + kc;
                     double2 zv = a.Zh[o];
@@ -774,7 +590,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                 }
 #pragma unroll
                 for (int q = 0; q < UF; ++q) {
-                    const int e = base + tid + q * FT, sl = e & (CU - 1), j = e >> 1, k = cunit(sl, rd);
+                    const int e = base + tid + q * FT, sl = e & (CU - 1), j = e >> CUS, k = cunit(sl, rd);
                     if (e < lim) {
                         if (keep && j < n1 && k < nuB) a.Xp[(long long)j * H2 + k] = v[q];
                         cbuf(sl, 0)[pad8(j)] = v[q];
@@ -799,7 +615,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             __syncthreads();
             const int w2 = fftCU(w, true, rd, nuB);
             for (int e = tid; e < CU * n1; e += FT) {
-                const int sl = e & (CU - 1), j = e >> 1, k = cunit(sl, rd);
+                const int sl = e & (CU - 1), j = e >> CUS, k = cunit(sl, rd);
                 if (k < nuB) a.Yb[(long long)j * H2 + k] = cbuf(sl, w2)[pad8(j)];
             }
             sub(26);
@@ -1321,24 +1137,37 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
     const int H2 = a.L2 / 2 + 1;
     const int plr = a.L2 + a.L2 / 8 + 1, plc = a.L1 + a.L1 / 8 + 1;
     const int ngr = FT / std::max(a.L2 / kFftRadix, 1), ngc = FT / std::max(a.L1 / kFftRadix, 1);
-    const int nown = 1 + ((a.n1 + 1) / 2 - 1) / std::min(std::min(ctx->sm_count, std::max(std::max((a.n1 + 1) / 2,
-                                                         (a.n2 + 1) / 2), H2)), 160);  // row pairs per CTA
+    if (P->it_fgrid == 0) {
+        // one CTA per SM, or fewer when the passes have fewer units (small grids); FI_TAU_GRID caps it
+        // (greduce reads <= 5 partials per lane: <= 160)
+        const int units = std::max(std::max((a.n1 + 1) / 2, (a.n2 + 1) / 2), H2);
+        static const int cap = std::getenv("FI_TAU_GRID") ? std::atoi(std::getenv("FI_TAU_GRID")) : 0;
+        int g = std::min(std::min(ctx->sm_count, units), 160);
+        if (cap > 0) g = std::min(g, cap);
+        // the B column pass takes cu adjacent columns per CTA: the smallest power of two that covers the
+        // half spectrum's columns in one round, at most one per transform group
+        int cu = 1;
+        while (cu < ngc && (long long)g * cu < H2) cu *= 2;
+        P->it_fgrid = g;
+        P->it_cu = cu;
+        P->it_fparts.alloc((size_t)2 * kRedMax * g);
+        P->it_fbar.alloc(1);
+    }
+    a.cu = P->it_cu;
+    a.cus = ilog2(a.cu);
+    const int G = P->it_fgrid;
+    const int nown = ((a.n1 + 1) / 2 + G - 1) / G;  // row pairs per CTA
     const size_t smem = ((size_t)a.L1 + a.L2 + std::max((size_t)ngr * 2 * plr, (size_t)ngc * 2 * plc)) *
                             sizeof(double2) +
-                        (size_t)nown * 5 * 2 * a.ld2 * sizeof(double) + (size_t)2 * ngc * a.L1 * sizeof(double);
+                        (size_t)nown * 5 * 2 * a.ld2 * sizeof(double) +
+                        (size_t)std::max(2 * ngc, a.cu) * a.L1 * sizeof(double);
     if (smem > 227 * 1024) throw Error(FI_E_RESOURCE, "tau_pcg_fused: shared memory");
-    if (P->it_fgrid == 0) {
-        ensure_smem_attr((const void*)tau_pcg_fused, smem);
+    ensure_smem_attr((const void*)tau_pcg_fused, smem);
+    if (!P->it_occ_checked) {
         int per_sm = 0;
         FI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tau_pcg_fused, FT, smem));
         if (per_sm < 1) throw Error(FI_E_CUDA, "tau_pcg_fused cannot be resident");
-        // one CTA per SM, or fewer when the passes have fewer units (small grids)
-        const int units = std::max(std::max((a.n1 + 1) / 2, (a.n2 + 1) / 2), H2);
-        P->it_fgrid = std::min(std::min(ctx->sm_count, units), 160);  // greduce reads <= 5 partials per lane
-        P->it_fparts.alloc((size_t)2 * kRedMax * P->it_fgrid);
-        P->it_fbar.alloc(1);
-    } else {
-        ensure_smem_attr((const void*)tau_pcg_fused, smem);
+        P->it_occ_checked = true;
     }
     static const bool tracing = std::getenv("FI_ITER_TRACE") != nullptr;
     DevBuf<unsigned long long> trace;

@@ -36,6 +36,13 @@ struct fi_system {
     fib::DevBuf<double> gb, gx, gx0, gio;  // fi_gmres padded b / x / x0 and host-call staging
     fib::DevBuf<double> sp_u, sp_t;        // scratch of the split preconditioned apply
     int split_apply = 1;                   // fi_gmres: P^{-1} A v as v + P^{-1}((A - P) v) (fi_system_set_split_apply)
+    int apply_mode = 0;                    // FI_APPLY_AUTO / _DMMA / _FFT (fi_system_set_apply_mode)
+    bool fft_ok = false;                   // the FFT apply supports this layout (2D, n_i + 1 a power of two)
+    bool fft_ready = false;                // K1f tables and workspace allocated
+    fib::DevBuf<double2> fft_tw1, fft_tw2, fft_W;  // K1f: twiddles, half-spectrum workspace (S+1) x n1 x H2
+    fib::DevBuf<double> fft_lamB;                  // K1f: L1 x L2 spectrum of the embedded generating tensor
+    // AUTO: the transforms where they exist (2D), the dense DMMA contraction (K1) otherwise
+    bool use_fft() const { return fft_ok && apply_mode != 1; }
     fib::GmresEngine* engine = nullptr;  // cached Krylov workspace (owned; freed in fi_system_destroy)
     fib::OperatorView view() const {
         fib::OperatorView v;
@@ -55,4 +62,15 @@ class GmresEngine;
 // A, i.e. drop the -eta q_s f coupling (the block column that P zeroes, spectra.cpp:34-36).
 void toeplitz_apply(fi_ctx* ctx, const OperatorView& op, const double* U, double* Z, const int* skip,
                     const double* minus_from = nullptr, bool precond_matrix = false);
+// K1 in conv-only mode: the time levels' D1 o (U E^T) - eta q f alone (the f column is not written)
+void toeplitz_conv_apply(fi_ctx* ctx, const OperatorView& op, const double* U, double* Z, const int* skip,
+                         const double* minus_from, bool precond_matrix, cudaStream_t stream);
+// K1f: the same Z with K u_s by batched 2D FFTs (toeplitz_fft.cu); 2D layouts with n_i + 1 a power of two
+bool fft_apply_supported(const Layout& L);
+void fft_apply_prepare(fi_system* sys);  // tables and workspace (not inside a stream capture)
+void toeplitz_apply_fft(fi_ctx* ctx, fi_system* sys, const double* U, double* Z, const int* skip,
+                        const double* minus_from = nullptr, bool precond_matrix = false);
+// the system's operator apply in its selected realisation (K1f or K1)
+void system_apply(fi_ctx* ctx, fi_system* sys, const double* U, double* Z, const int* skip,
+                  const double* minus_from = nullptr, bool precond_matrix = false);
 }  // namespace fib

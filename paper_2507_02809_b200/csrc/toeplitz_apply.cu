@@ -97,7 +97,7 @@ __device__ __forceinline__ void load_stage(const OperatorView& op, const double*
 
 __global__ void __launch_bounds__(NTHREADS, 2)
 toeplitz_apply_kernel(OperatorView op, const double* __restrict__ U, double* __restrict__ Z, const int* skip,
-                      const double* __restrict__ minus_from, int precond_matrix) {
+                      const double* __restrict__ minus_from, int precond_matrix, int conv_only) {
     if (skip && *skip) return;
     extern __shared__ __align__(16) double smem[];
 
@@ -107,7 +107,7 @@ toeplitz_apply_kernel(OperatorView op, const double* __restrict__ U, double* __r
     tc.i1 = tc.i0 / op.ld2;
     tc.i2_0 = tc.i0 - tc.i1 * op.ld2;
     tc.nbj2 = (op.n2 + BK - 1) / BK;
-    tc.nmain = op.n1 * tc.nbj2;
+    tc.nmain = conv_only ? 0 : op.n1 * tc.nbj2;  // conv-only: the time convolution alone (K1f)
     const int conv_cols = min(tc.s0 + BN, op.S);
     tc.nconv = tc.s0 < op.S ? (conv_cols + BK - 1) / BK : 0;
     const int total = tc.nconv + tc.nmain;
@@ -279,9 +279,18 @@ void toeplitz_apply(fi_ctx* ctx, const OperatorView& op, const double* U, double
     FI_CUDA(cudaEventRecord(ctx->join, ctx->side));
     dim3 grid((unsigned)(op.Np / BM), (unsigned)((op.S + BN - 1) / BN));
     toeplitz_apply_kernel<<<grid, NTHREADS, SMEM_BYTES, ctx->stream>>>(op, U, Z, skip, minus_from,
-                                                                         precond_matrix ? 1 : 0);
+                                                                         precond_matrix ? 1 : 0, 0);
     FI_LAUNCHED(ctx);
     FI_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join, 0));
+}
+
+void toeplitz_conv_apply(fi_ctx* ctx, const OperatorView& op, const double* U, double* Z, const int* skip,
+                         const double* minus_from, bool precond_matrix, cudaStream_t stream) {
+    // time levels only: Z[:, s] = D1_s o (U E^T)[:, s] - eta q_s f (s < S); the f column is not written
+    ensure_smem_attr((const void*)toeplitz_apply_kernel, SMEM_BYTES);
+    dim3 grid((unsigned)(op.Np / BM), (unsigned)((op.S + BN - 1) / BN));
+    toeplitz_apply_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(op, U, Z, skip, minus_from, precond_matrix ? 1 : 0, 1);
+    FI_LAUNCHED(ctx);
 }
 
 }  // namespace fib

@@ -410,6 +410,20 @@ class SystemOperator:
         self.handle = h
         self._keep = None
 
+    APPLY_MODES = {"auto": 0, "dmma": 1, "fft": 2}
+
+    def set_apply_mode(self, mode: str):
+        """Realisation of the operator apply (also A inside gmres): "dmma" = K1, the dense FP64 DMMA
+        contraction K U with K generated per tile; "fft" = K1f, the reference's circulant-embedded FFT
+        Toeplitz products (toeplitz.cpp:68-114) as batched 2D transforms (2D grids with n_i + 1 a power
+        of two); "auto" (default) = fft where supported — fi_system_set_apply_mode."""
+        _check(lib.fi_system_set_apply_mode(self.handle, self.APPLY_MODES[mode]))
+
+    @property
+    def apply_mode(self) -> str:
+        """The realisation in use: "dmma" or "fft"."""
+        return {1: "dmma", 2: "fft"}[lib.fi_system_get_apply_mode(self.handle)]
+
     def set_split_apply(self, on: bool):
         """Arnoldi steps of gmres(self, P, ...) compute P^{-1} A v as v + P^{-1}((A - P) v) (default, one
         sweep per step) or as K1 then P^{-1} (the reference's order) — fi_system_set_split_apply."""
