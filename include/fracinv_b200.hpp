@@ -201,6 +201,12 @@ public:
     // EXTENSION: Arnoldi steps of gmres() with this system's preconditioner compute P^{-1} A v as
     // v + P^{-1}((A - P) v) (default, one sweep per step) or in the reference's order (K1, then P^{-1})
     void set_split_apply(bool on) { check(fi_system_set_split_apply(h_, on ? 1 : 0)); }
+    // EXTENSION: realisation of apply() (and of A inside gmres()): Dmma = K1, the dense FP64 DMMA contraction
+    // K U (north-star (a)); Fft = K1f, the reference's circulant-embedded FFT Toeplitz products as batched 2D
+    // transforms (2D grids with n_i + 1 a power of two; std::domain_error elsewhere); Auto = Fft where supported
+    enum class ApplyMode { Auto = FI_APPLY_AUTO, Dmma = FI_APPLY_DMMA, Fft = FI_APPLY_FFT };
+    void set_apply_mode(ApplyMode m) { check(fi_system_set_apply_mode(h_, (int)m)); }
+    ApplyMode apply_mode() const { return (ApplyMode)fi_system_get_apply_mode(h_); }
 
     // z = A y (system.cpp:144-174)
     std::vector<double> apply(const std::vector<double>& y) const {

@@ -62,8 +62,9 @@ int main(int argc, char** argv) {
         dim_error = true;
     }
     // the substituted 2D block solve (tau-PCG) against the dense inverses on a 15x15 grid
-    double tau_vs_dense = 1.0;
+    double tau_vs_dense = 1.0, fft_vs_dmma = 1.0;
     int tau_inner = -1;
+    bool fft_default = false, fft_refused_1d = false;
     {
         SpaceGrid g2({15, 15}, {0.0, 0.0}, {1.0, 1.0});
         const auto nodes2 = g2.nodes();
@@ -86,12 +87,29 @@ int main(int argc, char** argv) {
             den += yd[i] * yd[i];
         }
         tau_vs_dense = std::sqrt(num / den);
+        // the operator's two realisations: K1f (FFT, the default on this 2D grid) against K1 (DMMA)
+        fft_default = A2.apply_mode() == SystemOperator::ApplyMode::Fft;
+        const auto zf = A2.apply(v);
+        A2.set_apply_mode(SystemOperator::ApplyMode::Dmma);
+        const auto zd = A2.apply(v);
+        A2.set_apply_mode(SystemOperator::ApplyMode::Auto);
+        num = den = 0.0;
+        for (size_t i = 0; i < v.size(); ++i) {
+            num += (zf[i] - zd[i]) * (zf[i] - zd[i]);
+            den += zd[i] * zd[i];
+        }
+        fft_vs_dmma = std::sqrt(num / den);
+        try {
+            A.set_apply_mode(SystemOperator::ApplyMode::Fft);  // 1D: no FFT realisation
+        } catch (const std::domain_error&) {
+            fft_refused_1d = true;
+        }
     }
     std::printf("{\"iterations\": %d, \"converged\": %s, \"final_true_residual\": %.17g, \"recon_error\": %.17g, "
                 "\"singular_index\": %d, \"dimension_error\": %s, \"history_len\": %zu, \"tau_inner\": %d, "
-                "\"tau_vs_dense\": %.17g}\n",
+                "\"tau_vs_dense\": %.17g, \"fft_default\": %s, \"fft_vs_dmma\": %.17g, \"fft_refused_1d\": %s}\n",
                 rep.iterations, rep.converged ? "true" : "false", rep.final_true_residual,
                 relative_error(f, frec), singular_index, dim_error ? "true" : "false", rep.residual_history.size(),
-                tau_inner, tau_vs_dense);
+                tau_inner, tau_vs_dense, fft_default ? "true" : "false", fft_vs_dmma, fft_refused_1d ? "true" : "false");
     return 0;
 }

@@ -34,3 +34,5 @@ def test_cpp_facade_config0(tmp_path):
     assert np.linalg.norm(f - xo[-255:]) / np.linalg.norm(xo[-255:]) <= 1e-8
     assert rep["singular_index"] == 3 and rep["dimension_error"]
     assert rep["tau_inner"] == 1 and rep["tau_vs_dense"] <= 1e-12  # substituted 2D block solve
+    # the operator's realisations through the facade: K1f by default on the 2D grid, equal to K1; 1D refuses FFT
+    assert rep["fft_default"] and rep["fft_vs_dmma"] <= 1e-13 and rep["fft_refused_1d"]
