@@ -4,9 +4,6 @@
 
 #include <cuda_runtime.h>
 
-#ifndef FI_FFT_R8
-#define FI_FFT_R8 1  // radix-8 transform groups (L/8 threads); 0: radix-4 (L/4 threads), measured 7-9% slower
-#endif
 
 namespace fib {
 namespace {
@@ -20,15 +17,16 @@ __device__ __forceinline__ double2 mul_i(double2 a, bool inv) {  // -i a (forwar
 __device__ __forceinline__ int pad8(int i) { return i + (i >> 3); }
 
 
-// Stockham FFT of length L = 2^LG by the L/4 threads (index t) of one group, between the group's two padded
-// shared buffers (index pad8(i)).  Input in src (natural order); the output lands in src when the number
-// of passes is even, else in dst (natural order).  Radix-4 passes (one radix-2 pass first when LG is odd),
-// one butterfly per thread; LG and the direction are template parameters so the index arithmetic folds
-// to constants.  tw: the full table exp(-2 pi i k / L), k < L.  Every thread of the CTA must call it (it
-// contains __syncthreads); groups without a unit pass active = false.  Not inlined: one copy per length
-// and direction serves every pass (instruction cache).
-#if FI_FFT_R8
-// radix-8 variant: L/8 threads per transform, one radix-2 or radix-4 pass first when LG % 3 != 0
+// Stockham FFT of length L = 2^LG by the L/8 threads (index t) of one group, between the group's two padded
+// shared buffers (index pad8(i)): radix-8 passes, one radix-2 or radix-4 pass first when LG % 3 != 0, one
+// butterfly per thread.  Input in src (natural order); the output lands in src when the number of passes is
+// even, else in dst (natural order).  LG and the direction are template parameters so the index arithmetic
+// folds to constants.  tw: the STAGE twiddle table (fft_stage_twiddles): per radix-8 pass of span p > 1 the
+// seven factors exp(-2 pi i m k / (8p)) as [m - 1][k], so that the lanes of a warp (consecutive k) read
+// consecutive entries — a table indexed m k L / (8p) put up to 8 lanes of a warp on one bank (measured:
+// 8x the ideal shared-memory wavefronts on those loads).  Every thread of the CTA must call it (it contains
+// __syncthreads); groups without a unit pass active = false.  Not inlined: one copy per length and direction
+// serves every pass (instruction cache).
 __device__ __forceinline__ void dft8(double2 (&v)[8], bool inv) {
     constexpr double r = 0.70710678118654752440;
     double2 b[8];
@@ -56,10 +54,28 @@ __device__ __forceinline__ void dft8(double2 (&v)[8], bool inv) {
     v[3] = cadd(c6, c7);
     v[7] = csub(c6, c7);
 }
+
+// The stage twiddle table of length L = 2^lg (it needs fewer than L entries) from exp(-2 pi i k / L):
+// full(k) for k < L.  All threads of the CTA cooperate; the caller synchronises.
+template <class Full>
+__device__ __forceinline__ void fft_stage_twiddles(double2* dst, int lg, Full full) {
+    const int L = 1 << lg, rem = lg % 3;
+    int off = 0;
+    for (int s = rem; s < lg; s += 3) {
+        const int p = 1 << s;
+        if (p > 1) {
+            for (int q = threadIdx.x; q < 7 * p; q += blockDim.x) {
+                const int m = q / p + 1, k = q % p;
+                dst[off + q] = full((m * k * (L / (8 * p))) & (L - 1));
+            }
+            off += 7 * p;
+        }
+    }
+}
+
 template <int LG, bool INV>
 __device__ __noinline__ void fft_group(double2* src, double2* dst, const double2* tw, int t, bool active) {
     constexpr int L = 1 << LG, NT = (L >> 3) > 0 ? (L >> 3) : 1, REM = LG % 3;
-    int p = 1;
     if constexpr (REM == 1) {
         if (active)
             for (int j = t; j < (L >> 1); j += NT) {
@@ -71,7 +87,6 @@ __device__ __noinline__ void fft_group(double2* src, double2* dst, const double2
         double2* tt = src;
         src = dst;
         dst = tt;
-        p = 2;
     } else if constexpr (REM == 2) {
         constexpr int Q = L >> 2;
         if (active)
@@ -87,22 +102,21 @@ __device__ __noinline__ void fft_group(double2* src, double2* dst, const double2
         double2* tt = src;
         src = dst;
         dst = tt;
-        p = 4;
     }
     constexpr int Q8 = L >> 3;
+    int off = 0;
 #pragma unroll
     for (int s = REM; s < LG; s += 3) {
-        p = 1 << s;
+        const int p = 1 << s;
         if (active && Q8 > 0) {
             const int j = t, k = j & (p - 1);
             double2 v[8];
 #pragma unroll
             for (int m = 0; m < 8; ++m) v[m] = src[pad8(j + m * Q8)];
             if (p > 1) {
-                const int ts = k << (LG - s - 3);  // k L / (8 p)
 #pragma unroll
                 for (int m = 1; m < 8; ++m) {
-                    double2 w = tw[m * ts];
+                    double2 w = tw[off + (m - 1) * p + k];
                     if (INV) w.y = -w.y;
                     v[m] = make_double2(v[m].x * w.x - v[m].y * w.y, v[m].x * w.y + v[m].y * w.x);
                 }
@@ -112,6 +126,7 @@ __device__ __noinline__ void fft_group(double2* src, double2* dst, const double2
 #pragma unroll
             for (int m = 0; m < 8; ++m) dst[pad8(o + m * p)] = v[m];
         }
+        if (p > 1) off += 7 * p;
         __syncthreads();
         double2* tt = src;
         src = dst;
@@ -119,56 +134,6 @@ __device__ __noinline__ void fft_group(double2* src, double2* dst, const double2
     }
 }
 constexpr int kFftRadix = 8;
-#else
-template <int LG, bool INV>
-__device__ __noinline__ void fft_group(double2* src, double2* dst, const double2* tw, int t, bool active) {
-    constexpr int L = 1 << LG, Q = L >> 2;
-    if constexpr (LG & 1) {  // radix-2 pass: L/2 butterflies, two per thread
-        if (active)
-            for (int j = t; j < (L >> 1); j += Q) {
-                const double2 x0 = src[pad8(j)], x1 = src[pad8(j + (L >> 1))];
-                dst[pad8(2 * j)] = cadd(x0, x1);
-                dst[pad8(2 * j + 1)] = csub(x0, x1);
-            }
-        __syncthreads();
-        double2* tt = src;
-        src = dst;
-        dst = tt;
-    }
-#pragma unroll
-    for (int s = (LG & 1); s < LG; s += 2) {
-        const int p = 1 << s;
-        if (active && Q > 0) {
-            const int j = t;
-            const int k = j & (p - 1);
-            double2 a0 = src[pad8(j)], a1 = src[pad8(j + Q)], a2 = src[pad8(j + 2 * Q)], a3 = src[pad8(j + 3 * Q)];
-            if (p > 1) {
-                const int ts = k << (LG - s - 2);  // k L / (4 p)
-                double2 w1 = tw[ts], w2 = tw[2 * ts], w3 = tw[3 * ts];
-                if (INV) {
-                    w1.y = -w1.y;
-                    w2.y = -w2.y;
-                    w3.y = -w3.y;
-                }
-                a1 = make_double2(a1.x * w1.x - a1.y * w1.y, a1.x * w1.y + a1.y * w1.x);
-                a2 = make_double2(a2.x * w2.x - a2.y * w2.y, a2.x * w2.y + a2.y * w2.x);
-                a3 = make_double2(a3.x * w3.x - a3.y * w3.y, a3.x * w3.y + a3.y * w3.x);
-            }
-            const double2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = mul_i(csub(a1, a3), INV);
-            const int o = 4 * (j - k) + k;
-            dst[pad8(o)] = cadd(s02, s13);
-            dst[pad8(o + p)] = cadd(d02, d13);
-            dst[pad8(o + 2 * p)] = csub(s02, s13);
-            dst[pad8(o + 3 * p)] = csub(d02, d13);
-        }
-        __syncthreads();
-        double2* tt = src;
-        src = dst;
-        dst = tt;
-    }
-}
-constexpr int kFftRadix = 4;
-#endif
 // runtime dispatch on the transform length; returns the buffer index (0 = src) holding the output
 __device__ __forceinline__ int fft_dispatch(double2* src, double2* dst, int lg, const double2* tw, bool inv, int t,
                                             bool active) {
@@ -190,7 +155,7 @@ __device__ __forceinline__ int fft_dispatch(double2* src, double2* dst, int lg, 
         default: __trap();
     }
 #undef FI_FFT_CASE
-    return kFftRadix == 4 ? ((lg + 1) / 2) & 1 : ((lg / 3) + (lg % 3 ? 1 : 0)) & 1;
+    return ((lg / 3) + (lg % 3 ? 1 : 0)) & 1;
 }
 
 

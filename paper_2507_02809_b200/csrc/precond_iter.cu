@@ -278,14 +278,17 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     double2* tws1 = sm;             // full twiddle tables exp(-2 pi i k / L), k < L, in shared memory
     double2* tws2 = sm + L1;
     double2* gbuf = tws2 + L2;      // transform groups: two padded buffers each
-    for (int t = tid; t < L1; t += FT)
-        tws1[t] = t < L1 / 2 ? a.tw1[t] : make_double2(-a.tw1[t - L1 / 2].x, -a.tw1[t - L1 / 2].y);
-    for (int t = tid; t < L2; t += FT)
-        tws2[t] = t < L2 / 2 ? a.tw2[t] : make_double2(-a.tw2[t - L2 / 2].x, -a.tw2[t - L2 / 2].y);
+    // stage twiddle tables (fft_dev.cuh) from the half tables exp(-2 pi i k / L), k < L/2
+    fft_stage_twiddles(tws1, a.lg1, [&](int k) {
+        return k < L1 / 2 ? a.tw1[k] : make_double2(-a.tw1[k - L1 / 2].x, -a.tw1[k - L1 / 2].y);
+    });
+    fft_stage_twiddles(tws2, a.lg2, [&](int k) {
+        return k < L2 / 2 ? a.tw2[k] : make_double2(-a.tw2[k - L2 / 2].x, -a.tw2[k - L2 / 2].y);
+    });
     __syncthreads();
     // group geometry of the row (length L2) and column (length L1) passes
-    const int ntR = max(kFftRadix == 4 ? L2 >> 2 : L2 >> 3, 1), ngR = FT / ntR, gR = tid / ntR, tR = tid % ntR;
-    const int ntC = max(kFftRadix == 4 ? L1 >> 2 : L1 >> 3, 1), ngC = FT / ntC, gC = tid / ntC, tC = tid % ntC;
+    const int ntR = max(L2 >> 3, 1), ngR = FT / ntR, gR = tid / ntR, tR = tid % ntR;
+    const int ntC = max(L1 >> 3, 1), ngC = FT / ntC, gC = tid / ntC, tC = tid % ntC;
     const int ngR_ = ngR, ngC_ = ngC;
     const int PLR = pad8(L2) + 1, PLC = pad8(L1) + 1;  // padded buffer lengths
     // the row pairs of a row pass are the same in every row pass: the CTA's rows of r, z, p, x and delta

@@ -41,8 +41,9 @@ struct FftOpArgs {
     const int* skip;
 };
 
-__device__ __forceinline__ void load_twiddles(double2* dst, const double2* src, int L) {
-    for (int t = threadIdx.x; t < L; t += blockDim.x) dst[t] = src[t];
+// the stage twiddle table (fft_dev.cuh) of length L = 2^lg from the full table exp(-2 pi i k / L)
+__device__ __forceinline__ void load_twiddles(double2* dst, const double2* src, int lg) {
+    fft_stage_twiddles(dst, lg, [&](int k) { return src[k]; });
 }
 
 // row pairs (2p, 2p + 1) of column (level) l of U, forward FFT along the rows, half spectra -> W
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(FFT_T) fftop_rows_fwd(FftOpArgs a) {
     const int L = a.L2, nt = max(L >> 3, 1), ng = FFT_T / nt, PL = pad8(L) + 1;
     double2* tw = smf;
     double2* gb = smf + L;
-    load_twiddles(tw, a.tw2, L);
+    load_twiddles(tw, a.tw2, a.lg2);
     const int tid = threadIdx.x, g = tid / nt, t = tid % nt;
     const long long units = (long long)(a.S + 1) * a.nup;
     const long long u0 = (long long)blockIdx.x * ng;
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(FFT_T) fftop_cols(FftOpArgs a) {
     double2* tw = smf;
     double2* gb = smf + L;
     double* lam = reinterpret_cast<double*>(gb + (size_t)ng * 2 * PL);  // [ng][L]
-    load_twiddles(tw, a.tw1, L);
+    load_twiddles(tw, a.tw1, a.lg1);
     const int tid = threadIdx.x, g = tid / nt, t = tid % nt;
     const int cpl = (a.H2 + ng - 1) / ng;  // column groups per level
     const int l = blockIdx.x / cpl, k0 = (blockIdx.x % cpl) * ng;
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(FFT_T) fftop_rows_inv(FftOpArgs a) {
     const int L = a.L2, nt = max(L >> 3, 1), ng = FFT_T / nt, PL = pad8(L) + 1;
     double2* tw = smf;
     double2* gb = smf + L;
-    load_twiddles(tw, a.tw2, L);
+    load_twiddles(tw, a.tw2, a.lg2);
     const int tid = threadIdx.x, g = tid / nt, t = tid % nt;
     const long long units = (long long)(a.S + 1) * a.nup;
     const long long u0 = (long long)blockIdx.x * ng;
@@ -218,7 +219,7 @@ __global__ void fftop_plain(double2* X, int L, int lg, long long stride, long lo
     const int nt = max(L >> 3, 1), PL = pad8(L) + 1;
     double2* tws = smf;
     double2* gb = smf + L;
-    load_twiddles(tws, tw, L);
+    load_twiddles(tws, tw, lg);
     double2* base = X + (long long)blockIdx.x * step;
     for (int j = threadIdx.x; j < L; j += blockDim.x) gb[pad8(j)] = base[(long long)j * stride];
     __syncthreads();
