@@ -51,6 +51,17 @@ def load_peaks():
         return 6650.0, "fallback B200_PROFILING.md 6.65 TB/s"
 
 
+def load_traffic(kernel, cfg):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture (profiles/r02/ncu_traffic.json) when it
+    was taken on this configuration, else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")) as f:
+            e = json.load(f).get(kernel)
+        return (int(e["bytes"]), "profiles/r02/ncu_traffic.json: " + e["report"]) if e and e["config"] == cfg else (None, None)
+    except Exception:
+        return None, None
+
+
 def load_fp64_peak():
     with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
         p = json.load(f)
@@ -446,7 +457,8 @@ def run_ours(args):
         roof = {"bound": "hbm", "kernel": "tau_pcg_fused (K5: tau-preconditioned CG block solves, one cooperative "
                                           "kernel per P^-1; chain of S+1 dependent levels)",
                 "achieved": round(sweep_bytes / (ms_sweep * 1e-3) / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(sweep_bytes / (ms_sweep * 1e-3) / 1e9 / hbm_peak, 4), "traffic": None,
+                "frac": round(sweep_bytes / (ms_sweep * 1e-3) / 1e9 / hbm_peak, 4),
+                "traffic": load_traffic("tau_pcg_fused", cfg)[0], "traffic_source": load_traffic("tau_pcg_fused", cfg)[1],
                 "bytes_per_launch": sweep_bytes, "ms_per_launch": round(ms_sweep, 4),
                 "us_per_level": round(ms_sweep * 1e3 / (S + 1), 2), "cg_steps_per_level": round(steps_per_level, 2),
                 "passes_per_level": round(passes_per_level, 1),
@@ -465,7 +477,9 @@ def run_ours(args):
         roof = {"bound": "hbm", "kernel": ("hodlr_sweep_kernel (K2h: substitution over HODLR inverses)" if form == "hodlr"
                                            else "sweep_kernel (K2: substitution over packed tiles)"),
                 "achieved": round(sweep_bytes / (ms_sweep * 1e-3) / 1e9, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(sweep_bytes / (ms_sweep * 1e-3) / 1e9 / hbm_peak, 4), "traffic": None,
+                "frac": round(sweep_bytes / (ms_sweep * 1e-3) / 1e9 / hbm_peak, 4),
+                "traffic": load_traffic("hodlr_sweep_kernel", cfg)[0] if form == "hodlr" else None,
+                "traffic_source": load_traffic("hodlr_sweep_kernel", cfg)[1] if form == "hodlr" else None,
                 "bytes_per_launch": sweep_bytes, "ms_per_launch": round(ms_sweep, 4),
                 "us_per_level": round(ms_sweep * 1e3 / (S + 1), 3), "precond_form": form, "peak_source": peak_src}
     del out
@@ -572,6 +586,7 @@ def run_ours(args):
                                   "achieved": round(op_tflops, 3), "peak": fp64_peak, "unit": "TFLOP/s",
                                   "frac": round(op_tflops / fp64_peak, 4), "flops_per_launch": op_flops,
                                   "ms_per_launch": round(ms_op, 4), "peak_source": fp64_src,
+                                  "traffic": load_traffic("toeplitz_apply_kernel", cfg)[0],
                                   "note": "the dense contraction, timed in FI_APPLY_DMMA mode" +
                                           ("; the solve applies A by K1f (operator_fft)" if ms_fft else "")},
             "operator_fft": None if ms_fft is None else {
