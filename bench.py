@@ -545,6 +545,15 @@ def run_ours(args):
                                  "iters_per_s": round(itc / (msc * 1e-3), 3), "setup_s": su,
                                  "precond": Pc.inner if Pc.inner == "pcg" else Pc.form,
                                  "recon_error_vs_fstar": F.relative_error(sp.f_true, xc[-Ac.N:].cpu().numpy())}
+            if not args.no_cpu_baseline:
+                # the CPU restatement of the reference beside it, same box, all host threads (a bounded sample,
+                # extrapolated as for the headline's cpu_baseline)
+                nthr = os.cpu_count() or 1
+                cs_ = cpu_reference_sample(c, repc.iterations, nthr)
+                configs[NAMES[c]]["cpu_oracle"] = {
+                    "iters_per_s": round(cs_["iters_per_s"], 6), "cores": nthr, "kind": "port",
+                    "time_to_solve_s_extrapolated": round(cs_["time_to_solve_s_extrapolated"], 3),
+                    "gpu_speedup": round((itc / (msc * 1e-3)) / cs_["iters_per_s"], 1)}
             del Ac, Pc, bc, xc
             torch.cuda.empty_cache()
 
