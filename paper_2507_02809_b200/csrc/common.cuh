@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -30,9 +31,19 @@ struct Error : std::runtime_error {
     do {                                                                                             \
         cudaError_t e_ = cudaGetLastError();                                                         \
         if (e_ != cudaSuccess)                                                                       \
-            throw ::fib::Error(FI_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_));  \
+            throw ::fib::Error(FI_E_CUDA, std::string("kernel launch (") + __FILE__ + ":" +           \
+                                              std::to_string(__LINE__) + "): " + cudaGetErrorString(e_)); \
         (ctx)->launches++;                                                                           \
     } while (0)
+
+inline int poison_mode() {  // FI_POISON: 1 every buffer, 2 only >= 1 MiB, 3 only < 1 MiB (bisecting)
+    static const int m = std::getenv("FI_POISON") ? std::atoi(std::getenv("FI_POISON")) : 0;
+    return m;
+}
+inline bool poison_allocs(size_t bytes) {
+    const int m = poison_mode();
+    return m == 1 || (m == 2 && bytes >= (1u << 20)) || (m == 3 && bytes < (1u << 20));
+}
 
 // Owning device buffer (cudaMalloc/cudaFree).
 template <class T>
@@ -60,6 +71,15 @@ struct DevBuf {
                                            " bytes failed: " + cudaGetErrorString(e));
         }
         n = count;
+        // FI_POISON (diagnostics; the sanitizer is unavailable on this GPU pool): every new device buffer is
+        // filled with 0xff bytes (NaN as doubles, ~0 as counters), so a kernel that reads scratch it never
+        // wrote, or code that relies on zeroed allocations, shows up as NaN / wrong results in the parity tests
+        // (legacy-stream memset + sync: allowed while another stream captures a graph in relaxed mode, as a
+        // first apply inside the GMRES capture does; any error is cleared rather than left sticky)
+        if (poison_allocs(count * sizeof(T))) {
+            if (cudaMemset(p, 0xff, count * sizeof(T)) == cudaSuccess) cudaStreamSynchronize(0);
+            cudaGetLastError();
+        }
     }
     void release() {
         if (p) cudaFree(p);

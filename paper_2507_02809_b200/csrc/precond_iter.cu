@@ -552,6 +552,18 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                 dst_rows_out(rd);
             }
         }
+        // the level's pad columns (j in [n2, ld2)) of the CTA's rows: zero, like every other kernel's pads (the
+        // CG never touches them; an output buffer's previous contents must not leak into the Krylov vectors)
+        if (ld2 > n2)
+            for (int rd = 0; rd < rdR; ++rd) {
+                const int nae = nact(nuR, ngR, rd);
+                for (int sb = 0; sb < nae; ++sb)
+                    for (int e = tid; e < 2 * (ld2 - n2); e += FT) {
+                        const int hi = e / (ld2 - n2), j = n2 + e % (ld2 - n2);
+                        const int row = 2 * (cta + G * (sb + ngR * rd)) + hi;
+                        if (row < n1) x[(long long)row * ld2 + j] = 0.0;
+                    }
+            }
         sub(27);
         return bn;
     };
