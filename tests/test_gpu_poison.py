@@ -28,7 +28,7 @@ A = F.SystemOperator(spec)
 P = F.BlockTriangularPreconditioner(A, inner="pcg")
 mu = F.add_gaussian_noise(F.forward_solve(A, P).mu, 0.01, 7)
 z = F.build_rhs(A, mu).z
-x, r = F.gmres(A, P, z, F.GmresOptions(1e-10, 0, 50))
+x, r = F.gmres(A, P, z, F.GmresOptions(1e-10, 500, 50))
 print(json.dumps({"it": r.iterations, "conv": r.converged, "f": x[-A.N:].tolist(), "finite": bool(np.isfinite(x).all())}))
 """ % ROOT
 
