@@ -23,7 +23,10 @@
 namespace fib {
 namespace {
 
-constexpr int FFT_T = 256;  // threads per CTA: groups of L/8 threads (4 groups at L = 512)
+#ifndef FI_FFTOP_T
+#define FI_FFTOP_T 128  // 128: 3.37 ms on config 4, 256: 3.48 ms (occupancy: 41 KB of shared memory per CTA)
+#endif
+constexpr int FFT_T = FI_FFTOP_T;  // threads per CTA: groups of L/8 threads (FFT_T / 64 groups at L = 512)
 
 struct FftOpArgs {
     int n1, n2, ld2, S, L1, L2, lg1, lg2, H2, nup;
