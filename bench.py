@@ -506,6 +506,11 @@ def run_ours(args):
     ms_mgs = ms.value
     # algorithmic bytes of MGS step k: 8 n (3 (k + 1) + 3), doubled when the second pass runs
     mgs_bytes = 8 * n * (3 * (k_mgs + 1) + 3) * (2 if reorth.value else 1)
+    # the same at k = 25, the mean Arnoldi step of a GMRES(50) cycle (the unpreconditioned solve's regime)
+    reorth25 = ctypes.c_int()
+    assert lib.fi_mgs_step_timed(ctx.handle, n, 25, max(2, reps // 2), ctypes.byref(ms), ctypes.byref(reorth25)) == 0
+    ms_mgs25 = ms.value
+    mgs_bytes25 = 8 * n * (3 * 26 + 3) * (2 if reorth25.value else 1)
     del y
     # max over ranks for times, sum over ranks for the work done (replicas)
     ms_total_max, iters_all = replica_aggregate(ms_total, total_iters, b_dev.device)
@@ -609,7 +614,11 @@ def run_ours(args):
                                  "bytes_per_launch": mgs_bytes, "ms_per_launch": round(ms_mgs, 5), "k": k_mgs,
                                  "second_pass": bool(reorth.value),
                                  "note": "algorithmic bytes 8 n (3 (k + 1) + 3) (SURVEY 8(d)); the kernel moves "
-                                         "8 n (7 + 4 k) (w read and written every round); L2 flushed before each"},
+                                         "8 n (7 + 4 k) (w read and written every round); L2 flushed before each",
+                                 "k25": {"ms_per_launch": round(ms_mgs25, 4),
+                                         "achieved": round(mgs_bytes25 / (ms_mgs25 * 1e-3) / 1e9, 1),
+                                         "frac": round(mgs_bytes25 / (ms_mgs25 * 1e-3) / 1e9 / hbm_peak, 4),
+                                         "bytes_per_launch": mgs_bytes25, "second_pass": bool(reorth25.value)}},
             "configs": configs,
             "clocks": clocks,
         }
