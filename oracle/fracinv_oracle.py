@@ -42,6 +42,31 @@ import scipy.linalg as sla
 # the thread count).  The reference's FFTW plans are single-threaded (fft.cpp:47-50): set
 # FI_ORACLE_WORKERS=1 for a reference-faithful 1-core timing.
 FFT_WORKERS = int(os.environ.get("FI_ORACLE_WORKERS", "0")) or (os.cpu_count() or 1)
+_POOL = None
+
+
+def _sub_scaled(w: np.ndarray, v: np.ndarray, h: float, tmp: np.ndarray) -> None:
+    """w -= h * v as two separately rounded elementwise passes (multiply, then subtract: the
+    arithmetic of krylov.cpp:130).  Long vectors are cut into FFT_WORKERS slices handled by host
+    threads (numpy releases the GIL); every element sees the same two operations, so the result does
+    not depend on the thread count."""
+    global _POOL
+    n = w.size
+    if FFT_WORKERS == 1 or n < (1 << 22):
+        np.multiply(v, h, out=tmp)
+        np.subtract(w, tmp, out=w)
+        return
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(FFT_WORKERS)
+    step = -(-n // FFT_WORKERS)
+
+    def part(a):
+        b = min(n, a + step)
+        np.multiply(v[a:b], h, out=tmp[a:b])
+        np.subtract(w[a:b], tmp[a:b], out=w[a:b])
+
+    list(_POOL.map(part, range(0, n, step)))
 
 # --------------------------------------------------------------------------- errors
 # errors.hpp:9-43
@@ -728,12 +753,12 @@ class BlockTriangularPreconditioner:
         if self.inner == "pcg":
             x0 = None
             if prev and s <= self.S and self.pcg.warm and not self.pcg.dropped:
-                # polynomial extrapolation through the previous k levels (latest first):
-                # x0 = sum_j (-1)^(j+1) C(k, j) y_(s-j), summed in j order as on the device
-                k = len(prev)
+                # extrapolation through the previous levels (latest first), summed in j order as on the
+                # device: x0 = sum_j w_j y_(s-j), w from TauPCG.warm_weights
+                w = self.pcg.warm_weights(len(prev), s)
                 x0 = np.zeros_like(prev[0])
-                for j in range(1, k + 1):
-                    x0 = x0 + float((-1) ** (j + 1) * math.comb(k, j)) * prev[j - 1]
+                for j in range(1, len(w) + 1):
+                    x0 = x0 + w[j - 1] * prev[j - 1]
             return self.pcg.solve(s, rhs, x0)
         return sla.lu_solve(self._factor(s), rhs, check_finite=False)
 
@@ -749,18 +774,46 @@ class BlockTriangularPreconditioner:
         Y = y[: S * N].reshape(S, N)
         if self.inner == "pcg":
             self.pcg.dropped = False
+            self.pcg.rho = [math.inf, math.inf]
         for s in range(1, S + 1):
             rhs = z[(s - 1) * N: s * N].copy()
             if s > 1:
                 acc = e[s - 1:0:-1] @ Y[: s - 1]  # sum_{m<s} e_{s-m} y^(m)
                 rhs -= self.A.diags.D1[s - 1] * acc
-            Y[s - 1] = self.solve_block(s, rhs, [Y[s - 1 - k] for k in range(1, min(WARM_ORDER, s - 1) + 1)])
+            Y[s - 1] = self.solve_block(s, rhs, [Y[s - 1 - k] for k in range(1, min(LS_WINDOW, s - 1) + 1)])
         rhs = z[S * N:] - Y[S - 1]
         y[S * N:] = self.solve_block(S + 1, rhs)
         return y
 
 
 WARM_ORDER = 6  # previous levels in the tau-PCG initial-guess extrapolation (the device's kWarmOrder)
+LS_WINDOW = 10  # previous levels of the least-squares extrapolation (the device's kLsWindow)
+LS_SWITCH = 64.0  # least-squares weights once a guess's residual is within this factor of the rounding floor
+FLOOR_THETA = 1.0  # stop at theta * u * ||M|| ||x||: the rounding floor of the residual (the device's kFloorTheta)
+_U = 2.0 ** -53
+
+
+def _ls_weights(m: int, d: int):
+    """Weights w_j of y_(s-j), j = 1..m: the value at 0 of the degree-d least-squares polynomial through
+    the points (-j, y_(s-j)).  Exact rational arithmetic, rounded once (the device's kLsCoef literals)."""
+    from fractions import Fraction
+    V = [[Fraction(-(j + 1)) ** k for k in range(d + 1)] for j in range(m)]
+    G = [[sum(V[j][a] * V[j][b] for j in range(m)) for b in range(d + 1)] for a in range(d + 1)]
+    # solve G c = e0 by Gauss-Jordan in rationals; w_j = sum_k V[j][k] c_k
+    n = d + 1
+    aug = [G[i][:] + [Fraction(1 if i == 0 else 0)] for i in range(n)]
+    for i in range(n):
+        piv = next(r for r in range(i, n) if aug[r][i] != 0)
+        aug[i], aug[piv] = aug[piv], aug[i]
+        aug[i] = [v / aug[i][i] for v in aug[i]]
+        for r in range(n):
+            if r != i and aug[r][i] != 0:
+                aug[r] = [a - aug[r][i] * b for a, b in zip(aug[r], aug[i])]
+    c = [aug[i][n] for i in range(n)]
+    return [float(sum(V[j][k] * c[k] for k in range(n))) for j in range(m)]
+
+
+LS_COEF = _ls_weights(LS_WINDOW, WARM_ORDER - 1)
 
 
 class TauPCG:
@@ -790,6 +843,11 @@ class TauPCG:
         self.iterations = []
         self.warm = True  # extrapolated initial guesses for the time levels (the device's FI_TAU_WARM=1)
         self.dropped = False  # set when a guess was worse than zero: no guesses for the rest of the apply
+        # the latest guess of each kind (0 polynomial, 1 least squares): ||r|| / (u ||M|| ||x||)
+        self.rho = [math.inf, math.inf]
+        self.kind = 0
+        self.theta = FLOOR_THETA  # 0: stop on tol ||b|| alone (the device's FI_TAU_FLOOR=0)
+        self.lswin = LS_WINDOW  # 0: polynomial extrapolation on every level (the device's FI_TAU_LSWIN=0)
         S, N = A.steps, A.space_dim
         e0 = A.weights.e[0]
         for s in range(1, S + 1):
@@ -801,6 +859,26 @@ class TauPCG:
         if np.any(A.diags.D2[S - 1] == 0.0):
             raise SingularBlockError(f"precond_build: singular block at time level {S + 1}", S + 1)
 
+    def warm_weights(self, nprev: int, level: int = 0):
+        self._level = level
+        """Weights of the previous nprev (<= LS_WINDOW) levels' solutions, latest first, in the initial
+        guess.  While the systematic error of the extrapolation dominates (early levels: the solution's
+        weak singularity at t = 0): the degree-(k-1) polynomial through the last k = min(nprev, WARM_ORDER)
+        levels, w_j = (-1)^(j+1) C(k, j).  A guess's residual cannot fall below the rounding floor
+        u ||M|| ||x|| of the previous solutions' residuals amplified by ||w||_2 (30.4 for k = 6); when the
+        previous level's guess was within LS_SWITCH of the floor, the degree-5 least-squares polynomial
+        through LS_WINDOW = 10 levels (||w||_2 = 6.1, the same order of accuracy) is used instead."""
+        self.kind = 0
+        if self.lswin and nprev >= LS_WINDOW and self.rho[0] <= LS_SWITCH:
+            # which of the two is better depends on the problem (beta) and the level: every 16 levels each
+            # kind is tried once, in between the kind whose latest guess was closer is used
+            ph = (nprev_level := self._level) % 16
+            self.kind = 1 if ph == 0 else 0 if ph == 8 else int(self.rho[1] < self.rho[0])
+        if self.kind == 1:
+            return LS_COEF
+        k = min(nprev, WARM_ORDER)
+        return [float((-1) ** (j + 1) * math.comb(k, j)) for j in range(1, k + 1)]
+
     def _tau_inv(self, r, lam):
         R = r.reshape(self.n)
         X = self.sf.dstn(R, type=1, norm="ortho")
@@ -809,8 +887,13 @@ class TauPCG:
 
     def solve(self, s: int, rhs: np.ndarray, x0: Optional[np.ndarray] = None) -> np.ndarray:
         """x0 (time levels, EXTENSION identical to the device): an initial guess.  A pre-step sets
-        x = x0, r = b - M x0; the level is done if ||r|| <= tol ||b||, and a guess with ||r|| > ||b||
-        is dropped (x = 0, r = b) before the tau-preconditioned iteration starts."""
+        x = x0, r = b - M x0; the level is done if r passes the stopping test, and a guess with
+        ||r|| > ||b|| is dropped (x = 0, r = b) before the tau-preconditioned iteration starts.
+
+        Stopping test: ||r|| <= max(tol ||b||, theta u ||M|| ||x||), ||M|| taken as the largest tau
+        eigenvalue c max g + mean(delta), u = 2^-53.  The second term is the rounding floor of a residual
+        b - M x evaluated in double: below it the recursive r keeps falling while the true residual does
+        not (measured on config 4: true residual 1.7e-13 ||b|| = 1.0 u ||M|| ||x|| at every level)."""
         A = self.A
         S = A.steps
         e0 = A.weights.e[0]
@@ -824,6 +907,8 @@ class TauPCG:
             c, delta = A.scale_reg, np.zeros(A.space_dim)
         b = rhs / d2
         lam = c * self.g + delta.mean()
+        normM = float(lam.max())
+        floor = self.theta * _U * normM
         M = lambda v: c * A.laplacian.apply(v) + delta * v
         x = np.zeros_like(b)
         bn = np.linalg.norm(b)
@@ -831,10 +916,13 @@ class TauPCG:
             self.iterations.append(0)
             return x
         r = b.copy()
+        if s <= S and x0 is None:
+            self.rho = [math.inf, math.inf]
         if x0 is not None and s <= S:
             x = x0.copy()
             r = b - M(x0)
-            if np.linalg.norm(r) <= self.tol * bn:
+            self.rho[self.kind] = float(np.linalg.norm(r)) / (_U * normM * float(np.linalg.norm(x)))
+            if np.linalg.norm(r) <= max(self.tol * bn, floor * np.linalg.norm(x)):
                 self.iterations.append(0)
                 return x
             if float(r @ r) > float(b @ b):
@@ -850,7 +938,7 @@ class TauPCG:
             alpha = rz / float(p @ Ap)
             x += alpha * p
             r -= alpha * Ap
-            if np.linalg.norm(r) <= self.tol * bn:
+            if np.linalg.norm(r) <= max(self.tol * bn, floor * np.linalg.norm(x)):
                 break
             z = self._tau_inv(r, lam)
             rz_new = float(r @ z)
@@ -934,14 +1022,12 @@ def gmres(apply_A, apply_M_inv, b: np.ndarray, tol: float = 1e-8, maxit: int = 0
             for i in range(k + 1):  # modified Gram-Schmidt (krylov.cpp:127-132)
                 hik = float(V[i] @ w)
                 h[i] += hik
-                np.multiply(V[i], hik, out=tmp)
-                np.subtract(w, tmp, out=w)
+                _sub_scaled(w, V[i], hik, tmp)
             if np.linalg.norm(w) < pre_norm * 0.70710678118654752:  # krylov.cpp:134-140
                 for i in range(k + 1):
                     corr = float(V[i] @ w)
                     h[i] += corr
-                    np.multiply(V[i], corr, out=tmp)
-                    np.subtract(w, tmp, out=w)
+                    _sub_scaled(w, V[i], corr, tmp)
             del tmp
             hnext = float(np.linalg.norm(w))
             h[k + 1] = hnext

@@ -37,6 +37,7 @@ struct fi_precond {
     int it_maxit = 200;
     int it_L1 = 0, it_L2 = 0;
     std::vector<double> it_dmean;
+    double it_gmax = 0.0;  // largest tau eigenvalue g(theta)
     std::vector<int> it_direct;
     fib::DevBuf<double2> it_tw1, it_tw2, it_X;
     fib::DevBuf<double> it_lamT, it_lamB, it_Rr, it_vec, it_dmean_d, it_hb;

@@ -34,6 +34,16 @@ __constant__ double kWarmCoef[kWarmOrder + 1][kWarmOrder + 1] = {
     {0, 0, 0, 0, 0, 0, 0},          {0, 1, 0, 0, 0, 0, 0},           {0, 2, -1, 0, 0, 0, 0},
     {0, 3, -3, 1, 0, 0, 0},         {0, 4, -6, 4, -1, 0, 0},         {0, 5, -10, 10, -5, 1, 0},
     {0, 6, -15, 20, -15, 6, -1}};
+// A guess's residual cannot fall below the rounding floor u ||M|| ||x|| of the previous solutions' residuals
+// amplified by ||w||_2 (30.4 for the six binomial weights).  Once a polynomial guess has come within kLsSwitch
+// of the floor, the degree-5 least-squares polynomial through the previous kLsWindow = 10 levels (||w||_2 = 6.1,
+// the same order of accuracy, a larger error constant) competes with it: every 16 levels each kind is tried
+// once, in between the kind whose latest guess was closer to the floor is used (oracle: TauPCG.warm_weights).
+// The weights: exact rationals rounded once (oracle: _ls_weights(10, 5)).
+constexpr int kLsWindow = 10;
+constexpr double kLsSwitch = 64.0;
+__constant__ double kLsCoef[kLsWindow] = {3.6, -3.4, -1.0666666666666667, 1.6, 1.6, -0.26666666666666666,
+                                          -1.6, -0.6, 1.7333333333333334, -0.6};
 
 struct ItArgs {
     int n1, n2, ld2, L1, L2, lg1, lg2, S, levels, maxit;
@@ -62,6 +72,9 @@ struct ItArgs {
     double* Rr;   // n1 x n2 real DST work
     const int* skip;
     int warm;    // extrapolated initial guesses for the time levels (FI_TAU_WARM, default 1)
+    int lswin;   // least-squares window for the guesses of the noise-dominated levels (FI_TAU_LSWIN, default 1)
+    double gmax; // largest tau eigenvalue g(theta): ||M|| is taken as c gmax + mean(delta)
+    double floor_u; // theta 2^-53: a level stops at ||r|| <= max(tol ||b||, floor_u ||M|| ||x||) (FI_TAU_FLOOR = theta)
     int cu, cus; // B column pass: adjacent columns per CTA and round (a power of two <= the groups), log2
 };
 
@@ -425,7 +438,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     // ---- the passes
     // R0: level setup of the CTA's rows: history, b = rhs / D2 (r = zz = b), x0 -> p, x; then F2(x0) -> Zh
     // (warm start) or S2(b) -> Rr (from zero).  Returns the partial ||b||^2.
-    auto passR0 = [&](int lv, bool direct, bool warm, int kx) -> double {
+    auto passR0 = [&](int lv, bool direct, bool warm, int kx, bool ls) -> double {
         double bn = 0.0;
         double* x = a.y + (long long)lv * Np;
         const int B0 = lv & ~7, jt = lv & 7, nrec = lv - B0;
@@ -491,9 +504,9 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                         const double zv = a.z_in[(tl ? (long long)lv * Np : (long long)a.S * Np) + o];
                         const double d1 = a.D1[lo + o], d2i = a.d2inv[lo + o];
                         const double yprev = a.y[(long long)max(lv - 1, 0) * Np + o];
-                        double yw[kWarmOrder];
+                        double yw[kLsWindow];
 #pragma unroll
-                        for (int jj = 0; jj < kWarmOrder; ++jj) yw[jj] = a.y[(long long)max(lv - 1 - jj, 0) * Np + o];
+                        for (int jj = 0; jj < kLsWindow; ++jj) yw[jj] = a.y[(long long)max(lv - 1 - jj, 0) * Np + o];
                         double b = 0.0, xv = 0.0, x0 = 0.0;
                         if (tl) {
                             double hist = B0 > 0 ? hbv : 0.0;
@@ -508,10 +521,13 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                         }
                         // initial guess of the time levels: the polynomial extrapolation through the previous
                         // kx levels' solutions, x0 = sum_j (-1)^(j+1) C(kx, j) y_(lv-j)
+                        // (noise-dominated levels: the least-squares weights over kLsWindow levels)
                         if (warm) {
 #pragma unroll
-                            for (int jj = 0; jj < kWarmOrder; ++jj)
-                                if (jj < kx) x0 += kWarmCoef[kx][jj + 1] * yw[jj];
+                            for (int jj = 0; jj < kLsWindow; ++jj) {
+                                const double wj = ls ? kLsCoef[jj] : (jj < kWarmOrder ? kWarmCoef[kx][jj + 1] : 0.0);
+                                if (ls || jj < kx) x0 += wj * yw[jj];
+                            }
                         }
                         bq[q] = okq[q] ? b : 0.0;
                         x0q[q] = okq[q] ? x0 : 0.0;
@@ -640,10 +656,11 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     };
     // B3: inverse row FFT of the Yb row pairs -> B p; p = zz + beta p (cg) or p as is (pre-step); Ap = c Bp +
     // delta p; x += alpha p; r -= alpha Ap; partial ||r||^2; S2(r) -> Rr
-    auto passB3 = [&](int lv, double c, double alpha, double beta, bool cg) -> double {
+    auto passB3 = [&](int lv, double c, double alpha, double beta, bool cg, double& xx) -> double {
         const long long lo = (long long)min(lv, a.S - 1) * Np;
         double* x = a.y + (long long)lv * Np;
         double part = 0.0;
+        xx = 0.0;
         for (int rd = 0; rd < rdR; ++rd) {
             const int lim = nact(nuR, ngR, rd) * L2;
             for (int base = 0; base < lim; base += UF * FT) {
@@ -721,6 +738,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                             rv = rq[q] - alpha * ap;
                             vrow(ou, V_R)[li] = rv;
                             part += rv * rv;
+                            xx += xv * xv;
                         }
                         // the DST input of the new r straight from registers: odd extension of the row,
                         // r_j at j + 1 and -r_j at L2 - 1 - j (row i0 in .x, row i1 in .y)
@@ -883,8 +901,11 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     enum { PH_SETUP, PH_B2, PH_B3, PH_FALLBACK, PH_T2, PH_T3 };
     bool warm_ok = true;
     int lv = 0, phase = PH_SETUP, it = 0, kx = 0;
-    bool direct = false, warm = false, pre = false, first_t3 = true;
+    bool direct = false, warm = false, pre = false, first_t3 = true, ls = false;
     double bn2 = 0.0, c = 0.0, rz = 0.0, pdp = 0.0, beta = 0.0, alpha = 0.0;
+    // the latest guess of each kind (0 polynomial, 1 least squares): ||r|| / (u ||M|| ||x||); inf: none yet
+    double rho0 = INFINITY, rho1 = INFINITY;
+    double floor_c = 0.0, unorm = 0.0;  // floor_u ||M|| and u ||M|| of the level
     double red[kRedMax];
     auto level_done = [&](bool cg, bool conv) {
         if (cg && ctl.stats && cta == 0 && tid == 0) {
@@ -902,7 +923,14 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             kx = min(lv, kWarmOrder);
             warm = a.warm && warm_ok && lv >= 1 && lv < a.S && !direct;
             for (int j = 1; j <= kx; ++j) warm = warm && !a.direct[lv - j];
-            red[0] = passR0(lv, direct, warm, kx);
+            ls = warm && a.lswin && lv >= kLsWindow && rho0 <= kLsSwitch;
+            if (ls)
+                for (int j = kx + 1; j <= kLsWindow; ++j) ls = ls && !a.direct[lv - j];
+            if (ls) {
+                const int ph = (lv + 1) & 15;
+                ls = ph == 0 ? true : ph == 8 ? false : rho1 < rho0;
+            }
+            red[0] = passR0(lv, direct, warm, kx, ls);
             greduce(red, 1);
             bn2 = red[0];
             stamp(0);
@@ -911,6 +939,9 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                 continue;
             }
             c = level_c(a, lv);
+            unorm = 0x1p-53 * __dadd_rn(__dmul_rn(c, a.gmax), level_dmean(a, lv));
+            floor_c = a.floor_u * 0x1p53 * unorm;
+            if (lv < a.S && !warm) rho0 = rho1 = INFINITY;
             it = 0;
             first_t3 = true;
             // warm start: a pre-step with alpha = 1 along p = x0 gives x = x0, r = b - M x0
@@ -928,12 +959,14 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             stamp(4);
             phase = PH_B3;
         } else if (phase == PH_B3) {
-            red[0] = pre ? passB3(lv, c, 1.0, 0.0, false) : passB3(lv, c, alpha, beta, true);
-            greduce(red, 1);
+            red[0] = pre ? passB3(lv, c, 1.0, 0.0, false, red[1]) : passB3(lv, c, alpha, beta, true, red[1]);
+            greduce(red, 2);
             stamp(5);
-            const bool conv = sqrt(red[0]) <= a.tol * sqrt(bn2);
+            // stop at tol ||b||, or at the rounding floor of a residual evaluated in double, u ||M|| ||x||
+            const bool conv = sqrt(red[0]) <= fmax(a.tol * sqrt(bn2), floor_c * sqrt(red[1]));
             if (pre) {
                 pre = false;
+                (ls ? rho1 : rho0) = sqrt(red[0]) / (unorm * sqrt(red[1]));
                 if (conv) {  // the guess already solves the level
                     level_done(true, true);
                     continue;
@@ -1032,6 +1065,11 @@ ItArgs make_args(fi_precond* P) {
     a.hb = P->it_hb.p;
     static const int warm = std::getenv("FI_TAU_WARM") ? std::atoi(std::getenv("FI_TAU_WARM")) : 1;
     a.warm = warm;
+    static const int lswin = std::getenv("FI_TAU_LSWIN") ? std::atoi(std::getenv("FI_TAU_LSWIN")) : 1;
+    a.lswin = lswin;
+    static const double theta = std::getenv("FI_TAU_FLOOR") ? std::atof(std::getenv("FI_TAU_FLOOR")) : 1.0;
+    a.floor_u = theta * 0x1p-53;  // (times 2^53 u ||M|| in the kernel: exact scalings)
+    a.gmax = P->it_gmax;
     a.Rr = P->it_Rr.p;
     return a;
 }
@@ -1119,6 +1157,7 @@ void precond_build_iterative(fi_precond* P, double tol, int maxit) {
             const double s1 = std::sin(j1 * M_PI / (L.n1 + 1) / 2.0), s2 = std::sin(j2 * M_PI / (L.n2 + 1) / 2.0);
             lamT[(size_t)(j1 - 1) * L.n2 + (j2 - 1)] = std::pow(4.0 * s1 * s1 + 4.0 * s2 * s2, omega_half);
         }
+    P->it_gmax = *std::max_element(lamT.begin(), lamT.end());
     P->it_lamT.alloc(lamT.size());
     FI_CUDA(cudaMemcpy(P->it_lamT.p, lamT.data(), lamT.size() * sizeof(double), cudaMemcpyHostToDevice));
     P->it_X.alloc((size_t)L1 * L2);

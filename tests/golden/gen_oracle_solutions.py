@@ -59,9 +59,48 @@ def run(cfg, precond=True):
           f"solve {t2 - t1:.1f}s -> {name}", flush=True)
 
 
+def run_unprec_resumable(cfg, maxit=2000):
+    """The unpreconditioned GMRES(50) solve, one restart cycle per oracle call.
+
+    O.gmres(x0=x, maxit=RESTART, restart=RESTART) is exactly one cycle of the oracle's GMRES(m): the same
+    r = b - A x at the start, the same Arnoldi loop and x update (the first history entry of a
+    continued call repeats the restart residual and is dropped).  After every cycle x and the history
+    go to scratch/unprec<cfg>_ckpt.npz, so an interrupted run resumes; every 10 cycles and at the end the
+    golden tests/golden/oracle_config<cfg>_unprec.npz is (re)written with `maxit` = the iterations it
+    covers (the GPU test runs the device solve to the same maxit).
+    """
+    A = O.SystemOperator(baseline_problem(O, cfg))
+    mu_eps = np.load(os.path.join(HERE, f"oracle_config{cfg}.npz"))["mu_eps"]
+    z = O.build_rhs(A, mu_eps).z
+    os.makedirs(os.path.join(ROOT, "scratch"), exist_ok=True)
+    ckpt = os.path.join(ROOT, "scratch", f"unprec{cfg}_ckpt.npz")
+    x, hist, iters, spent = None, [], 0, 0.0
+    if os.path.exists(ckpt):
+        c = np.load(ckpt)
+        x, hist, iters, spent = c["x"], list(c["history"]), int(c["iterations"]), float(c["solve_s"])
+        print(f"resuming at {iters} iterations ({spent:.0f}s so far)", flush=True)
+    converged = False
+    ftr = float("nan")
+    while iters < maxit and not converged:
+        t1 = time.time()
+        x, rep = O.gmres(A.apply, None, z, tol=TOL[cfg], restart=RESTART, maxit=min(RESTART, maxit - iters), x0=x)
+        hist += rep.residual_history if not hist else rep.residual_history[1:]
+        iters += rep.iterations
+        converged, ftr = rep.converged, rep.final_true_residual
+        spent += time.time() - t1
+        np.savez(ckpt, x=x, history=np.array(hist), iterations=iters, solve_s=spent)
+        print(f"  config {cfg} unpreconditioned: {iters} iterations, history {hist[-1]:.6e}, true residual "
+              f"{ftr:.6e}, {spent:.0f}s", flush=True)
+        if converged or iters >= maxit or (iters // RESTART) % 10 == 0:
+            np.savez_compressed(os.path.join(HERE, f"oracle_config{cfg}_unprec.npz"), mu_eps=mu_eps, f=x[-A.N:],
+                                iterations=iters, maxit=iters, history=np.array(hist), final_true_residual=ftr,
+                                converged=converged, recon_error=O.relative_error(A.spec.f_true, x[-A.N:]),
+                                setup_s=0.0, solve_s=spent, inner="none")
+
+
 if __name__ == "__main__":
     for arg in sys.argv[1:]:
         if arg.endswith("u"):
-            run(int(arg[:-1]), precond=False)
+            run_unprec_resumable(int(arg[:-1]))
         else:
             run(int(arg))

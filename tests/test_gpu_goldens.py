@@ -85,7 +85,9 @@ def test_unpreconditioned_config4_matches_oracle_golden():
     g = np.load(path)
     A = F.SystemOperator(baseline_problem(F, 4))
     z = F.build_rhs(A, g["mu_eps"]).z
-    x, rep = F.gmres(A, None, z, F.GmresOptions(TOL[4], 2000, RESTART))
+    # the golden records how many iterations the oracle's run covers (2000 = BASELINE's cap)
+    maxit = int(g["maxit"]) if "maxit" in g.files else 2000
+    x, rep = F.gmres(A, None, z, F.GmresOptions(TOL[4], maxit, RESTART))
     f = x[-A.N:]
     h, ho = np.asarray(rep.residual_history), np.asarray(g["history"])
     print(f"config4 unpreconditioned: {rep.iterations} iterations (oracle {int(g['iterations'])}), converged "
