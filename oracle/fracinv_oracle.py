@@ -774,7 +774,7 @@ class BlockTriangularPreconditioner:
         Y = y[: S * N].reshape(S, N)
         if self.inner == "pcg":
             self.pcg.dropped = False
-            self.pcg.rho = [math.inf, math.inf]
+            self.pcg.rho = [math.inf] * 4
         for s in range(1, S + 1):
             rhs = z[(s - 1) * N: s * N].copy()
             if s > 1:
@@ -788,7 +788,6 @@ class BlockTriangularPreconditioner:
 
 WARM_ORDER = 6  # previous levels in the tau-PCG initial-guess extrapolation (the device's kWarmOrder)
 LS_WINDOW = 10  # previous levels of the least-squares extrapolation (the device's kLsWindow)
-LS_SWITCH = 64.0  # least-squares weights once a guess's residual is within this factor of the rounding floor
 FLOOR_THETA = 1.0  # stop at theta * u * ||M|| ||x||: the rounding floor of the residual (the device's kFloorTheta)
 _U = 2.0 ** -53
 
@@ -823,8 +822,9 @@ class TauPCG:
     G_f = cr D2_S B (f-block, delta = 0).  Solved as M y = r / D2 with M = c B + diag(delta) SPD, by
     CG preconditioned with the tau matrix  tau^{-1} = S diag(1/(c g(theta_j) + mean(delta))) S,
     S the orthonormal DST-I, g the symbol (sum_i 4 sin^2(theta_i/2))^{w/2} at theta_j = j pi/(n+1).
-    x0 = 0; stop when ||r_k|| <= tol ||b|| (2-norm) or after maxit steps.  The device (precond_iter.cu)
-    runs the same recurrence in the same order of operations.
+    x0 = 0 or the extrapolation through the previous levels (warm_weights); stop when
+    ||r_k|| <= max(tol ||b||, u ||M|| ||x_k||) (2-norms; solve()) or after maxit steps.  The device
+    (precond_iter.cu) runs the same recurrence in the same order of operations.
     """
 
     def __init__(self, A: SystemOperator, tol: float = 1e-14, maxit: int = 200):
@@ -844,7 +844,7 @@ class TauPCG:
         self.warm = True  # extrapolated initial guesses for the time levels (the device's FI_TAU_WARM=1)
         self.dropped = False  # set when a guess was worse than zero: no guesses for the rest of the apply
         # the latest guess of each kind (0 polynomial, 1 least squares): ||r|| / (u ||M|| ||x||)
-        self.rho = [math.inf, math.inf]
+        self.rho = [math.inf] * 4
         self.kind = 0
         self.theta = FLOOR_THETA  # 0: stop on tol ||b|| alone (the device's FI_TAU_FLOOR=0)
         self.lswin = LS_WINDOW  # 0: polynomial extrapolation on every level (the device's FI_TAU_LSWIN=0)
@@ -860,23 +860,30 @@ class TauPCG:
             raise SingularBlockError(f"precond_build: singular block at time level {S + 1}", S + 1)
 
     def warm_weights(self, nprev: int, level: int = 0):
-        self._level = level
         """Weights of the previous nprev (<= LS_WINDOW) levels' solutions, latest first, in the initial
-        guess.  While the systematic error of the extrapolation dominates (early levels: the solution's
-        weak singularity at t = 0): the degree-(k-1) polynomial through the last k = min(nprev, WARM_ORDER)
-        levels, w_j = (-1)^(j+1) C(k, j).  A guess's residual cannot fall below the rounding floor
-        u ||M|| ||x|| of the previous solutions' residuals amplified by ||w||_2 (30.4 for k = 6); when the
-        previous level's guess was within LS_SWITCH of the floor, the degree-5 least-squares polynomial
-        through LS_WINDOW = 10 levels (||w||_2 = 6.1, the same order of accuracy) is used instead."""
+        guess of time level `level` (1-based).  Four kinds of guess compete:
+          0  the polynomial through the last min(nprev, 6) levels, w_j = (-1)^(j+1) C(k, j)   ||w||_2 = 30.4
+          1  the polynomial through the last 8 levels                                           ||w||_2 = 113
+          2  the polynomial through the last 10 levels                                          ||w||_2 = 430
+          3  the degree-5 least-squares polynomial through the last 10 levels                  ||w||_2 = 6.1
+        A guess's residual is the extrapolation's truncation error (large near the solution's weak
+        singularity at t = 0, falling like level^-order) plus the rounding floor u ||M|| ||x|| of the
+        previous solutions' residuals amplified by ||w||_2: high orders win on the early levels, low
+        noise on the late ones, and where the change happens depends on beta and the input.  So the kind
+        is chosen by measurement: on the levels e, e+1, e+2, e+3 with e = 2^j or 3 2^(j-1) >= 16 each kind
+        is tried once (kind = level - e); on every other level the kind whose latest guess was closest to
+        the floor (rho, set in solve()) is used.  Until the first trial (level < 16) kind 0 is used."""
         self.kind = 0
-        if self.lswin and nprev >= LS_WINDOW and self.rho[0] <= LS_SWITCH:
-            # which of the two is better depends on the problem (beta) and the level: every 16 levels each
-            # kind is tried once, in between the kind whose latest guess was closer is used
-            ph = (nprev_level := self._level) % 16
-            self.kind = 1 if ph == 0 else 0 if ph == 8 else int(self.rho[1] < self.rho[0])
-        if self.kind == 1:
+        if self.lswin and nprev >= LS_WINDOW:
+            hb = 1 << (level.bit_length() - 1)
+            e = hb + hb // 2 if level >= hb + hb // 2 else hb
+            if level >= 16 and level - e < 4:
+                self.kind = level - e
+            else:
+                self.kind = min(range(4), key=lambda k: self.rho[k])  # ties: the lowest kind
+        if self.kind == 3:
             return LS_COEF
-        k = min(nprev, WARM_ORDER)
+        k = min(nprev, (WARM_ORDER, 8, 10)[self.kind])
         return [float((-1) ** (j + 1) * math.comb(k, j)) for j in range(1, k + 1)]
 
     def _tau_inv(self, r, lam):
@@ -917,7 +924,7 @@ class TauPCG:
             return x
         r = b.copy()
         if s <= S and x0 is None:
-            self.rho = [math.inf, math.inf]
+            self.rho = [math.inf] * 4
         if x0 is not None and s <= S:
             x = x0.copy()
             r = b - M(x0)

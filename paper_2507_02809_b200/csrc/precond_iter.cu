@@ -27,21 +27,32 @@ namespace {
 
 constexpr int CB = 4;   // columns per CTA of the setup column FFT (spectrum of B)
 
-// warm start: extrapolation order (previous levels used) and the coefficients
-// (-1)^(j+1) C(k, j) of the degree-(k-1) polynomial through them
+// Warm start: the initial guess of a time level is an extrapolation through the previous levels' solutions.
+// kWarmCoef[k][j] = (-1)^(j+1) C(k, j): the degree-(k-1) polynomial through the last k levels; kLsCoef: the
+// degree-5 least-squares polynomial through the last kLsWindow = 10 levels (exact rationals rounded once;
+// oracle: _ls_weights(10, 5)).  Four kinds of guess compete (oracle: TauPCG.warm_weights):
+//   0  polynomial through min(level, 6) levels   ||w||_2 = 30.4      2  polynomial through 10 levels   430
+//   1  polynomial through 8 levels               113                 3  least squares over 10 levels   6.1
+// A guess's residual is the extrapolation's truncation error (large near the solution's weak singularity at
+// t = 0, falling like level^-order) plus the rounding floor u ||M|| ||x|| of the previous solutions' residuals
+// amplified by ||w||_2: high orders win on the early levels, low noise on the late ones, and where the change
+// happens depends on beta and the input.  So the kind is chosen by measurement: on the (1-based) levels
+// e .. e+3 with e = 2^j or 3 2^(j-1) >= 16 each kind is tried once; on every other level the kind whose latest
+// guess was closest to the floor is used.
 constexpr int kWarmOrder = 6;
-__constant__ double kWarmCoef[kWarmOrder + 1][kWarmOrder + 1] = {
-    {0, 0, 0, 0, 0, 0, 0},          {0, 1, 0, 0, 0, 0, 0},           {0, 2, -1, 0, 0, 0, 0},
-    {0, 3, -3, 1, 0, 0, 0},         {0, 4, -6, 4, -1, 0, 0},         {0, 5, -10, 10, -5, 1, 0},
-    {0, 6, -15, 20, -15, 6, -1}};
-// A guess's residual cannot fall below the rounding floor u ||M|| ||x|| of the previous solutions' residuals
-// amplified by ||w||_2 (30.4 for the six binomial weights).  Once a polynomial guess has come within kLsSwitch
-// of the floor, the degree-5 least-squares polynomial through the previous kLsWindow = 10 levels (||w||_2 = 6.1,
-// the same order of accuracy, a larger error constant) competes with it: every 16 levels each kind is tried
-// once, in between the kind whose latest guess was closer to the floor is used (oracle: TauPCG.warm_weights).
-// The weights: exact rationals rounded once (oracle: _ls_weights(10, 5)).
 constexpr int kLsWindow = 10;
-constexpr double kLsSwitch = 64.0;
+__constant__ double kWarmCoef[kLsWindow + 1][kLsWindow + 1] = {
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 2, -1, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 3, -3, 1, 0, 0, 0, 0, 0, 0, 0},
+    {0, 4, -6, 4, -1, 0, 0, 0, 0, 0, 0},
+    {0, 5, -10, 10, -5, 1, 0, 0, 0, 0, 0},
+    {0, 6, -15, 20, -15, 6, -1, 0, 0, 0, 0},
+    {0, 7, -21, 35, -35, 21, -7, 1, 0, 0, 0},
+    {0, 8, -28, 56, -70, 56, -28, 8, -1, 0, 0},
+    {0, 9, -36, 84, -126, 126, -84, 36, -9, 1, 0},
+    {0, 10, -45, 120, -210, 252, -210, 120, -45, 10, -1}};
 __constant__ double kLsCoef[kLsWindow] = {3.6, -3.4, -1.0666666666666667, 1.6, 1.6, -0.26666666666666666,
                                           -1.6, -0.6, 1.7333333333333334, -0.6};
 
@@ -525,7 +536,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
                         if (warm) {
 #pragma unroll
                             for (int jj = 0; jj < kLsWindow; ++jj) {
-                                const double wj = ls ? kLsCoef[jj] : (jj < kWarmOrder ? kWarmCoef[kx][jj + 1] : 0.0);
+                                const double wj = ls ? kLsCoef[jj] : kWarmCoef[kx][jj + 1];
                                 if (ls || jj < kx) x0 += wj * yw[jj];
                             }
                         }
@@ -903,8 +914,9 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
     int lv = 0, phase = PH_SETUP, it = 0, kx = 0;
     bool direct = false, warm = false, pre = false, first_t3 = true, ls = false;
     double bn2 = 0.0, c = 0.0, rz = 0.0, pdp = 0.0, beta = 0.0, alpha = 0.0;
-    // the latest guess of each kind (0 polynomial, 1 least squares): ||r|| / (u ||M|| ||x||); inf: none yet
-    double rho0 = INFINITY, rho1 = INFINITY;
+    // the latest guess of each kind: ||r|| / (u ||M|| ||x||); inf: none yet
+    double rho0 = INFINITY, rho1 = INFINITY, rho2 = INFINITY, rho3 = INFINITY;
+    int kind = 0;
     double floor_c = 0.0, unorm = 0.0;  // floor_u ||M|| and u ||M|| of the level
     double red[kRedMax];
     auto level_done = [&](bool cg, bool conv) {
@@ -923,13 +935,25 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             kx = min(lv, kWarmOrder);
             warm = a.warm && warm_ok && lv >= 1 && lv < a.S && !direct;
             for (int j = 1; j <= kx; ++j) warm = warm && !a.direct[lv - j];
-            ls = warm && a.lswin && lv >= kLsWindow && rho0 <= kLsSwitch;
-            if (ls)
-                for (int j = kx + 1; j <= kLsWindow; ++j) ls = ls && !a.direct[lv - j];
-            if (ls) {
-                const int ph = (lv + 1) & 15;
-                ls = ph == 0 ? true : ph == 8 ? false : rho1 < rho0;
+            bool wide = warm && a.lswin && lv >= kLsWindow;
+            if (wide)
+                for (int j = kx + 1; j <= kLsWindow; ++j) wide = wide && !a.direct[lv - j];
+            kind = 0;
+            if (wide) {
+                const int level = lv + 1, hb = 1 << (31 - __clz(level));
+                const int e = level >= hb + hb / 2 ? hb + hb / 2 : hb;
+                if (level >= 16 && level - e < 4) {
+                    kind = level - e;  // the trial levels
+                } else {               // the kind closest to the floor (ties: the lowest kind)
+                    double best = rho0;
+                    if (rho1 < best) { best = rho1; kind = 1; }
+                    if (rho2 < best) { best = rho2; kind = 2; }
+                    if (rho3 < best) { best = rho3; kind = 3; }
+                }
             }
+            ls = kind == 3;
+            if (kind == 1) kx = 8;
+            if (kind == 2) kx = 10;
             red[0] = passR0(lv, direct, warm, kx, ls);
             greduce(red, 1);
             bn2 = red[0];
@@ -941,7 +965,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             c = level_c(a, lv);
             unorm = 0x1p-53 * __dadd_rn(__dmul_rn(c, a.gmax), level_dmean(a, lv));
             floor_c = a.floor_u * 0x1p53 * unorm;
-            if (lv < a.S && !warm) rho0 = rho1 = INFINITY;
+            if (lv < a.S && !warm) rho0 = rho1 = rho2 = rho3 = INFINITY;
             it = 0;
             first_t3 = true;
             // warm start: a pre-step with alpha = 1 along p = x0 gives x = x0, r = b - M x0
@@ -966,7 +990,11 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             const bool conv = sqrt(red[0]) <= fmax(a.tol * sqrt(bn2), floor_c * sqrt(red[1]));
             if (pre) {
                 pre = false;
-                (ls ? rho1 : rho0) = sqrt(red[0]) / (unorm * sqrt(red[1]));
+                const double rho = sqrt(red[0]) / (unorm * sqrt(red[1]));
+                if (kind == 0) rho0 = rho;
+                else if (kind == 1) rho1 = rho;
+                else if (kind == 2) rho2 = rho;
+                else rho3 = rho;
                 if (conv) {  // the guess already solves the level
                     level_done(true, true);
                     continue;
