@@ -119,7 +119,8 @@ int fi_system_apply_host(fi_system* sys, const double* y_host, double* z_host);
 int fi_precond_create(fi_system* sys, long long block_cap, fi_precond** out);
 /* Explicit choice of the per-block solve.  inner = 0: dense (the reference's direct solve, above
  * block_cap -> FI_E_RESOURCE); inner = 1: tau-preconditioned CG per block to relative residual
- * `tol` (at most `maxit` steps) — the substituted solve for 2D blocks beyond the cap (needs
+ * `tol`, or to the rounding floor of a residual evaluated in double, u ||M|| ||x||, where that is
+ * larger (at most `maxit` steps) — the substituted solve for 2D blocks beyond the cap (needs
  * n_i + 1 a power of two); inner = -1: what fi_precond_create does (dense up to block_cap, tau-PCG
  * above it for 2D). */
 int fi_precond_create_ex(fi_system* sys, long long block_cap, int inner, double tol, int maxit, fi_precond** out);
