@@ -928,6 +928,30 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
         ++lv;
         phase = PH_SETUP;
     };
+    {
+        // Leading time levels with a zero right-hand side have y = 0 (GMRES applies P^-1 to b = [0; ..; mu]
+        // first): find the first time level with a nonzero entry in one streaming pass (a thread stops at its
+        // first nonzero: four loads per thread on a dense input), zero y below it and start at the 8-level
+        // block it lies in (the blocked history is formed at block starts).
+        const int ntl = min(a.S, a.levels);
+        const long long nt = (long long)ntl * Np, st4 = (long long)G * FT;
+        unsigned m = 0;  // S - level of the thread's first nonzero entry
+        for (long long i = (long long)cta * FT + tid; i < nt && m == 0; i += 4 * st4) {
+            double v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = a.z_in[min(i + q * st4, nt - 1)];
+#pragma unroll
+            for (int q = 3; q >= 0; --q)
+                if (i + q * st4 < nt && v[q] != 0.0) m = (unsigned)(a.S - (int)((i + q * st4) / Np));
+        }
+        for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+        if (lane == 0 && m) atomicMax(ctl.bar + 1, m);
+        gsync();
+        const int s0 = a.S - (int)__ldcg(ctl.bar + 1);
+        lv = min(s0, ntl) & ~7;
+        for (long long i = (long long)cta * FT + tid; i < (long long)lv * Np; i += st4) a.y[i] = 0.0;
+        if (lv > 0) gsync();
+    }
     while (lv < a.levels) {
         if (phase == PH_SETUP) {
             // ---- level setup: rhs (forward substitution, krylov.cpp:55-68), b = rhs / D2, initial guess
@@ -1233,7 +1257,7 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
         P->it_fgrid = g;
         P->it_cu = cu;
         P->it_fparts.alloc((size_t)2 * kRedMax * g);
-        P->it_fbar.alloc(1);
+        P->it_fbar.alloc(2);  // the grid barrier's counter; S - the first time level with a nonzero input
     }
     a.cu = P->it_cu;
     a.cus = ilog2(a.cu);
@@ -1258,7 +1282,7 @@ void precond_apply_iterative(fi_ctx* ctx, fi_precond* P, const double* z, double
         FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
     }
     FusedCtl ctl{P->it_fbar.p, P->it_fparts.p, tracing ? trace.p : nullptr, P->it_stats.p};
-    FI_CUDA(cudaMemsetAsync(P->it_fbar.p, 0, sizeof(unsigned), ctx->stream));
+    FI_CUDA(cudaMemsetAsync(P->it_fbar.p, 0, 2 * sizeof(unsigned), ctx->stream));
     void* args[] = {&a, &ctl};
     FI_CUDA(cudaLaunchCooperativeKernel((const void*)tau_pcg_fused, dim3(P->it_fgrid), dim3(FT), args, smem,
                                         ctx->stream));
