@@ -96,3 +96,30 @@ def test_config2_forward_solve_parity():
     mu, muo = F.forward_solve(A, P).mu, O.forward_solve(Ao, P=Po).mu
     print(f"config2 forward solve parity {_rel(mu, muo):.3e}")
     assert _rel(mu, muo) <= 1e-12
+
+
+def test_tau_pcg_guesses_and_floor_on_a_smooth_input():
+    """The input a solve feeds P^-1 (smooth in time: the guesses are used, every kind is tried on the trial
+    levels, levels stop at the rounding floor): device against the oracle's tau-PCG and the reference's LU block
+    solves (krylov.cpp:48-70); CG steps as the oracle's."""
+    from test_oracle_taupcg import arnoldi_like_input, smooth_problem
+    A, Ao = F.SystemOperator(smooth_problem(F)), O.SystemOperator(smooth_problem(O))
+    P = F.BlockTriangularPreconditioner(A, inner="pcg")
+    Po, Pl = O.BlockTriangularPreconditioner(Ao, inner="pcg"), O.BlockTriangularPreconditioner(Ao, inner="lu")
+    u = arnoldi_like_input(Ao)
+    P.stats(reset=True)
+    y = P.apply(u)
+    st = P.stats()
+    yo, yl = Po.apply(u), Pl.apply(u)
+    so = sum(Po.pcg.iterations)
+    print(f"smooth input: device vs oracle tau-PCG {_rel(y, yo):.3e}, vs LU {_rel(y, yl):.3e}, CG steps device "
+          f"{st['cg_steps']} / oracle {so}")
+    assert _rel(y, yo) <= 1e-12 and _rel(y, yl) <= 1e-12
+    assert st["nonconverged_blocks"] == 0 and not Po.pcg.dropped
+    assert abs(st["cg_steps"] - so) <= max(3, 0.05 * so)
+    # leading zero levels (GMRES's first apply: b = [0; ..; mu]) are skipped: same result as the oracle
+    z = np.zeros(A.dim())
+    z[40 * Ao.N:] = u[40 * Ao.N:]
+    z[-Ao.N:] = np.random.default_rng(4).uniform(-1, 1, Ao.N)
+    yz, yzo = P.apply(z), Pl.apply(z)
+    assert _rel(yz, yzo) <= 1e-12 and not np.any(yz[: 40 * Ao.N])
