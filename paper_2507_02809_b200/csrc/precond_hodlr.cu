@@ -233,6 +233,7 @@ struct HArgs {
     double* xg;          // [2][Np] x of the level (leaf siblings read it), level-tagged
     double* proj;        // [2][nnodes][2 sides][slots <= nb * 2][RK] partial projections, level-tagged
     const int* skip;
+    const unsigned* first;      // S - (the first time level with a nonzero entry of z) (0: none), or nullptr
     unsigned long long* trace;  // optional [8]: per-phase time sums of CTA 0 (FI_HODLR_TRACE=1)
     int dbg;                    // FI_HODLR_DBG experiment bits (0 in production)
     unsigned long long* ttrace; // optional [nlev][G]: globaltimer of every CTA's publish (FI_HODLR_TTRACE)
@@ -252,6 +253,23 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 constexpr int YS = 36;   // y history row stride (DMMA A-fragment loads: 2 wavefronts)
 constexpr int SGS = 36;  // segment-sum stride (16-byte aligned rows)
 __host__ __device__ inline int es_len(int nlev) { return (nlev + 24 + 1) & ~1; }
+
+// S - (the first time level of z with a nonzero entry) into *out (0 if the time levels are all zero; *out is
+// zeroed before the launch).  A thread stops at its first nonzero: four loads per thread on a dense input.
+__global__ void first_nonzero_level_kernel(const double* z, long long nt, long long Np, int S, unsigned* out) {
+    const long long st = (long long)gridDim.x * blockDim.x;
+    unsigned m = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nt && m == 0; i += 4 * st) {
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = z[min(i + q * st, nt - 1)];
+#pragma unroll
+        for (int q = 3; q >= 0; --q)
+            if (i + q * st < nt && v[q] != 0.0) m = (unsigned)(S - (int)((i + q * st) / Np));
+    }
+    for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
 
 __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
     if (a.skip && *a.skip) return;
@@ -324,6 +342,11 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
         }
         s_gfirst[DMAX + 1] = gg;
     }
+    // Leading time levels with a zero right-hand side have y = 0 (GMRES applies P^-1 to b = [0; ..; mu] first):
+    // the sweep starts at the 16-level block of the first nonzero level (8-level history blocks, level tags of
+    // period 4: the state at such a level with nothing before it is the initial state), y = 0 below it.
+    const int L0 = a.first ? max(min(S - (int)*a.first, nlev - 1), 0) & ~15 : 0;
+    for (int q = t; q < L0 * YS; q += blockDim.x) yh[q] = 0.0;
     for (int q = t; q < es_len(nlev); q += blockDim.x) es[q] = a.epad[q];
     for (int q = t; q < 8 * 8 * 32; q += blockDim.x) hpart[q] = 0.0;
     __shared__ unsigned long long s_trace[8];
@@ -390,12 +413,14 @@ __global__ void __launch_bounds__(256, 1) hodlr_sweep_kernel(HArgs a) {
             tl = now;
         }
     };
-    load_level(0, cur);
+    load_level(L0, cur);
     double cz, cd1, cdi, nz, nd1, ndi;
-    load_coef(0, cz, cd1, cdi);
+    load_coef(L0, cz, cd1, cdi);
+    if (w == 0)
+        for (int lv = 0; lv < L0; ++lv) a.y[(long long)lv * Np + row] = 0.0;
     double yprev = 0.0, hrest = 0.0;  // y of the previous level and sum_{m <= lv-2} e_{lv-m} y_m (lane's row)
     double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // old-part history (DMMA C)
-    for (int lv = 0; lv < nlev; ++lv) {
+    for (int lv = L0; lv < nlev; ++lv) {
         stamp(7);
         const int par = lv & 1;
         const unsigned tag = (unsigned)(lv >> 1) & 1u;
@@ -722,6 +747,7 @@ struct HodlrData {
     std::vector<int> depth_off, depth_cnt;  // nodes of each depth in nodes_by_depth
     DevBuf<double2> hd;                     // [levels][Np/32][16][256]
     DevBuf<double> proj, xg;
+    DevBuf<unsigned> first;                 // hodlr_sweep: S - the first nonzero time level of the input
     Tree tree() const {
         return Tree{D, nb, nnodes, rb_node.p, rb_side.p, lo.p, mid.p, hi.p};
     }
@@ -786,6 +812,7 @@ HodlrData* hodlr_create(const Layout& L, int levels) {
     h->hd.alloc((size_t)levels * (L.Np / HR) * (RK / 2) * 256);
     h->proj.alloc((size_t)2 * h->nnodes * 2 * (2 * nb) * RK);
     h->xg.alloc((size_t)2 * L.Np);
+    h->first.alloc(1);
     return h;
 }
 
@@ -899,6 +926,16 @@ void hodlr_sweep(fi_ctx* ctx, HodlrData* h, const fi_system* sys, const double* 
         trace.alloc(8);
         FI_CUDA(cudaMemsetAsync(trace.p, 0, trace.bytes(), ctx->stream));
         a.trace = trace.p;
+    }
+    a.first = nullptr;
+    static const bool zskip = !std::getenv("FI_HODLR_ZSKIP") || std::atoi(std::getenv("FI_HODLR_ZSKIP")) != 0;
+    if (zskip && !tracing && !ttfile) {
+        const int tl = std::min(levels, L.S);
+        FI_CUDA(cudaMemsetAsync(h->first.p, 0, sizeof(unsigned), ctx->stream));
+        first_nonzero_level_kernel<<<ctx->sm_count, 256, 0, ctx->stream>>>(z, (long long)tl * L.Np, L.Np, L.S,
+                                                                         h->first.p);
+        FI_LAUNCHED(ctx);
+        a.first = h->first.p;
     }
     FI_CUDA(cudaMemsetAsync(h->proj.p, 0xff, h->proj.bytes(), ctx->stream));
     FI_CUDA(cudaMemsetAsync(h->xg.p, 0xff, h->xg.bytes(), ctx->stream));
