@@ -464,6 +464,12 @@ def run_ours(args):
                 "passes_per_level": round(passes_per_level, 1),
                 "us_per_pass": round(ms_sweep * 1e3 / (S + 1) / passes_per_level, 2),
                 "inner_nonconverged": st["nonconverged_blocks"], "input": "(A - P) v0, the first Arnoldi step's",
+                # SURVEY 8(d), P-apply configs 2-4: "count the inner-solve vector traffic per level x inner
+                # iterations": a textbook PCG step touches 17 length-N vectors (B p: 2, p.Bp: 2, x: 3, r: 3,
+                # tau solve: 2, r.z: 2, p: 3); here they stay in shared memory / L2 (see `traffic`)
+                "inner_solve_vector_bytes": int(17 * 8 * N * st["cg_steps"] / applies),
+                "achieved_incl_inner_vectors": round((sweep_bytes + 17 * 8 * N * st["cg_steps"] / applies) /
+                                                     (ms_sweep * 1e-3) / 1e9, 1),
                 "note": "latency-bound: per CG step 4 grid-synchronised transform passes (rows, columns, rows, "
                         "columns) on an L2-resident working set; us_per_pass is the number to watch",
                 "peak_source": peak_src}
