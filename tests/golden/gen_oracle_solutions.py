@@ -6,7 +6,8 @@ oracle's iteration count, residual history, final true residual and recovered f.
 feed the same mu_eps to the device path and compare against these (iterations +-1, f <= 1e-8).
 1D blocks use the reference's dense LU (config 1: refactored per apply, 68.8 GB of factors do not
 fit in host RAM); 2D blocks use the substituted tau-PCG solve.
-Usage: python tests/golden/gen_oracle_solutions.py 2 3 ...   (writes tests/golden/oracle_config<i>.npz)
+Usage: python tests/golden/gen_oracle_solutions.py [--keep-observation] 2 3 4u ...
+(writes tests/golden/oracle_config<i>.npz; <i>u: the unpreconditioned solve, resumable)
 """
 import os
 import sys
@@ -29,8 +30,9 @@ def run(cfg, precond=True):
     A = O.SystemOperator(baseline_problem(O, cfg))
     P = O.BlockTriangularPreconditioner(A, cache=(cfg != 1))
     prec_file = os.path.join(HERE, f"oracle_config{cfg}.npz")
-    if not precond and os.path.exists(prec_file):
-        # the unpreconditioned solve runs on the same observation as the preconditioned golden
+    if (not precond or KEEP_OBSERVATION) and os.path.exists(prec_file):
+        # the unpreconditioned solve runs on the same observation as the preconditioned golden;
+        # --keep-observation: a regenerated golden keeps its observation (the unpreconditioned golden's input)
         mu_eps = np.load(prec_file)["mu_eps"]
     else:
         Pfs = P if P.inner == "pcg" else None
@@ -98,8 +100,10 @@ def run_unprec_resumable(cfg, maxit=2000):
                                 setup_s=0.0, solve_s=spent, inner="none")
 
 
+KEEP_OBSERVATION = "--keep-observation" in sys.argv
+
 if __name__ == "__main__":
-    for arg in sys.argv[1:]:
+    for arg in [a for a in sys.argv[1:] if not a.startswith("--")]:
         if arg.endswith("u"):
             run_unprec_resumable(int(arg[:-1]))
         else:
