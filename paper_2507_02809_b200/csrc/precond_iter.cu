@@ -5,7 +5,7 @@
 // 255^2) each block is solved instead by tau-preconditioned CG on the SPD form (
 // the oracle's TauPCG runs the identical recurrence):
 //   G_s y = r  <=>  M y = r / D2,   M = c B + diag(delta),  delta = e0 D1/D2 (f-block: c = cr, 0)
-//   tau^{-1} = S diag(1/(c g(theta) + mean(delta))) S,   S = orthonormal 2D DST-I
+//   tau^{-1} = S diag(1/(c g(theta) + hmean(delta))) S,  S = orthonormal 2D DST-I, hmean = harmonic mean
 // B x is a 2D circulant-embedded convolution (forward/inverse 2D FFT of size L1 x L2 with
 // L_i = 2(n_i + 1) a power of two); the DST-I is an odd-extended FFT of the same size.  The FFTs are
 // hand-written Stockham transforms in shared memory.
@@ -64,7 +64,7 @@ struct ItArgs {
     const double2* tw2;
     const double* lamB;  // L1 x L2 real spectrum of the embedded B
     const double* lamT;  // n1 x n2 tau eigenvalues g(theta)
-    const double* dmean; // per level mean(delta)
+    const double* dmean; // per level shift of the tau preconditioner: the harmonic mean of delta
     const int* direct;   // per level: D2 == 0 (G = e0 D1)
     const double* z_in;  // right-hand side of P (padded layout)
     double* y;           // output of P (padded layout); x of the level is y's slice
@@ -84,7 +84,7 @@ struct ItArgs {
     const int* skip;
     int warm;    // extrapolated initial guesses for the time levels (FI_TAU_WARM, default 1)
     int lswin;   // least-squares window for the guesses of the noise-dominated levels (FI_TAU_LSWIN, default 1)
-    double gmax; // largest tau eigenvalue g(theta): ||M|| is taken as c gmax + mean(delta)
+    double gmax; // largest tau eigenvalue g(theta): ||M|| is taken as c gmax + hmean(delta)
     double floor_u; // theta 2^-53: a level stops at ||r|| <= max(tol ||b||, floor_u ||M|| ||x||) (FI_TAU_FLOOR = theta)
     int cu, cus; // B column pass: adjacent columns per CTA and round (a power of two <= the groups), log2
 };
@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(FT, 1) tau_pcg_fused(ItArgs a, FusedCtl ctl) {
             dst_rows_out(rd);
         }
     };
-    // T2: tau column pass on the column pairs (k0, k0 + 1) of Rr: S1, divide by c g(theta) + mean(delta), S1
+    // T2: tau column pass on the column pairs (k0, k0 + 1) of Rr: S1, divide by c g(theta) + hmean(delta), S1
     auto passT2 = [&](int lv) {
         const double c = level_c(a, lv), dmean = level_dmean(a, lv);
         for (int rd = 0; rd < rdT; ++rd) {
@@ -1144,7 +1144,11 @@ void precond_build_iterative(fi_precond* P, double tol, int maxit) {
         throw Error(FI_E_RESOURCE, "precond_build: 2D block of " + std::to_string(N) +
                                        " unknowns needs n_i + 1 a power of two (<= 512) for the tau-PCG solve");
     const double e0 = sys->e_h[0];
-    // admissibility (as the dense path) and per-level mean(delta)
+    // admissibility (as the dense path) and the per-level shift of the tau preconditioner: the HARMONIC mean of
+    // delta = e0 D1 / D2 (0 if delta vanishes somewhere).  Where delta varies strongly (config 4: 80x) the
+    // arithmetic mean over-shifts the low frequencies, the only ones where delta matters against c g(theta):
+    // oracle CG steps per config-4 apply 2137 -> 1915 with the harmonic mean, configs 2 and 3 (delta within
+    // 3x) unchanged (DESIGN 4, K5)
     std::vector<double> d2inv((size_t)S * Np, 0.0), dmean((size_t)S + 1, 0.0);
     std::vector<int> direct((size_t)S + 1, 0);
     for (int s = 1; s <= S; ++s) {
@@ -1167,10 +1171,10 @@ void precond_build_iterative(fi_precond* P, double tol, int maxit) {
             if (d1 / d2 < 0.0)
                 throw Error(FI_E_DOMAIN, "precond_build: gamma1/gamma2 < 0 at level " + std::to_string(s));
             d2inv[(size_t)pidx] = 1.0 / d2;
-            acc += e0 * d1 / d2;
+            acc += 1.0 / (e0 * d1 / d2);  // (delta = 0: inf, harmonic mean 0)
         }
         direct[(size_t)s - 1] = all_zero ? 1 : 0;
-        dmean[(size_t)s - 1] = acc / (double)N;
+        dmean[(size_t)s - 1] = all_zero ? 0.0 : (double)N / acc;
     }
     for (long long j = 0; j < N; ++j)
         if (sys->D2_h[(size_t)(S - 1) * N + j] == 0.0)
