@@ -51,7 +51,7 @@ for s in range(1, nlev + 1):
     d1, d2 = A.diags.D1[s - 1], A.diags.D2[s - 1]
     c, delta = A.scale_space, e[0] * d1 / d2
     b = rhs / d2
-    lam = c * pcg.g + delta.mean()
+    lam = c * pcg.g + O._hmean(delta)
     M = lambda v: c * T.apply(v) + delta * v
     true_res = lambda v: float(np.linalg.norm(b.astype(np.longdouble) - (np.longdouble(c) * B_ld(v) + delta * v.astype(np.longdouble))))
     bn = np.linalg.norm(b)
