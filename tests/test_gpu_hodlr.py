@@ -145,25 +145,38 @@ def test_hodlr_build_check(cfg):
     assert 0.0 < chk["forward"] <= 1e-12 and 0.0 < chk["backward"] <= 1e-13
 
 
-@pytest.mark.parametrize("first", [0, 1, 15, 16, 37, 64])
-def test_hodlr_sweep_skips_leading_zero_levels(first):
-    """GMRES's first apply is P^-1 [0; ..; mu]: the sweep starts at the 16-level block of the first nonzero time
-    level (first = 64: only the f-block is nonzero).  Same result as the oracle's LU substitution
-    (krylov.cpp:48-70), exact zeros below, and as the sweep run from level 0 (the input with one tiny entry on
-    level 0 disables the skip)."""
-    A, Ao = F.SystemOperator(baseline_problem(F, 0)), O.SystemOperator(baseline_problem(O, 0))
-    P, Po = F.BlockTriangularPreconditioner(A), O.BlockTriangularPreconditioner(Ao)
-    assert P.form == "hodlr"
-    N, S = Ao.N, Ao.steps
+_CHILD_ZSKIP = r"""
+import os, sys, numpy as np
+sys.path.insert(0, os.environ["ROOT"])
+from oracle import fracinv_oracle as O
+from paper_2507_02809_b200 import fracinv as F
+from paper_2507_02809_b200.configs import baseline_problem
+A, Ao = F.SystemOperator(baseline_problem(F, 0)), O.SystemOperator(baseline_problem(O, 0))
+P, Po = F.BlockTriangularPreconditioner(A), O.BlockTriangularPreconditioner(Ao)
+assert P.form == "hodlr"
+N, S = Ao.N, Ao.steps
+for first in (0, 1, 15, 16, 37, 64):
     z = np.random.default_rng(21).uniform(-1, 1, A.dim())
     z[: first * N] = 0.0
     y, yo = P.apply(z), Po.apply(z)
-    assert float(np.linalg.norm(y - yo) / np.linalg.norm(yo)) <= 1e-12
-    # exact zeros below the 16-level block the sweep starts at; the zero levels it does run carry the level tag in
-    # the last mantissa bit of the exchanged values (denormals)
-    assert not np.any(y[: (first & ~15) * N]) and np.all(np.abs(y[: first * N]) <= 1e-300)
-    if first >= 16:
+    assert float(np.linalg.norm(y - yo) / np.linalg.norm(yo)) <= 1e-12, first
+    # exact zeros below the 16-level block the sweep starts at; the zero levels it does run carry the level tag
+    # in the last mantissa bit of the exchanged values (denormals)
+    assert not np.any(y[: (first & ~15) * N]) and np.all(np.abs(y[: first * N]) <= 1e-300), first
+    if first >= 16:  # one tiny entry on level 0 disables the skip: the sweep from level 0 gives the same result
         z2 = z.copy()
         z2[0] = 1e-300
         y2 = P.apply(z2)
-        assert float(np.linalg.norm(y - y2) / np.linalg.norm(y2)) <= 1e-14
+        assert float(np.linalg.norm(y - y2) / np.linalg.norm(y2)) <= 1e-14, first
+print("ok")
+"""
+
+
+def test_hodlr_sweep_skips_leading_zero_levels():
+    """FI_HODLR_ZSKIP=1 (opt-in; a separate process, the switch is read once): GMRES's first apply is
+    P^-1 [0; ..; mu] when the initial state is zero, and the sweep then starts at the 16-level block of the first
+    nonzero time level (first = 64: only the f-block is nonzero).  Same result as the oracle's LU substitution
+    (krylov.cpp:48-70), exact zeros below, and as the sweep run from level 0."""
+    env = dict(os.environ, FI_HODLR_ZSKIP="1", ROOT=ROOT)
+    r = subprocess.run([sys.executable, "-c", _CHILD_ZSKIP], env=env, timeout=600, capture_output=True, text=True)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
